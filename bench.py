@@ -1,0 +1,318 @@
+"""Benchmark: Stokes operator-apply DoF/s (fp64) on the BASELINE.json workload, with the smoother
+(fp32), the MG-FGMRES solve, the end-to-end host-buffer path, the roofline of the dominant kernel and
+the CPU baseline on this box's host cores. Prints ONE JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (configs[1] of BASELINE.json, the largest config that fits one GPU and that the metric is
+quoted on): 3D unit-cube Stokes, RT_2 velocity / DGQ_2 pressure, 64^3 cells (level 5), 28.4 M DoF.
+Each step is one fp64 operator apply y = A x; x and y are 227 MB each (> 126 MB L2), so no L2 flush
+is needed between steps. Under torchrun each rank runs the same workload on its own GPU (weak
+scaling, no data-path collective yet: the slab-partitioned multi-GPU operator is future work, see
+DESIGN.md §Multi-GPU); value = all DoF processed / max-over-ranks time.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEGREE, LEVEL = 2, 5
+METRIC = "Stokes operator-apply DoF/s (fp64), RT_2 64^3 cells; + fp32 smoother DoF/s and MG-FGMRES solve time"
+
+
+def dofs(k, level):
+    n = (2 << level) * (k + 1)
+    return 3 * (n + 1) * n * n + n ** 3
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [v.strip() for v in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(key):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)["dram_bytes_per_launch"].get(key)
+    except Exception:
+        return None
+
+
+def cpu_baseline(k, level, budget_s=12.0):
+    """The CPU oracle (restatement of the reference algorithm, Alg. 1 cell/face loops, OpenMP) timed on
+    this host on a bounded sample: level-1 of the workload (1/8 of its DoF)."""
+    import numpy as np
+
+    import oracle
+    sample_level = max(level - 1, 0)
+    n = dofs(k, sample_level)
+    x = np.random.default_rng(0).uniform(-1, 1, n)
+    oracle.apply_stokes(k, sample_level, x)  # warm-up (tables)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.apply_stokes(k, sample_level, x)
+        reps += 1
+        if time.perf_counter() - t0 >= budget_s or reps >= 50:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n * reps / dt, "unit": "DoF/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"oracle Alg.1 vmult fp64 at k={k}, level {sample_level} ({2 << sample_level}^3 cells, {n} DoF),"
+                      f" {reps} reps in {dt:.1f}s, OpenMP all host threads"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    k, level = args.degree, args.level
+    sample_level = max(level - 1, 0)
+    n = dofs(k, sample_level)
+    x = np.random.default_rng(0).uniform(-1, 1, n)
+    for _ in range(args.warmup):
+        oracle.apply_stokes(k, sample_level, x)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.apply_stokes(k, sample_level, x)
+    dt = time.perf_counter() - t0
+    value = n * args.steps / dt
+    sample = (f"reference CPU path (oracle restatement; the reference ships no code for this path) vmult fp64, "
+              f"k={k}, level {sample_level} ({n} DoF) per step, all {os.cpu_count()} host threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C2 sample: RT_{k} {2 << sample_level}^3 cells (1/8 of the 64^3 workload)",
+                   "degree": k, "level": sample_level, "dofs": n},
+        "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": os.cpu_count(), "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--degree", type=int, default=DEGREE)
+    ap.add_argument("--level", type=int, default=LEVEL)
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2410_09497_b200 as smg
+
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    k, level = args.degree, args.level
+    N = dofs(k, level)
+    ctx = smg.Context(k, level, device=local, cg_max_iter=30, cg_tol=1e-5, cg_fixed=False, cg_precond=1)
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    x = torch.rand(N, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    # ---- headline: fp64 vmult, inputs resident in HBM ----
+    for _ in range(args.warmup):
+        ctx.apply_stokes(level, x, out=y)
+    barrier()
+    l0 = ctx.launch_count
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            ctx.apply_stokes(level, x, out=y)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.launch_count - l0
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = N * world / (ms * 1e-3)
+
+    # ---- fp32 vmult ----
+    x32 = x.float()
+    y32 = torch.empty_like(x32)
+    for _ in range(args.warmup):
+        ctx.apply_stokes(level, x32, out=y32)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        ctx.apply_stokes(level, x32, out=y32)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms32 = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+
+    # ---- fp32 smoothing step (8 colours: residual + patch solve each) ----
+    b32 = ctx.apply_stokes(level, x32)
+    xs = torch.zeros_like(b32)
+    ctx.smooth(level, xs, b32, zero_init=True)
+    torch.cuda.synchronize()
+    nsm = max(1, min(args.steps, 3))
+    ev0.record(stream)
+    for _ in range(nsm):
+        ctx.smooth(level, xs, b32, zero_init=False)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms_smooth = max_over_ranks(ev0.elapsed_time(ev1) / nsm)
+
+    # ---- MG-FGMRES solve (mixed precision: fp64 Krylov, fp32 V-cycle) ----
+    solve = None
+    if not args.no_solve:
+        b = ctx.apply_stokes(level, x)
+        ctx.solve(level, b, 1e-8, 30, smg.F32, allow_not_converged=True)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        xsol, it, hist = ctx.solve(level, b, 1e-8, 30, smg.F32, allow_not_converged=True)
+        torch.cuda.synchronize()
+        ts = max_over_ranks(time.perf_counter() - t0)
+        nu = -8.0 / np.log10((hist[-1] / hist[0]) ** (1.0 / it)) if it > 0 and hist[-1] > 0 else None
+        solve = {"iterations": it, "rel_residual": float(hist[-1] / hist[0]), "fractional_count_nu": nu,
+                 "time_s": ts, "ns_per_dof": ts / N * 1e9, "tol": 1e-8, "precision": "fp64 FGMRES + fp32 V-cycle"}
+
+    # ---- e2e: host BlockVector buffers through the C ABI, copies inside the timed region ----
+    s = ctx.sizes(level)
+    xb = [torch.empty(s[i], dtype=torch.float64, pin_memory=True) for i in range(4)]
+    yb = [torch.empty(s[i], dtype=torch.float64, pin_memory=True) for i in range(4)]
+    off = 0
+    xh = x.cpu()
+    for i in range(4):
+        xb[i].copy_(xh[off:off + s[i]])
+        off += s[i]
+    xbn, ybn = [t.numpy() for t in xb], [t.numpy() for t in yb]
+    for _ in range(args.warmup):
+        ctx.vmult_host(level, xbn, smg.F64, out=ybn)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.vmult_host(level, xbn, smg.F64, out=ybn)
+    te = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    e2e = {"value": N * world / te, "unit": "DoF/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = measured_peaks()
+    bytes_per_launch = 16 * N  # algorithmic: read x + write y, fp64
+    achieved = bytes_per_launch / (ms * 1e-3) / 1e9
+    traffic = ncu_traffic(f"k{k}_l{level}_f64")
+    cpu = None if args.no_cpu else cpu_baseline(k, level)
+    out = {
+        "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C2: 3D unit-cube Stokes RT_{k}/DGQ_{k}, {2 << level}^3 cells (level {level}), "
+                               f"fp64 operator apply", "degree": k, "level": level, "dofs": N,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (x, y 227 MB each vs 126 MB L2); no flush"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_per_launch, "kernel": "stokes_vmult_kernel<double,2,4,4,4>"},
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+        "fp32_vmult": {"value": N * world / (ms32 * 1e-3), "unit": "DoF/s", "ms": ms32},
+        "smoother_fp32": {"value": N * world / (ms_smooth * 1e-3), "unit": "DoF/s", "ms_per_step": ms_smooth,
+                          "ns_per_dof": ms_smooth * 1e6 / N},
+        "solve": solve,
+    }
+    print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,106 @@
+/* smg_b200.h — C ABI of the B200-native hot path of arXiv 2410.09497 (matrix-free multigrid for the
+ * H(div)-DG Stokes problem): Stokes operator vmult, vertex-patch Schur/fast-diagonalisation smoother,
+ * intergrid transfer, level vectors, and the V-cycle / mixed-precision FGMRES driver built on them.
+ *
+ * The reference (/root/reference) ships no code for this path: its interfaces exist as SPEC.md
+ * operation signatures plus the BlockVector<dim,T> type (proj/include/stokesmg/block_vector.hpp:15-93).
+ * Each entry point below names the reference operation it replaces. Conventions:
+ *   - plain pointers and sizes only; no C++ or torch types cross this boundary;
+ *   - every call returns an int status (SMG_OK or a negative SMG_E* code); smg_last_error() gives text.
+ *     The reference signals errors with std::invalid_argument (mesh.hpp:31-34, fem1d.hpp:95-96);
+ *     the C++ wrapper (paper_2410_09497_b200/host/stokesmg_b200.hpp) rethrows them as such;
+ *   - device-vector entry points take DEVICE pointers to one contiguous level vector in the stored
+ *     layout [u_x | u_y | u_z | p]; *_host entry points take HOST arrays in
+ *     the BlockVector layout (3 velocity arrays + pressure, block_vector.hpp:17-18) and copy;
+ *   - all device work is ordered on the context's stream (smg_set_stream); calls that return host
+ *     scalars (dot, norms, solve) synchronise that stream;
+ *   - a context is not re-entrant: one host thread per context.
+ * There is no CPU fallback: without a usable sm_100 device smg_create fails with SMG_ECUDA.
+ */
+#ifndef SMG_B200_H
+#define SMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMG_OK 0
+#define SMG_EINVAL (-22)   /* std::invalid_argument in the reference */
+#define SMG_ECUDA (-100)   /* CUDA runtime / launch failure */
+#define SMG_ENOTCONV (-101) /* Krylov did not converge within max_iter */
+#define SMG_ENOMEM (-12)
+
+#define SMG_F64 0
+#define SMG_F32 1
+
+typedef struct smg_context smg_context;
+
+typedef struct {
+  int degree;        /* RT_k velocity / DGQ_k pressure, k >= 1 */
+  int max_level;     /* finest level L; level l has 2^(l+1) cells per direction (mesh.hpp:21) */
+  int device;        /* CUDA device ordinal */
+  int cg_max_iter;   /* patch Schur-CG cap */
+  double cg_tol;     /* patch Schur-CG relative tolerance */
+  int cg_fixed;      /* 1: exactly cg_max_iter iterations (parity mode) */
+  int cg_precond;    /* 0: none (SPEC-literal), 1: pressure-mass preconditioned (default) */
+} smg_config;
+
+/* ---- context (replaces the reference's per-level setup: build_hierarchy mesh.hpp:30-36, the 1D
+ *      matrix cache SPEC.md:157, fast_diag_prepare SPEC.md:338, coarse pseudo-inverse SPEC.md:468) */
+int smg_config_default(smg_config* cfg);
+int smg_create(const smg_config* cfg, smg_context** ctx);
+int smg_destroy(smg_context* ctx);
+int smg_set_stream(smg_context* ctx, void* cuda_stream); /* NULL = legacy default stream */
+const char* smg_last_error(const smg_context* ctx);
+/* number of CUDA kernels this context has launched so far (evidence counter for benchmarks) */
+int64_t smg_launch_count(const smg_context* ctx);
+
+/* ---- level layout (DoFLayout; BlockVector sizes block_vector.hpp:21-24) ---- */
+/* sizes[0..2] velocity component blocks, sizes[3] pressure, sizes[4] total stored DoFs */
+int smg_level_sizes(int degree, int level, int64_t sizes[5]);
+
+/* ---- level vectors (device) ---- */
+int smg_vec_alloc(smg_context* ctx, int level, int precision, void** dptr);
+int smg_vec_free(smg_context* ctx, void* dptr);
+
+/* ---- operator: y = A x, A = [[A, B^T],[B, 0]] (apply_stokes; Alg. 1)
+ *      constrained (boundary-normal) rows of y are zero; constrained entries of x are ignored. */
+int smg_vmult(smg_context* ctx, int level, int precision, void* y, const void* x);
+/* r = b - A x (the residual of SPEC.md:424 / v_cycle SPEC.md:462) */
+int smg_residual(smg_context* ctx, int level, int precision, void* r, const void* b, const void* x);
+
+/* ---- smoother: one colour-by-colour multiplicative vertex-patch step on x (smooth SPEC.md:400-408,
+ *      Alg. 2, local solver schur_solve SPEC.md:356-364). zero_init: x := 0 first. */
+int smg_smooth(smg_context* ctx, int level, int precision, void* x, const void* b, int zero_init);
+
+/* ---- transfer (prolongate / restrict SPEC.md:441-458): x_f += P x_c ;  r_c = P^T r_f ---- */
+int smg_prolongate_add(smg_context* ctx, int coarse_level, int precision, void* x_fine, const void* x_coarse);
+int smg_restrict(smg_context* ctx, int coarse_level, int precision, void* r_coarse, const void* r_fine);
+/* level-0 pseudo-inverse apply (coarse_solve SPEC.md:468-476) */
+int smg_coarse_solve(smg_context* ctx, int precision, void* x, const void* b);
+
+/* ---- multigrid / Krylov callers (v_cycle SPEC.md:459-467; fgmres/solve_mixed SPEC.md:507-533) ---- */
+int smg_vcycle(smg_context* ctx, int level, int precision, void* x, const void* b);
+/* FGMRES(apply_A = fp64 vmult, apply_P = V-cycle in `vcycle_precision`) from x0 = 0; x, b fp64 device.
+ * iters (out), history (out, max_iter+1 residual norms, may be NULL). Returns SMG_ENOTCONV if the
+ * relative residual did not reach rel_tol. */
+int smg_solve(smg_context* ctx, int level, void* x, const void* b, double rel_tol, int max_iter,
+              int vcycle_precision, int* iters, double* history);
+
+/* ---- BLAS-1 on level vectors (block_vector.hpp:52-93); dots accumulate in fp64 ---- */
+int smg_dot(smg_context* ctx, int level, int precision, const void* a, const void* b, double* out);
+int smg_axpy(smg_context* ctx, int level, int precision, double alpha, const void* x, void* y);
+int smg_convert(smg_context* ctx, int level, int dst_precision, void* dst, int src_precision, const void* src);
+
+/* ---- host-buffer entry points in the BlockVector layout (reference-facing e2e path) ---- */
+int smg_vmult_host(smg_context* ctx, int level, int precision, void* const y_vel[3], void* y_p,
+                   const void* const x_vel[3], const void* x_p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMG_B200_H */

@@ -1,0 +1,277 @@
+"""B200-native hot path of arXiv 2410.09497 (matrix-free multigrid for the H(div)-DG Stokes problem).
+
+Python mirror of the reference's operator / smoother / transfer interface (SPEC.md: apply_stokes,
+smooth, prolongate, restrict, v_cycle, fgmres/solve_mixed; BlockVector block_vector.hpp:15-93) over the
+C ABI of libsmg_b200.so (include/smg_b200.h). Device vectors are torch CUDA tensors holding one level
+vector in the stored layout [u_x | u_y | u_z | p]; torch is used only for device memory and
+streams. There is no CPU fallback: if the CUDA library is missing or no sm_100 device is present,
+constructing a Context raises.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBPATH = os.path.join(_HERE, "libsmg_b200.so")
+_LIB = None
+
+SMG_OK, SMG_EINVAL, SMG_ECUDA, SMG_ENOTCONV, SMG_ENOMEM = 0, -22, -100, -101, -12
+F64, F32 = 0, 1
+
+EXPORTED = [
+    "smg_config_default", "smg_create", "smg_destroy", "smg_set_stream", "smg_last_error", "smg_launch_count",
+    "smg_level_sizes", "smg_vec_alloc", "smg_vec_free", "smg_vmult", "smg_residual", "smg_smooth",
+    "smg_prolongate_add", "smg_restrict", "smg_coarse_solve", "smg_vcycle", "smg_solve", "smg_dot", "smg_axpy",
+    "smg_convert", "smg_vmult_host",
+]
+
+
+class SmgConfig(ctypes.Structure):
+    _fields_ = [("degree", ctypes.c_int), ("max_level", ctypes.c_int), ("device", ctypes.c_int),
+                ("cg_max_iter", ctypes.c_int), ("cg_tol", ctypes.c_double), ("cg_fixed", ctypes.c_int),
+                ("cg_precond", ctypes.c_int)]
+
+
+class SmgError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"smg error {code}: {msg}")
+        self.code = code
+
+
+class NotConverged(SmgError):
+    pass
+
+
+def build(force=False):
+    """Compile libsmg_b200.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    if force or not os.path.exists(_LIBPATH):
+        subprocess.check_call(["make", "-s", "-j8", "-C", _HERE])
+    else:
+        subprocess.check_call(["make", "-s", "-j8", "-C", _HERE])
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(_LIBPATH):
+            raise RuntimeError(f"{_LIBPATH} is missing: run paper_2410_09497_b200.build() (no CPU fallback)")
+        L = ctypes.CDLL(_LIBPATH)
+        P, I, D, I64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64
+        L.smg_last_error.restype = ctypes.c_char_p
+        L.smg_last_error.argtypes = [P]
+        L.smg_launch_count.restype = I64
+        L.smg_launch_count.argtypes = [P]
+        L.smg_create.argtypes = [ctypes.POINTER(SmgConfig), ctypes.POINTER(P)]
+        L.smg_destroy.argtypes = [P]
+        L.smg_set_stream.argtypes = [P, P]
+        L.smg_level_sizes.argtypes = [I, I, P]
+        L.smg_vmult.argtypes = [P, I, I, P, P]
+        L.smg_residual.argtypes = [P, I, I, P, P, P]
+        L.smg_smooth.argtypes = [P, I, I, P, P, I]
+        L.smg_prolongate_add.argtypes = [P, I, I, P, P]
+        L.smg_restrict.argtypes = [P, I, I, P, P]
+        L.smg_coarse_solve.argtypes = [P, I, P, P]
+        L.smg_vcycle.argtypes = [P, I, I, P, P]
+        L.smg_solve.argtypes = [P, I, P, P, D, I, I, ctypes.POINTER(I), P]
+        L.smg_dot.argtypes = [P, I, I, P, P, ctypes.POINTER(D)]
+        L.smg_axpy.argtypes = [P, I, I, D, P, P]
+        L.smg_convert.argtypes = [P, I, I, P, I, P]
+        L.smg_vmult_host.argtypes = [P, I, I, P, P, P, P]
+        _LIB = L
+    return _LIB
+
+
+def level_sizes(degree, level):
+    s = (ctypes.c_int64 * 5)()
+    rc = lib().smg_level_sizes(degree, level, s)
+    if rc != SMG_OK:
+        raise ValueError(f"invalid degree/level ({degree}, {level})")
+    return [int(v) for v in s]
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Context:
+    """One B200 context for a mesh hierarchy of degree `degree` up to `max_level`.
+
+    Mirrors the reference's per-level operator / smoother / transfer objects (SPEC.md modules
+    stokes_op, smoother, multigrid, solver). Methods take torch CUDA tensors (float64 = SMG_F64,
+    float32 = SMG_F32) in the stored level layout and launch on torch's current CUDA stream.
+    """
+
+    def __init__(self, degree, max_level, device=0, cg_max_iter=30, cg_tol=1e-8, cg_fixed=False, cg_precond=1):
+        import torch
+        self._torch = torch
+        cfg = SmgConfig(degree, max_level, device, cg_max_iter, cg_tol, int(cg_fixed), int(cg_precond))
+        h = ctypes.c_void_p()
+        rc = lib().smg_create(ctypes.byref(cfg), ctypes.byref(h))
+        if rc != SMG_OK:
+            msg = lib().smg_last_error(None).decode()
+            if rc == SMG_EINVAL:
+                raise ValueError(msg)
+            raise SmgError(rc, msg)
+        self._h = h
+        self.degree, self.max_level, self.device = degree, max_level, device
+        self._stream = None
+        self._sync_stream()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().smg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- plumbing ----
+    def _sync_stream(self):
+        s = self._torch.cuda.current_stream(self.device).cuda_stream
+        if s != self._stream:
+            self._check(lib().smg_set_stream(self._h, ctypes.c_void_p(s)))
+            self._stream = s
+
+    def _check(self, rc):
+        if rc == SMG_OK:
+            return
+        msg = lib().smg_last_error(self._h).decode()
+        if rc == SMG_EINVAL:
+            raise ValueError(msg)
+        if rc == SMG_ENOTCONV:
+            raise NotConverged(rc, msg)
+        raise SmgError(rc, msg)
+
+    def _prec(self, t):
+        torch = self._torch
+        if not t.is_cuda:
+            raise ValueError("device vectors must be CUDA tensors (use vmult_host for host buffers)")
+        if not t.is_contiguous():
+            raise ValueError("device vectors must be contiguous")
+        if t.dtype == torch.float64:
+            return F64
+        if t.dtype == torch.float32:
+            return F32
+        raise ValueError("dtype must be float64 or float32")
+
+    def _check_size(self, t, level):
+        if t.numel() != self.sizes(level)[4]:
+            raise ValueError(f"vector has {t.numel()} entries, level {level} needs {self.sizes(level)[4]}")
+
+    def sizes(self, level):
+        return level_sizes(self.degree, level)
+
+    def new_vector(self, level, dtype=None):
+        torch = self._torch
+        return torch.zeros(self.sizes(level)[4], dtype=dtype or torch.float64, device=f"cuda:{self.device}")
+
+    @property
+    def launch_count(self):
+        return int(lib().smg_launch_count(self._h))
+
+    # ---- hot path ----
+    def apply_stokes(self, level, x, out=None):
+        """y = A x (apply_stokes)."""
+        p = self._prec(x)
+        self._check_size(x, level)
+        y = self._torch.empty_like(x) if out is None else out
+        self._sync_stream()
+        self._check(lib().smg_vmult(self._h, level, p, _ptr(y), _ptr(x)))
+        return y
+
+    vmult = apply_stokes
+
+    def residual(self, level, b, x, out=None):
+        p = self._prec(x)
+        r = self._torch.empty_like(x) if out is None else out
+        self._sync_stream()
+        self._check(lib().smg_residual(self._h, level, p, _ptr(r), _ptr(b), _ptr(x)))
+        return r
+
+    def smooth(self, level, x, b, zero_init=False):
+        """one multiplicative colour-by-colour vertex-patch step, in place on x."""
+        p = self._prec(x)
+        self._sync_stream()
+        self._check(lib().smg_smooth(self._h, level, p, _ptr(x), _ptr(b), int(zero_init)))
+        return x
+
+    def prolongate_add(self, coarse_level, x_fine, x_coarse):
+        p = self._prec(x_fine)
+        self._sync_stream()
+        self._check(lib().smg_prolongate_add(self._h, coarse_level, p, _ptr(x_fine), _ptr(x_coarse)))
+        return x_fine
+
+    def restrict(self, coarse_level, r_fine, out=None):
+        p = self._prec(r_fine)
+        rc = out if out is not None else self._torch.zeros(self.sizes(coarse_level)[4], dtype=r_fine.dtype,
+                                                           device=r_fine.device)
+        self._sync_stream()
+        self._check(lib().smg_restrict(self._h, coarse_level, p, _ptr(rc), _ptr(r_fine)))
+        return rc
+
+    def coarse_solve(self, b):
+        p = self._prec(b)
+        x = self._torch.zeros_like(b)
+        self._sync_stream()
+        self._check(lib().smg_coarse_solve(self._h, p, _ptr(x), _ptr(b)))
+        return x
+
+    def vcycle(self, level, b):
+        p = self._prec(b)
+        x = self._torch.zeros_like(b)
+        self._sync_stream()
+        self._check(lib().smg_vcycle(self._h, level, p, _ptr(x), _ptr(b)))
+        return x
+
+    def solve(self, level, b, rel_tol=1e-8, max_iter=50, vcycle_precision=F32, allow_not_converged=False):
+        """MG-preconditioned FGMRES (solve_mixed SPEC.md:525-533). Returns (x, iterations, history)."""
+        if self._prec(b) != F64:
+            raise ValueError("solve expects a float64 right-hand side")
+        x = self._torch.zeros_like(b)
+        it = ctypes.c_int()
+        hist = np.zeros(max_iter + 1)
+        self._sync_stream()
+        rc = lib().smg_solve(self._h, level, _ptr(x), _ptr(b), rel_tol, max_iter, vcycle_precision,
+                             ctypes.byref(it), hist.ctypes.data_as(ctypes.c_void_p))
+        if rc == SMG_ENOTCONV and allow_not_converged:
+            rc = SMG_OK
+        self._check(rc)
+        return x, it.value, hist[: it.value + 1]
+
+    def dot(self, level, a, b):
+        out = ctypes.c_double()
+        self._sync_stream()
+        self._check(lib().smg_dot(self._h, level, self._prec(a), _ptr(a), _ptr(b), ctypes.byref(out)))
+        return out.value
+
+    def vmult_host(self, level, x_blocks, precision=F64, out=None):
+        """Reference-facing path: host arrays in the BlockVector layout (3 velocity + pressure) in,
+        host arrays out; host<->device copies included (block_vector.hpp:17-18)."""
+        dt = np.float64 if precision == F64 else np.float32
+        s = self.sizes(level)
+        xs = [np.ascontiguousarray(a, dtype=dt) for a in x_blocks]
+        for i in range(4):
+            if xs[i].size != s[i]:
+                raise ValueError("block sizes do not match the level layout")
+        ys = out if out is not None else [np.empty(s[i], dtype=dt) for i in range(4)]
+        for i in range(4):
+            if ys[i].size != s[i] or ys[i].dtype != dt or not ys[i].flags.c_contiguous:
+                raise ValueError("output blocks do not match the level layout")
+        xv = (ctypes.c_void_p * 3)(*[a.ctypes.data for a in xs[:3]])
+        yv = (ctypes.c_void_p * 3)(*[a.ctypes.data for a in ys[:3]])
+        self._sync_stream()
+        self._check(lib().smg_vmult_host(self._h, level, precision, yv, ctypes.c_void_p(ys[3].ctypes.data), xv,
+                                         ctypes.c_void_p(xs[3].ctypes.data)))
+        return ys
+
+
+def split_blocks(v, degree, level):
+    """Split a stored level vector into the BlockVector blocks (u_x, u_y, u_z, p)."""
+    s = level_sizes(degree, level)
+    o = np.cumsum([0] + s[:4])
+    return [v[o[i]:o[i + 1]] for i in range(4)]

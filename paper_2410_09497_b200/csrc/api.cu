@@ -1,0 +1,580 @@
+// C ABI of libsmg_b200.so (include/smg_b200.h): context setup, level vectors, operator / smoother /
+// transfer entry points, and the caller side of the hot path — the V-cycle (v_cycle SPEC.md:459-467)
+// and the mixed-precision flexible GMRES (fgmres / solve_mixed SPEC.md:507-533) — driving the sm_100a
+// kernels from the host. No CPU fallback: every numeric operation runs on the device.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "smg_internal.cuh"
+
+namespace smg {
+
+std::vector<double> pack_patch_tables(const PatchTables& P);  // smoother.cu
+
+namespace {
+
+void* dev_upload(Context& c, const std::vector<double>& v, int prec) {
+  void* d = nullptr;
+  const size_t n = v.size();
+  SMG_CUDA(cudaMalloc(&d, std::max<size_t>(n, 1) * elem_size(prec)));
+  c.allocations.push_back(d);
+  if (prec == SMG_F64) {
+    SMG_CUDA(cudaMemcpy(d, v.data(), n * 8, cudaMemcpyHostToDevice));
+  } else {
+    std::vector<float> f(v.begin(), v.end());
+    SMG_CUDA(cudaMemcpy(d, f.data(), n * 4, cudaMemcpyHostToDevice));
+  }
+  return d;
+}
+
+// Dense global 1D operator (rows x cols) from the cell-row blocks of LevelTables.
+Dense global1d(const LevelTables& T, int op, bool par_rows, bool par_cols) {
+  const int H = T.k + 1, n = T.m * H;
+  const int rows = par_rows ? n + 1 : n, cols = par_cols ? n + 1 : n;
+  const int nb = par_cols ? H + 1 : H;
+  Dense A(rows, cols);
+  LevelTables& W = const_cast<LevelTables&>(T);
+  for (int e = 0; e < T.m; ++e) {
+    const int var = e == 0 ? 0 : (e == T.m - 1 ? 2 : 1);
+    for (int d = -1; d <= 1; ++d) {
+      if (e + d < 0 || e + d >= T.m) continue;
+      for (int a = 0; a < H; ++a)
+        for (int b = 0; b < nb; ++b) A(e * H + a, (e + d) * H + b) += W.w(op, var, d, a, b);
+    }
+  }
+  return A;
+}
+
+// Level-0 pseudo-inverse (coarse_solve SPEC.md:468-476): dense A_0 on the free DoFs from the
+// Kronecker factors, then the leading block of the inverse of [[A, e],[e^T, 0]] with e the constant
+// pressure vector — equal to A^+ for symmetric A with ker A = span(e).
+void setup_coarse(Context& c) {
+  const LevelTables& T = c.tables[0];
+  const LevelLayout lay(c.cfg.degree, 0);
+  const int n = lay.n;
+  const Dense MO = global1d(T, OP_MO, false, false), LO = global1d(T, OP_LO, false, false);
+  const Dense MP = global1d(T, OP_MP, true, true), LP = global1d(T, OP_LP, true, true);
+  const Dense D = global1d(T, OP_D, false, true);  // n x (n+1)
+  std::vector<int64_t> fr;
+  for (int comp = 0; comp < 3; ++comp)
+    for (int64_t z = 0; z < lay.dims[comp][2]; ++z)
+      for (int64_t y = 0; y < lay.dims[comp][1]; ++y)
+        for (int64_t x = 0; x < lay.dims[comp][0]; ++x) {
+          const int64_t g[3] = {x, y, z};
+          if (g[comp] == 0 || g[comp] == n) continue;
+          fr.push_back(lay.off[comp] + (z * lay.dims[comp][1] + y) * lay.dims[comp][0] + x);
+        }
+  for (int64_t i = 0; i < lay.size[3]; ++i) fr.push_back(lay.off[3] + i);
+  const int nf = static_cast<int>(fr.size());
+  // decode stored index -> (block, coords)
+  auto decode = [&](int64_t idx, int& blk, int* g) {
+    blk = 3;
+    for (int b = 0; b < 3; ++b)
+      if (idx >= lay.off[b] && idx < lay.off[b + 1]) blk = b;
+    const int64_t l = idx - lay.off[blk];
+    const int64_t d0 = blk < 3 ? lay.dims[blk][0] : n, d1 = blk < 3 ? lay.dims[blk][1] : n;
+    g[0] = static_cast<int>(l % d0);
+    g[1] = static_cast<int>((l / d0) % d1);
+    g[2] = static_cast<int>(l / (d0 * d1));
+  };
+  Dense K(nf + 1, nf + 1);
+  std::vector<int> blk(nf);
+  std::vector<int> co(3 * nf);
+  for (int i = 0; i < nf; ++i) decode(fr[i], blk[i], &co[3 * i]);
+  for (int i = 0; i < nf; ++i)
+    for (int j = 0; j < nf; ++j) {
+      const int bi = blk[i], bj = blk[j];
+      const int* gi = &co[3 * i];
+      const int* gj = &co[3 * j];
+      double v = 0.0;
+      if (bi < 3 && bj == bi) {
+        // Kronecker sum: sum_d L_d (x) M_others, par factors along axis bi
+        for (int d = 0; d < 3; ++d) {
+          double t = 1.0;
+          for (int a = 0; a < 3 && t != 0.0; ++a) {
+            const bool par = (a == bi);
+            const Dense& Mm = par ? MP : MO;
+            const Dense& Ll = par ? LP : LO;
+            t *= (a == d ? Ll : Mm)(gi[a], gj[a]);
+          }
+          v += t;
+        }
+      } else if (bi == 3 && bj < 3) {
+        double t = 1.0;
+        for (int a = 0; a < 3; ++a) t *= (a == bj ? D(gi[a], gj[a]) : MO(gi[a], gj[a]));
+        v = t;
+      } else if (bi < 3 && bj == 3) {
+        double t = 1.0;
+        for (int a = 0; a < 3; ++a) t *= (a == bi ? D(gj[a], gi[a]) : MO(gj[a], gi[a]));
+        v = t;
+      }
+      K(i, j) = v;
+    }
+  for (int i = 0; i < nf; ++i)
+    if (blk[i] == 3) K(i, nf) = K(nf, i) = 1.0;
+  const Dense Ki = inverse(K);
+  std::vector<double> pinv(static_cast<size_t>(nf) * nf);
+  for (int i = 0; i < nf; ++i)
+    for (int j = 0; j < nf; ++j) pinv[static_cast<size_t>(i) * nf + j] = 0.5 * (Ki(i, j) + Ki(j, i));
+  c.coarse_free = fr;
+  c.coarse_pinv[0] = dev_upload(c, pinv, SMG_F64);
+  c.coarse_pinv[1] = dev_upload(c, pinv, SMG_F32);
+  void* d = nullptr;
+  SMG_CUDA(cudaMalloc(&d, fr.size() * sizeof(int64_t)));
+  c.allocations.push_back(d);
+  SMG_CUDA(cudaMemcpy(d, fr.data(), fr.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  c.coarse_free_dev = d;
+}
+
+void* alloc_vec(Context& c, int level, int prec) {
+  void* d = nullptr;
+  SMG_CUDA(cudaMalloc(&d, c.dev[0][level].lay.total * elem_size(prec)));
+  c.allocations.push_back(d);
+  return d;
+}
+
+void ensure_work(Context& c, int prec) {
+  if (!c.work_r[prec].empty()) return;
+  const int L = c.cfg.max_level;
+  c.work_r[prec].assign(L + 1, nullptr);
+  c.work_x[prec].assign(L + 1, nullptr);
+  c.work_b[prec].assign(L + 1, nullptr);
+  for (int l = 0; l <= L; ++l) {
+    c.work_r[prec][l] = alloc_vec(c, l, prec);
+    c.work_x[prec][l] = alloc_vec(c, l, prec);
+    c.work_b[prec][l] = alloc_vec(c, l, prec);
+  }
+}
+
+void check_level(const Context& c, int level) {
+  if (level < 0 || level > c.cfg.max_level) throw std::invalid_argument("level out of range");
+}
+
+void smooth(Context& c, int level, int prec, void* x, const void* b) {
+  ensure_work(c, prec);
+  void* r = c.work_r[prec][level];
+  for (int col = 0; col < 8; ++col) {
+    launch_vmult(c, level, prec, r, x, b);
+    launch_smooth_colour(c, level, prec, col, x, r);
+  }
+}
+
+void vcycle(Context& c, int level, int prec, void* x, const void* b) {
+  if (level == 0) {
+    launch_coarse_apply(c, prec, x, b);
+    return;
+  }
+  ensure_work(c, prec);
+  const int64_t N = c.dev[0][level].lay.total;
+  launch_zero(c, N, prec, x);
+  smooth(c, level, prec, x, b);
+  void* r = c.work_r[prec][level];
+  void* bc = c.work_b[prec][level - 1];
+  void* xc = c.work_x[prec][level - 1];
+  launch_vmult(c, level, prec, r, x, b);
+  launch_restrict(c, level - 1, prec, bc, r);
+  vcycle(c, level - 1, prec, xc, bc);
+  launch_prolongate_add(c, level - 1, prec, x, xc);
+  smooth(c, level, prec, x, b);
+}
+
+// FGMRES, right-preconditioned, no restart, MGS + one re-orthogonalisation pass, x0 = 0
+// (SPEC.md:507-515, 549-550); the V-cycle runs in `vp` precision with conversion at its boundary
+// (SPEC.md:528).
+int fgmres(Context& c, int level, double* x, const double* b, double tol, int max_iter, int vp, int* iters,
+           double* hist) {
+  const int64_t N = c.dev[0][level].lay.total;
+  std::vector<double*> V, Z, owned;
+  struct Guard {
+    std::vector<double*>* v;
+    ~Guard() {
+      for (double* p : *v) cudaFree(p);
+    }
+  } guard{&owned};
+  auto newvec = [&]() {
+    void* d = nullptr;
+    SMG_CUDA(cudaMalloc(&d, N * sizeof(double)));
+    owned.push_back(static_cast<double*>(d));
+    return static_cast<double*>(d);
+  };
+  void *vb = nullptr, *vx = nullptr;
+  if (vp == SMG_F32) ensure_work(c, SMG_F32);
+  std::vector<std::vector<double>> H(max_iter + 1, std::vector<double>(max_iter, 0.0));
+  std::vector<double> cs(max_iter, 0.0), sn(max_iter, 0.0), g(max_iter + 1, 0.0);
+  launch_zero(c, N, SMG_F64, x);
+  const double beta = std::sqrt(dot(c, N, SMG_F64, b, b));
+  if (hist) hist[0] = beta;
+  int it = 0;
+  if (beta == 0.0) {
+    if (iters) *iters = 0;
+    return SMG_OK;
+  }
+  V.push_back(newvec());
+  launch_convert(c, N, SMG_F64, V[0], SMG_F64, b);
+  launch_scale(c, N, SMG_F64, 1.0 / beta, V[0]);
+  g[0] = beta;
+  double* w = newvec();
+  bool converged = false;
+  for (; it < max_iter;) {
+    const int j = it;
+    Z.push_back(newvec());
+    if (vp == SMG_F64) {
+      vcycle(c, level, SMG_F64, Z[j], V[j]);
+    } else {
+      // fp64 -> fp32 at the V-cycle boundary; the top-level scratch of the fp32 hierarchy holds b and x
+      vb = c.work_b[SMG_F32][level];
+      vx = c.work_x[SMG_F32][level];
+      launch_convert(c, N, SMG_F32, vb, SMG_F64, V[j]);
+      vcycle(c, level, SMG_F32, vx, vb);
+      launch_convert(c, N, SMG_F64, Z[j], SMG_F32, vx);
+    }
+    launch_vmult(c, level, SMG_F64, w, Z[j], nullptr);
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i = 0; i <= j; ++i) {
+        const double hij = dot(c, N, SMG_F64, w, V[i]);
+        H[i][j] += hij;
+        launch_axpy(c, N, SMG_F64, -hij, V[i], w);
+      }
+    const double wn = std::sqrt(dot(c, N, SMG_F64, w, w));
+    H[j + 1][j] = wn;
+    for (int i = 0; i < j; ++i) {
+      const double t = cs[i] * H[i][j] + sn[i] * H[i + 1][j];
+      H[i + 1][j] = -sn[i] * H[i][j] + cs[i] * H[i + 1][j];
+      H[i][j] = t;
+    }
+    const double den = std::hypot(H[j][j], H[j + 1][j]);
+    cs[j] = H[j][j] / den;
+    sn[j] = H[j + 1][j] / den;
+    H[j][j] = den;
+    H[j + 1][j] = 0.0;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    ++it;
+    if (hist) hist[it] = std::fabs(g[j + 1]);
+    if (std::fabs(g[j + 1]) <= tol * beta || wn == 0.0) {
+      converged = true;
+      break;
+    }
+    V.push_back(newvec());
+    launch_convert(c, N, SMG_F64, V.back(), SMG_F64, w);
+    launch_scale(c, N, SMG_F64, 1.0 / wn, V.back());
+  }
+  std::vector<double> y(it, 0.0);
+  for (int i = it - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int l = i + 1; l < it; ++l) s -= H[i][l] * y[l];
+    y[i] = s / H[i][i];
+  }
+  for (int i = 0; i < it; ++i) launch_axpy(c, N, SMG_F64, y[i], Z[i], x);
+  launch_sub_pressure_mean(c, level, SMG_F64, x);
+  SMG_CUDA(cudaStreamSynchronize(c.stream));
+  if (iters) *iters = it;
+  return converged ? SMG_OK : SMG_ENOTCONV;
+}
+
+template <class F>
+int guarded(smg_context* h, F&& f) {
+  Context* c = reinterpret_cast<Context*>(h);
+  try {
+    return f();
+  } catch (const std::invalid_argument& e) {
+    if (c) c->last_error = e.what();
+    return SMG_EINVAL;
+  } catch (const std::bad_alloc& e) {
+    if (c) c->last_error = "out of memory";
+    return SMG_ENOMEM;
+  } catch (const not_converged& e) {
+    if (c) c->last_error = e.what();
+    return SMG_ENOTCONV;
+  } catch (const std::exception& e) {
+    if (c) c->last_error = e.what();
+    return SMG_ECUDA;
+  }
+}
+
+Context& ctx_of(smg_context* h) {
+  if (!h) throw std::invalid_argument("null context");
+  return *reinterpret_cast<Context*>(h);
+}
+
+void check_prec(int p) {
+  if (p != SMG_F64 && p != SMG_F32) throw std::invalid_argument("precision must be SMG_F64 or SMG_F32");
+}
+
+}  // namespace
+
+Context::~Context() {
+  for (void* p : allocations) cudaFree(p);
+  if (dot_host) cudaFreeHost(dot_host);
+}
+
+}  // namespace smg
+
+using smg::Context;
+
+extern "C" {
+
+int smg_config_default(smg_config* cfg) {
+  if (!cfg) return SMG_EINVAL;
+  cfg->degree = 2;
+  cfg->max_level = 3;
+  cfg->device = 0;
+  cfg->cg_max_iter = 30;
+  cfg->cg_tol = 1e-8;
+  cfg->cg_fixed = 0;
+  cfg->cg_precond = 1;
+  return SMG_OK;
+}
+
+int smg_level_sizes(int degree, int level, int64_t sizes[5]) {
+  try {
+    smg::LevelLayout l(degree, level);
+    for (int i = 0; i < 4; ++i) sizes[i] = l.size[i];
+    sizes[4] = l.total;
+    return SMG_OK;
+  } catch (...) {
+    return SMG_EINVAL;
+  }
+}
+
+static thread_local std::string g_create_error;
+
+int smg_create(const smg_config* cfg, smg_context** out) {
+  if (!cfg || !out) return SMG_EINVAL;
+  *out = nullptr;
+  Context* c = new (std::nothrow) Context();
+  if (!c) return SMG_ENOMEM;
+  int rc = smg::guarded(reinterpret_cast<smg_context*>(c), [&] {
+    if (cfg->degree < 1 || cfg->degree > 7) throw std::invalid_argument("degree must be in 1..7");
+    if (cfg->max_level < 0 || cfg->max_level > 10) throw std::invalid_argument("max_level must be in 0..10");
+    if (cfg->cg_max_iter < 0) throw std::invalid_argument("cg_max_iter must be >= 0");
+    c->cfg = *cfg;
+    int ndev = 0;
+    SMG_CUDA(cudaGetDeviceCount(&ndev));
+    if (cfg->device < 0 || cfg->device >= ndev) throw smg::cuda_error("no such CUDA device");
+    SMG_CUDA(cudaSetDevice(cfg->device));
+    cudaDeviceProp prop{};
+    SMG_CUDA(cudaGetDeviceProperties(&prop, cfg->device));
+    if (prop.major < 10) throw smg::cuda_error("libsmg_b200 needs an sm_100 (Blackwell) device");
+    c->device = cfg->device;
+    const int L = cfg->max_level;
+    c->ttab = smg::build_transfer_tables(cfg->degree);
+    std::vector<double> ttab;
+    for (double v : c->ttab.Ec.a) ttab.push_back(v);
+    for (double v : c->ttab.Ed.a) ttab.push_back(v);
+    for (int p = 0; p < 2; ++p) c->dev[p].resize(L + 1);
+    for (int l = 0; l <= L; ++l) {
+      c->tables.push_back(smg::build_level_tables(cfg->degree, l));
+      c->ptables.push_back(smg::build_patch_tables(c->tables.back()));
+      const auto packed = smg::pack_patch_tables(c->ptables.back());
+      const auto pw = smg::pressure_node_weights(cfg->degree);
+      for (int p = 0; p < 2; ++p) {
+        smg::DevLevel& d = c->dev[p][l];
+        d.lay = smg::LevelLayout(cfg->degree, l);
+        d.ops = smg::dev_upload(*c, c->tables.back().ops, p);
+        d.patch = smg::dev_upload(*c, packed, p);
+        d.transfer = smg::dev_upload(*c, ttab, p);
+        d.pweights = smg::dev_upload(*c, pw, SMG_F64);
+      }
+    }
+    SMG_CUDA(cudaMalloc(&c->dot_partials, (smg::kDotBlocks + 8) * sizeof(double)));
+    c->allocations.push_back(c->dot_partials);
+    SMG_CUDA(cudaMallocHost(&c->dot_host, 64));
+    smg::setup_coarse(*c);
+    return SMG_OK;
+  });
+  if (rc != SMG_OK) {
+    g_create_error = c->last_error;
+    delete c;
+    return rc;
+  }
+  *out = reinterpret_cast<smg_context*>(c);
+  return SMG_OK;
+}
+
+int smg_destroy(smg_context* h) {
+  if (!h) return SMG_EINVAL;
+  delete reinterpret_cast<Context*>(h);
+  return SMG_OK;
+}
+
+int smg_set_stream(smg_context* h, void* stream) {
+  return smg::guarded(h, [&] {
+    smg::ctx_of(h).stream = static_cast<cudaStream_t>(stream);
+    return SMG_OK;
+  });
+}
+
+const char* smg_last_error(const smg_context* h) {
+  if (!h) return g_create_error.c_str();
+  return reinterpret_cast<const Context*>(h)->last_error.c_str();
+}
+
+int64_t smg_launch_count(const smg_context* h) { return h ? reinterpret_cast<const Context*>(h)->launches : -1; }
+
+int smg_vec_alloc(smg_context* h, int level, int precision, void** dptr) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!dptr) throw std::invalid_argument("null output pointer");
+    SMG_CUDA(cudaMalloc(dptr, c.dev[0][level].lay.total * smg::elem_size(precision)));
+    SMG_CUDA(cudaMemset(*dptr, 0, c.dev[0][level].lay.total * smg::elem_size(precision)));
+    return SMG_OK;
+  });
+}
+
+int smg_vec_free(smg_context* h, void* dptr) {
+  return smg::guarded(h, [&] {
+    SMG_CUDA(cudaFree(dptr));
+    return SMG_OK;
+  });
+}
+
+int smg_vmult(smg_context* h, int level, int precision, void* y, const void* x) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!x || !y || x == y) throw std::invalid_argument("vmult: x and y must be distinct non-null vectors");
+    smg::launch_vmult(c, level, precision, y, x, nullptr);
+    return SMG_OK;
+  });
+}
+
+int smg_residual(smg_context* h, int level, int precision, void* r, const void* b, const void* x) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!r || !b || !x || r == x || r == b) throw std::invalid_argument("residual: r must differ from b and x");
+    smg::launch_vmult(c, level, precision, r, x, b);
+    return SMG_OK;
+  });
+}
+
+int smg_smooth(smg_context* h, int level, int precision, void* x, const void* b, int zero_init) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (level < 1) throw std::invalid_argument("smooth: level 0 uses the coarse solver (SPEC.md:71)");
+    if (zero_init) smg::launch_zero(c, c.dev[0][level].lay.total, precision, x);
+    smg::smooth(c, level, precision, x, b);
+    return SMG_OK;
+  });
+}
+
+int smg_prolongate_add(smg_context* h, int coarse_level, int precision, void* xf, const void* xc) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, coarse_level + 1);
+    smg::check_prec(precision);
+    smg::launch_prolongate_add(c, coarse_level, precision, xf, xc);
+    return SMG_OK;
+  });
+}
+
+int smg_restrict(smg_context* h, int coarse_level, int precision, void* rc, const void* rf) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, coarse_level + 1);
+    smg::check_prec(precision);
+    smg::launch_restrict(c, coarse_level, precision, rc, rf);
+    return SMG_OK;
+  });
+}
+
+int smg_coarse_solve(smg_context* h, int precision, void* x, const void* b) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_prec(precision);
+    smg::launch_coarse_apply(c, precision, x, b);
+    return SMG_OK;
+  });
+}
+
+int smg_vcycle(smg_context* h, int level, int precision, void* x, const void* b) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    smg::vcycle(c, level, precision, x, b);
+    return SMG_OK;
+  });
+}
+
+int smg_solve(smg_context* h, int level, void* x, const void* b, double rel_tol, int max_iter, int vp, int* iters,
+              double* history) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(vp);
+    if (!(rel_tol > 0.0 && rel_tol < 1.0)) throw std::invalid_argument("rel_tol must be in (0,1)");
+    if (max_iter < 1) throw std::invalid_argument("max_iter must be >= 1");
+    return smg::fgmres(c, level, static_cast<double*>(x), static_cast<const double*>(b), rel_tol, max_iter, vp,
+                       iters, history);
+  });
+}
+
+int smg_dot(smg_context* h, int level, int precision, const void* a, const void* b, double* out) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    *out = smg::dot(c, c.dev[0][level].lay.total, precision, a, b);
+    return SMG_OK;
+  });
+}
+
+int smg_axpy(smg_context* h, int level, int precision, double alpha, const void* x, void* y) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    smg::launch_axpy(c, c.dev[0][level].lay.total, precision, alpha, x, y);
+    return SMG_OK;
+  });
+}
+
+int smg_convert(smg_context* h, int level, int dp, void* dst, int sp, const void* src) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(dp);
+    smg::check_prec(sp);
+    smg::launch_convert(c, c.dev[0][level].lay.total, dp, dst, sp, src);
+    return SMG_OK;
+  });
+}
+
+int smg_vmult_host(smg_context* h, int level, int precision, void* const y_vel[3], void* y_p,
+                   const void* const x_vel[3], const void* x_p) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    const smg::LevelLayout& lay = c.dev[0][level].lay;
+    const size_t es = smg::elem_size(precision);
+    // device staging buffers: reuse the level's work vectors of this precision
+    smg::ensure_work(c, precision);
+    char* dx = static_cast<char*>(c.work_x[precision][level]);
+    char* dy = static_cast<char*>(c.work_b[precision][level]);
+    for (int b = 0; b < 3; ++b)
+      SMG_CUDA(cudaMemcpyAsync(dx + lay.off[b] * es, x_vel[b], lay.size[b] * es, cudaMemcpyHostToDevice, c.stream));
+    SMG_CUDA(cudaMemcpyAsync(dx + lay.off[3] * es, x_p, lay.size[3] * es, cudaMemcpyHostToDevice, c.stream));
+    smg::launch_vmult(c, level, precision, dy, dx, nullptr);
+    for (int b = 0; b < 3; ++b)
+      SMG_CUDA(cudaMemcpyAsync(y_vel[b], dy + lay.off[b] * es, lay.size[b] * es, cudaMemcpyDeviceToHost, c.stream));
+    SMG_CUDA(cudaMemcpyAsync(y_p, dy + lay.off[3] * es, lay.size[3] * es, cudaMemcpyDeviceToHost, c.stream));
+    SMG_CUDA(cudaStreamSynchronize(c.stream));
+    return SMG_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// Internal declarations shared by the CUDA translation units of libsmg_b200.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/smg_b200.h"
+#include "setup1d.hpp"
+
+namespace smg {
+
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct not_converged : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define SMG_CUDA(call)                                                                             \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      throw ::smg::cuda_error(std::string(#call) + ": " + cudaGetErrorString(e_));                \
+  } while (0)
+
+// Stored layout of one level vector.
+struct LevelLayout {
+  int k = 0, level = 0, m = 0, n = 0;
+  int64_t dims[3][3]{};  // dims[c][axis]
+  int64_t off[4]{};
+  int64_t size[4]{};
+  int64_t total = 0;
+  LevelLayout() = default;
+  LevelLayout(int kk, int lvl) : k(kk), level(lvl) {
+    if (kk < 1) throw std::invalid_argument("degree must be >= 1");
+    if (lvl < 0 || lvl > 12) throw std::invalid_argument("level out of range");
+    m = 2 << lvl;
+    n = m * (k + 1);
+    int64_t o = 0;
+    for (int c = 0; c < 3; ++c) {
+      for (int a = 0; a < 3; ++a) dims[c][a] = a == c ? n + 1 : n;
+      off[c] = o;
+      size[c] = dims[c][0] * dims[c][1] * dims[c][2];
+      o += size[c];
+    }
+    off[3] = o;
+    size[3] = static_cast<int64_t>(n) * n * n;
+    total = o + size[3];
+  }
+};
+
+// Device-resident constant data of one level in one precision.
+struct DevLevel {
+  LevelLayout lay;
+  void* ops = nullptr;      // N_OPS x 9 x (k+1) x (k+2) operator blocks
+  void* patch = nullptr;    // packed patch tables (smoother)
+  void* transfer = nullptr; // packed embedding tables (this level as the fine level)
+  void* pweights = nullptr; // pressure node weights (k+1)
+};
+
+struct Context {
+  smg_config cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  int64_t launches = 0;
+  std::vector<LevelTables> tables;      // per level
+  std::vector<PatchTables> ptables;     // per level
+  TransferTables ttab;
+  std::vector<DevLevel> dev[2];         // [precision][level]
+  // coarse solve: dense pseudo-inverse on the free DoFs of level 0
+  std::vector<int64_t> coarse_free;
+  void* coarse_pinv[2] = {nullptr, nullptr};
+  void* coarse_free_dev = nullptr;
+  // scratch
+  void* dot_partials = nullptr;  // double[kDotBlocks]
+  void* dot_host = nullptr;      // pinned double[kDotBlocks]
+  std::vector<void*> allocations;
+  // per-level work vectors for the smoother / V-cycle (allocated lazily): [prec][level]
+  std::vector<void*> work_r[2], work_x[2], work_b[2];
+  ~Context();
+};
+
+constexpr int kDotBlocks = 1184;  // 8 x 148 SMs
+
+size_t elem_size(int precision);
+
+// ---- launchers (stream-ordered) ----
+void launch_vmult(Context& c, int level, int prec, void* y, const void* x, const void* b /*residual if !null*/);
+void launch_smooth_colour(Context& c, int level, int prec, int colour, void* x, const void* r);
+void launch_prolongate_add(Context& c, int coarse_level, int prec, void* xf, const void* xc);
+void launch_restrict(Context& c, int coarse_level, int prec, void* rc, const void* rf);
+void launch_coarse_apply(Context& c, int prec, void* x, const void* b);
+double dot(Context& c, int64_t n, int prec, const void* a, const void* b);
+void launch_axpy(Context& c, int64_t n, int prec, double alpha, const void* x, void* y);
+void launch_axpby(Context& c, int64_t n, int prec, double alpha, const void* x, double beta, void* y);
+void launch_convert(Context& c, int64_t n, int dst_prec, void* dst, int src_prec, const void* src);
+void launch_zero(Context& c, int64_t n, int prec, void* x);
+void launch_scale(Context& c, int64_t n, int prec, double alpha, void* x);
+void launch_sub_pressure_mean(Context& c, int level, int prec, void* x);  // mass-weighted mean removal
+
+}  // namespace smg

@@ -1,0 +1,218 @@
+// K4/K6: intergrid transfer and the coarse solve (prolongate / restrict SPEC.md:441-458,
+// coarse_solve SPEC.md:468-476).
+// Prolongation is the canonical embedding of the coarse finite element function into the fine
+// space: per velocity component the continuous two-child embedding along its own axis and the
+// discontinuous one along the others; pressure discontinuous in all three (fem1d.hpp:243-264).
+// Restriction is its exact transpose on coefficient vectors. Both are one thread
+// per output DoF, reading the (k+2)(k+1)^2 / 2(k+1)-stencil from L1/L2; HBM-bound by construction.
+#include <cuda_runtime.h>
+
+#include "smg_internal.cuh"
+
+namespace smg {
+namespace {
+
+constexpr int kThreads = 256;
+
+// 1D stencils. Continuous (par): fine node gf of a coarse mesh with mc cells, H = k+1:
+//   cell E = gf / 2H, row r = gf - 2HE (last node: E = mc-1, r = 2H); coarse nodes E*H + j, j<=H.
+// Discontinuous: E = gf / 2H, r = gf % 2H; coarse nodes E*H + j, j < H.
+template <typename T, int K>
+__global__ void prolongate_kernel(T* __restrict__ xf, const T* __restrict__ xc, const T* __restrict__ tab, int mc) {
+  constexpr int H = K + 1;
+  constexpr int EC_R = 2 * H + 1, EC_C = H + 1, ED_R = 2 * H, ED_C = H;
+  __shared__ T Ec[EC_R * EC_C], Ed[ED_R * ED_C];
+  for (int i = threadIdx.x; i < EC_R * EC_C; i += blockDim.x) Ec[i] = tab[i];
+  for (int i = threadIdx.x; i < ED_R * ED_C; i += blockDim.x) Ed[i] = tab[EC_R * EC_C + i];
+  __syncthreads();
+  const int comp = blockIdx.y;
+  const int nc = mc * H, nf = 2 * nc;
+  int64_t fd[3] = {nf, nf, nf}, cd[3] = {nc, nc, nc};
+  if (comp < 3) { fd[comp] = nf + 1; cd[comp] = nc + 1; }
+  const int64_t fsize = fd[0] * fd[1] * fd[2];
+  const int64_t vf = static_cast<int64_t>(nf + 1) * nf * nf, vc = static_cast<int64_t>(nc + 1) * nc * nc;
+  T* out = xf + comp * vf;
+  const T* in = xc + comp * vc;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < fsize;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g[3] = {static_cast<int>(i % fd[0]), static_cast<int>((i / fd[0]) % fd[1]),
+                      static_cast<int>(i / (fd[0] * fd[1]))};
+    int base[3], row[3], cnt[3];
+    const T* W[3];
+    for (int a = 0; a < 3; ++a) {
+      if (a == comp) {
+        int E = g[a] / (2 * H), r = g[a] - 2 * H * E;
+        if (E == mc) { E = mc - 1; r = 2 * H; }
+        base[a] = E * H; row[a] = r; cnt[a] = EC_C; W[a] = Ec + r * EC_C;
+      } else {
+        const int E = g[a] / (2 * H);
+        base[a] = E * H; row[a] = g[a] - 2 * H * E; cnt[a] = ED_C; W[a] = Ed + row[a] * ED_C;
+      }
+    }
+    T s = T(0);
+    for (int j2 = 0; j2 < cnt[2]; ++j2) {
+      const T w2 = W[2][j2];
+      if (w2 == T(0)) continue;
+      const int c2 = base[2] + j2;
+      if (comp == 2 && (c2 == 0 || c2 == nc)) continue;
+      for (int j1 = 0; j1 < cnt[1]; ++j1) {
+        const T w12 = w2 * W[1][j1];
+        if (w12 == T(0)) continue;
+        const int c1 = base[1] + j1;
+        if (comp == 1 && (c1 == 0 || c1 == nc)) continue;
+        const T* src = in + (static_cast<int64_t>(c2) * cd[1] + c1) * cd[0] + base[0];
+        for (int j0 = 0; j0 < cnt[0]; ++j0) {
+          const int c0 = base[0] + j0;
+          if (comp == 0 && (c0 == 0 || c0 == nc)) continue;
+          s += w12 * W[0][j0] * src[j0];
+        }
+      }
+    }
+    out[i] += s;
+  }
+}
+
+// Restriction = P^T: coarse node gc collects fine rows r < 2H of every coarse cell containing it
+// (the fine vertex at r = 2H of cell E is row 0 of cell E+1, counted once).
+template <typename T, int K>
+__global__ void restrict_kernel(T* __restrict__ rc, const T* __restrict__ rf, const T* __restrict__ tab, int mc) {
+  constexpr int H = K + 1;
+  constexpr int EC_R = 2 * H + 1, EC_C = H + 1, ED_R = 2 * H, ED_C = H;
+  __shared__ T Ec[EC_R * EC_C], Ed[ED_R * ED_C];
+  for (int i = threadIdx.x; i < EC_R * EC_C; i += blockDim.x) Ec[i] = tab[i];
+  for (int i = threadIdx.x; i < ED_R * ED_C; i += blockDim.x) Ed[i] = tab[EC_R * EC_C + i];
+  __syncthreads();
+  const int comp = blockIdx.y;
+  const int nc = mc * H, nf = 2 * nc;
+  int64_t fd[3] = {nf, nf, nf}, cd[3] = {nc, nc, nc};
+  if (comp < 3) { fd[comp] = nf + 1; cd[comp] = nc + 1; }
+  const int64_t csize = cd[0] * cd[1] * cd[2];
+  const int64_t vf = static_cast<int64_t>(nf + 1) * nf * nf, vc = static_cast<int64_t>(nc + 1) * nc * nc;
+  T* out = rc + comp * vc;
+  const T* in = rf + comp * vf;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < csize;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g[3] = {static_cast<int>(i % cd[0]), static_cast<int>((i / cd[0]) % cd[1]),
+                      static_cast<int>(i / (cd[0] * cd[1]))};
+    if (comp < 3 && (g[comp] == 0 || g[comp] == nc)) {
+      out[i] = T(0);  // constrained coarse DoF
+      continue;
+    }
+    // per axis up to two (cell, local index) pairs
+    int ncell[3], fbase[3][2], jj[3][2];
+    bool par[3];
+    for (int a = 0; a < 3; ++a) {
+      par[a] = (a == comp);
+      const int E = g[a] / H, j = g[a] - E * H;
+      ncell[a] = 0;
+      if (E < mc) { fbase[a][ncell[a]] = 2 * H * E; jj[a][ncell[a]] = j; ++ncell[a]; }
+      if (par[a] && j == 0 && E > 0) { fbase[a][ncell[a]] = 2 * H * (E - 1); jj[a][ncell[a]] = H; ++ncell[a]; }
+    }
+    T s = T(0);
+    for (int p2 = 0; p2 < ncell[2]; ++p2)
+      for (int r2 = 0; r2 < 2 * H; ++r2) {
+        const T w2 = par[2] ? Ec[r2 * EC_C + jj[2][p2]] : Ed[r2 * ED_C + jj[2][p2]];
+        if (w2 == T(0)) continue;
+        const int f2 = fbase[2][p2] + r2;
+        for (int p1 = 0; p1 < ncell[1]; ++p1)
+          for (int r1 = 0; r1 < 2 * H; ++r1) {
+            const T w12 = w2 * (par[1] ? Ec[r1 * EC_C + jj[1][p1]] : Ed[r1 * ED_C + jj[1][p1]]);
+            if (w12 == T(0)) continue;
+            const int f1 = fbase[1][p1] + r1;
+            const T* src = in + (static_cast<int64_t>(f2) * fd[1] + f1) * fd[0];
+            for (int p0 = 0; p0 < ncell[0]; ++p0)
+              for (int r0 = 0; r0 < 2 * H; ++r0) {
+                const T w0 = par[0] ? Ec[r0 * EC_C + jj[0][p0]] : Ed[r0 * ED_C + jj[0][p0]];
+                const int f0 = fbase[0][p0] + r0;
+                if (comp == 0 && (f0 == 0 || f0 == nf)) continue;
+                if (comp == 1 && (f1 == 0 || f1 == nf)) continue;
+                if (comp == 2 && (f2 == 0 || f2 == nf)) continue;
+                s += w12 * w0 * src[f0];
+              }
+          }
+      }
+    out[i] = s;
+  }
+}
+
+// x_free = Pinv b_free, one warp per row (level 0: at most a few thousand free DoFs)
+template <typename T>
+__global__ void coarse_kernel(T* __restrict__ x, const T* __restrict__ b, const T* __restrict__ pinv,
+                              const int64_t* __restrict__ free_idx, int nf) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= nf) return;
+  const T* row = pinv + static_cast<int64_t>(warp) * nf;
+  T s = T(0);
+  for (int j = lane; j < nf; j += 32) s += row[j] * b[free_idx[j]];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) x[free_idx[warp]] = s;
+}
+
+int grid_for(int64_t n) {
+  const int64_t g = (n + kThreads - 1) / kThreads;
+  return static_cast<int>(g < 4 * kDotBlocks ? (g < 1 ? 1 : g) : 4 * kDotBlocks);
+}
+
+template <typename T, int K>
+void transfer_k(Context& ctx, int coarse_level, void* out, const void* in, bool prolong) {
+  const int p = sizeof(T) == 8 ? 0 : 1;
+  const DevLevel& fine = ctx.dev[p][coarse_level + 1];
+  const DevLevel& coarse = ctx.dev[p][coarse_level];
+  const int mc = coarse.lay.m;
+  if (prolong) {
+    dim3 grid(grid_for(fine.lay.size[0]), 4);
+    prolongate_kernel<T, K><<<grid, kThreads, 0, ctx.stream>>>(static_cast<T*>(out), static_cast<const T*>(in),
+                                                              static_cast<const T*>(fine.transfer), mc);
+  } else {
+    dim3 grid(grid_for(coarse.lay.size[0]), 4);
+    restrict_kernel<T, K><<<grid, kThreads, 0, ctx.stream>>>(static_cast<T*>(out), static_cast<const T*>(in),
+                                                            static_cast<const T*>(fine.transfer), mc);
+  }
+  SMG_CUDA(cudaGetLastError());
+  ++ctx.launches;
+}
+
+template <typename T>
+void transfer_prec(Context& ctx, int coarse_level, void* out, const void* in, bool prolong) {
+  switch (ctx.cfg.degree) {
+    case 1: transfer_k<T, 1>(ctx, coarse_level, out, in, prolong); break;
+    case 2: transfer_k<T, 2>(ctx, coarse_level, out, in, prolong); break;
+    case 3: transfer_k<T, 3>(ctx, coarse_level, out, in, prolong); break;
+    case 4: transfer_k<T, 4>(ctx, coarse_level, out, in, prolong); break;
+    case 5: transfer_k<T, 5>(ctx, coarse_level, out, in, prolong); break;
+    case 6: transfer_k<T, 6>(ctx, coarse_level, out, in, prolong); break;
+    case 7: transfer_k<T, 7>(ctx, coarse_level, out, in, prolong); break;
+    default: throw std::invalid_argument("degree not supported by the transfer kernels (1..7)");
+  }
+}
+
+}  // namespace
+
+void launch_prolongate_add(Context& ctx, int coarse_level, int prec, void* xf, const void* xc) {
+  if (prec == SMG_F64) transfer_prec<double>(ctx, coarse_level, xf, xc, true);
+  else transfer_prec<float>(ctx, coarse_level, xf, xc, true);
+}
+
+void launch_restrict(Context& ctx, int coarse_level, int prec, void* rc, const void* rf) {
+  if (prec == SMG_F64) transfer_prec<double>(ctx, coarse_level, rc, rf, false);
+  else transfer_prec<float>(ctx, coarse_level, rc, rf, false);
+}
+
+void launch_coarse_apply(Context& ctx, int prec, void* x, const void* b) {
+  const int nf = static_cast<int>(ctx.coarse_free.size());
+  const DevLevel& dl = ctx.dev[prec][0];
+  SMG_CUDA(cudaMemsetAsync(x, 0, dl.lay.total * elem_size(prec), ctx.stream));
+  const int blocks = (nf * 32 + kThreads - 1) / kThreads;
+  if (prec == SMG_F64)
+    coarse_kernel<double><<<blocks, kThreads, 0, ctx.stream>>>(
+        static_cast<double*>(x), static_cast<const double*>(b), static_cast<const double*>(ctx.coarse_pinv[0]),
+        static_cast<const int64_t*>(ctx.coarse_free_dev), nf);
+  else
+    coarse_kernel<float><<<blocks, kThreads, 0, ctx.stream>>>(
+        static_cast<float*>(x), static_cast<const float*>(b), static_cast<const float*>(ctx.coarse_pinv[1]),
+        static_cast<const int64_t*>(ctx.coarse_free_dev), nf);
+  SMG_CUDA(cudaGetLastError());
+  ++ctx.launches;
+}
+
+}  // namespace smg

@@ -1,0 +1,182 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle on the same inputs.
+
+Bar (BASELINE.json north_star): fp64 operator / smoother within 1e-12 relative, fp32 path within 1e-5,
+Krylov iteration counts equal +-1.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2410_09497_b200 as smg  # noqa: E402
+
+
+def rand_vec(k, level, seed, zero_constrained=True):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1.0, 1.0, oracle.sizes(k, level)[4])
+    if zero_constrained:
+        mask = constrained_mask(k, level)
+        x[mask] = 0.0
+    return x
+
+
+def constrained_mask(k, level):
+    s = oracle.sizes(k, level)
+    m = 2 << level
+    n = m * (k + 1)
+    mask = np.zeros(s[4], dtype=bool)
+    off = 0
+    for c in range(3):
+        dims = [n + 1 if a == c else n for a in range(3)]
+        arr = np.zeros(dims[::-1], dtype=bool)  # (z, y, x)
+        sl = [slice(None)] * 3
+        ax = 2 - c
+        sl[ax] = 0
+        arr[tuple(sl)] = True
+        sl[ax] = n
+        arr[tuple(sl)] = True
+        mask[off:off + arr.size] = arr.ravel()
+        off += arr.size
+    return mask
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def dev(x, dtype=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(device="cuda", dtype=dtype)
+
+
+@pytest.mark.parametrize("k,level", [(1, 0), (1, 1), (1, 2), (2, 0), (2, 1), (2, 2), (3, 1), (3, 2), (4, 1)])
+def test_vmult_fp64_matches_oracle(k, level):
+    ctx = smg.Context(k, level)
+    x = rand_vec(k, level, 1, zero_constrained=False)  # constrained entries must be ignored
+    y_ref = oracle.apply_stokes(k, level, x)
+    y = ctx.apply_stokes(level, dev(x)).cpu().numpy()
+    assert rel(y, y_ref) <= 1e-12
+
+
+@pytest.mark.parametrize("k,level", [(1, 2), (2, 2), (3, 1)])
+def test_vmult_fp32_matches_oracle(k, level):
+    ctx = smg.Context(k, level)
+    x = rand_vec(k, level, 2)
+    y_ref = oracle.apply_stokes(k, level, x)
+    y = ctx.apply_stokes(level, dev(x, torch.float32)).double().cpu().numpy()
+    assert rel(y, y_ref) <= 1e-5
+
+
+@pytest.mark.parametrize("k,level", [(1, 2), (2, 1)])
+def test_residual(k, level):
+    ctx = smg.Context(k, level)
+    x, b = rand_vec(k, level, 3), rand_vec(k, level, 4)
+    r_ref = oracle.residual(k, level, b, x)
+    r = ctx.residual(level, dev(b), dev(x)).cpu().numpy()
+    assert rel(r, r_ref) <= 1e-12
+
+
+@pytest.mark.parametrize("k,level", [(1, 1), (1, 2), (2, 1), (3, 1)])
+def test_smoother_fp64_fixed_cg_matches_oracle(k, level):
+    # parity mode: a fixed number of inner CG iterations on both sides
+    ctx = smg.Context(k, level, cg_max_iter=12, cg_fixed=True, cg_precond=1)
+    x0, b = rand_vec(k, level, 5), rand_vec(k, level, 6)
+    x_ref, _ = oracle.smooth(k, level, x0, b, oracle.cg_opts(12, 0.0, True, 1))
+    x = dev(x0)
+    ctx.smooth(level, x, dev(b))
+    assert rel(x.cpu().numpy(), x_ref) <= 1e-11
+
+
+@pytest.mark.parametrize("k,level", [(1, 2), (2, 1)])
+def test_smoother_fp32_matches_oracle(k, level):
+    ctx = smg.Context(k, level, cg_max_iter=12, cg_fixed=True, cg_precond=1)
+    x0, b = rand_vec(k, level, 7), rand_vec(k, level, 8)
+    x_ref, _ = oracle.smooth(k, level, x0, b, oracle.cg_opts(12, 0.0, True, 1))
+    x = dev(x0, torch.float32)
+    ctx.smooth(level, x, dev(b, torch.float32))
+    assert rel(x.double().cpu().numpy(), x_ref) <= 1e-4
+
+
+@pytest.mark.parametrize("k,level", [(1, 1), (2, 1), (2, 2), (3, 1)])
+def test_transfer_matches_oracle(k, level):
+    ctx = smg.Context(k, level)
+    xc = rand_vec(k, level - 1, 9)
+    xf = rand_vec(k, level, 10)
+    ref_p = oracle.prolongate_add(k, level - 1, xc, xf)
+    got = dev(xf)
+    ctx.prolongate_add(level - 1, got, dev(xc))
+    assert rel(got.cpu().numpy(), ref_p) <= 1e-13
+    ref_r = oracle.restrict(k, level - 1, xf)
+    got_r = ctx.restrict(level - 1, dev(xf)).cpu().numpy()
+    assert rel(got_r, ref_r) <= 1e-13
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_coarse_solve_matches_oracle(k):
+    ctx = smg.Context(k, 1)
+    b = oracle.apply_stokes(k, 0, rand_vec(k, 0, 11))
+    ref = oracle.coarse_solve(k, b)
+    got = ctx.coarse_solve(dev(b)).cpu().numpy()
+    assert rel(got, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("k,level", [(1, 2), (2, 1)])
+def test_vcycle_fp64_matches_oracle(k, level):
+    ctx = smg.Context(k, level, cg_max_iter=10, cg_fixed=True)
+    b = rand_vec(k, level, 12)
+    ref = oracle.vcycle(k, level, b, oracle.cg_opts(10, 0.0, True, 1))
+    got = ctx.vcycle(level, dev(b)).cpu().numpy()
+    assert rel(got, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("k,level", [(1, 2), (2, 2), (3, 1)])
+def test_solve_iteration_counts(k, level):
+    ctx = smg.Context(k, level, cg_max_iter=30, cg_tol=1e-8, cg_fixed=False)
+    b = oracle.apply_stokes(k, level, rand_vec(k, level, 13))
+    x_ref, it_ref, _ = oracle.fgmres(k, level, b, 1e-8, 40, oracle.cg_opts(30, 1e-8, False, 1))
+    for vp in (smg.F64, smg.F32):
+        x, it, hist = ctx.solve(level, dev(b), 1e-8, 40, vp)
+        assert abs(it - it_ref) <= 1, (vp, it, it_ref)
+        xr = x.cpu().numpy()
+        res = np.linalg.norm(b - oracle.apply_stokes(k, level, xr)) / np.linalg.norm(b)
+        assert res <= 2e-8
+
+
+def test_vmult_host_blockvector_path():
+    k, level = 2, 2
+    ctx = smg.Context(k, level)
+    x = rand_vec(k, level, 14)
+    blocks = smg.split_blocks(x, k, level)
+    ys = ctx.vmult_host(level, blocks)
+    assert rel(np.concatenate(ys), oracle.apply_stokes(k, level, x)) <= 1e-12
+
+
+def test_large_level_properties_symmetry_linearity():
+    # full-size properties where the oracle is too slow: <A x, y> = <x, A y>, A(ax + y) = aAx + Ay
+    k, level = 2, 5
+    ctx = smg.Context(k, level)
+    n = ctx.sizes(level)[4]
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    y = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    mask = torch.from_numpy(constrained_mask(k, level)).cuda()
+    x[mask] = 0
+    y[mask] = 0
+    Ax, Ay = ctx.apply_stokes(level, x), ctx.apply_stokes(level, y)
+    a, b = float(torch.dot(Ax, y)), float(torch.dot(x, Ay))
+    assert abs(a - b) <= 1e-11 * max(abs(a), 1.0) * 1e3
+    A2 = ctx.apply_stokes(level, 0.5 * x + y)
+    assert float((A2 - (0.5 * Ax + Ay)).abs().max()) <= 1e-12 * float(Ax.abs().max()) * 10
+    assert bool((Ax[mask] == 0).all())
+
+
+def test_errors_are_loud():
+    with pytest.raises(ValueError):
+        smg.Context(0, 2)
+    ctx = smg.Context(1, 1)
+    with pytest.raises(ValueError):
+        ctx.apply_stokes(1, torch.zeros(5, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        ctx.apply_stokes(3, ctx.new_vector(1))
