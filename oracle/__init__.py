@@ -204,3 +204,22 @@ def fgmres(k, level, b, tol=1e-8, max_iter=50, opts=None):
 
 def set_threads(n):
     lib().orc_set_threads(int(n))
+
+
+def constrained_mask(k, level):
+    """Boolean mask of the constrained boundary-normal DoFs in the stored level layout."""
+    s = sizes(k, level)
+    n = (2 << level) * (k + 1)
+    mask = np.zeros(s[4], dtype=bool)
+    off = 0
+    for c in range(3):
+        dims = [n + 1 if a == c else n for a in range(3)]
+        arr = np.zeros(dims[::-1], dtype=bool)  # (z, y, x)
+        sl = [slice(None)] * 3
+        sl[2 - c] = 0
+        arr[tuple(sl)] = True
+        sl[2 - c] = n
+        arr[tuple(sl)] = True
+        mask[off:off + arr.size] = arr.ravel()
+        off += arr.size
+    return mask

@@ -24,23 +24,7 @@ def rand_vec(k, level, seed, zero_constrained=True):
 
 
 def constrained_mask(k, level):
-    s = oracle.sizes(k, level)
-    m = 2 << level
-    n = m * (k + 1)
-    mask = np.zeros(s[4], dtype=bool)
-    off = 0
-    for c in range(3):
-        dims = [n + 1 if a == c else n for a in range(3)]
-        arr = np.zeros(dims[::-1], dtype=bool)  # (z, y, x)
-        sl = [slice(None)] * 3
-        ax = 2 - c
-        sl[ax] = 0
-        arr[tuple(sl)] = True
-        sl[ax] = n
-        arr[tuple(sl)] = True
-        mask[off:off + arr.size] = arr.ravel()
-        off += arr.size
-    return mask
+    return oracle.constrained_mask(k, level)
 
 
 def rel(a, b):
