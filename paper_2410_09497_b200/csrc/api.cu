@@ -362,6 +362,7 @@ int smg_create(const smg_config* cfg, smg_context** out) {
     SMG_CUDA(cudaGetDeviceProperties(&prop, cfg->device));
     if (prop.major < 10) throw smg::cuda_error("libsmg_b200 needs an sm_100 (Blackwell) device");
     c->device = cfg->device;
+    smg::upload_reference_tables();
     const int L = cfg->max_level;
     c->ttab = smg::build_transfer_tables(cfg->degree);
     std::vector<double> ttab;

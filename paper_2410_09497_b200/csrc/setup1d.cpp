@@ -271,6 +271,37 @@ TransferTables build_transfer_tables(int k) {
   return T;
 }
 
+std::vector<double> reference_cell_tables() {
+  std::vector<double> t(kRefTotal, 0.0);
+  for (int k = 1; k <= kMaxK; ++k) {
+    const int H = k + 1, P = k + 2;
+    const CellMats C = cell_mats(k, 1.0);
+    const FaceBlocks F = face_blocks(C, (k + 1) * (k + 2));
+    double* o = t.data() + ref_base(k);
+    auto put = [&](const Dense& A) {
+      for (double v : A.a) *o++ = v;
+    };
+    Dense LO0(H, H), DLF(H, H), DLL(H, H);
+    for (int a = 0; a < H; ++a)
+      for (int b = 0; b < H; ++b) {
+        LO0(a, b) = C.Ko(a, b) + F.RR(a, b) + F.LL(a, b);
+        DLF(a, b) = F.NitL(a, b) - F.RR(a, b);
+        DLL(a, b) = F.NitR(a, b) - F.LL(a, b);
+      }
+    put(C.Mo);
+    put(LO0);
+    put(F.RL);
+    put(F.LR);
+    put(DLF);
+    put(DLL);
+    put(C.Mp);
+    put(C.Kp);
+    put(C.Dc);
+    (void)P;
+  }
+  return t;
+}
+
 std::vector<double> pressure_node_weights(int k) {
   const auto z = gl_nodes(k);
   std::vector<double> qx, qw, w(k + 1, 0.0);

@@ -67,6 +67,24 @@ LevelTables build_level_tables(int k, int level);
 PatchTables build_patch_tables(const LevelTables& lt);
 TransferTables build_transfer_tables(int k);
 
+// Reference-cell (h = 1) operator blocks for the register-pencil kernels, for every k in 1..kMaxK,
+// concatenated in the order of ref_layout(): per k
+//   MO (H x H) DG mass | LO0 (H x H) interior SIPG diagonal block | LOM (H x H) delta=-1 block |
+//   LOP (H x H) delta=+1 block | DLF (H x H) first-cell correction (Nitsche - interior face) |
+//   DLL (H x H) last-cell correction | MP (P x P) C0 cell mass | LP (P x P) C0 cell stiffness |
+//   D (H x P) divergence factor,     H = k+1, P = k+2.
+// On level l (h = 2^-(l+1)) every mass block scales with h and every SIPG / stiffness block with 1/h
+// (the penalty (k+1)(k+2)/h and the trace derivatives carry the same 1/h); D is h-independent.
+constexpr int kMaxK = 7;
+constexpr int ref_size(int k) { return 6 * (k + 1) * (k + 1) + 2 * (k + 2) * (k + 2) + (k + 1) * (k + 2); }
+constexpr int ref_base(int k) {
+  int s = 0;
+  for (int j = 1; j < k; ++j) s += ref_size(j);
+  return s;
+}
+constexpr int kRefTotal = ref_base(kMaxK + 1);
+std::vector<double> reference_cell_tables();
+
 // Weights of the mass-weighted pressure mean: int psi_a over the reference cell.
 std::vector<double> pressure_node_weights(int k);
 

@@ -89,6 +89,8 @@ constexpr int kDotBlocks = 1184;  // 8 x 148 SMs
 
 size_t elem_size(int precision);
 
+void upload_reference_tables();  // __constant__ reference-cell blocks (vmult.cu)
+
 // ---- launchers (stream-ordered) ----
 void launch_vmult(Context& c, int level, int prec, void* y, const void* x, const void* b /*residual if !null*/);
 void launch_smooth_colour(Context& c, int level, int prec, int colour, void* x, const void* r);

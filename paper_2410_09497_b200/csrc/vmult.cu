@@ -2,264 +2,428 @@
 //
 // Reference: apply_stokes evaluated by Alg. 1. On the uniform
 // Cartesian unit cube the cell/face loops of Alg. 1 equal a Kronecker sum of banded 1D operators
-// (verified here against the quadrature-based CPU oracle to 1e-13). Per velocity
-// component c with orthogonal axes o1, o2:
-//   S  = M_o1 M_o2 u_c                      (DG mass, block diagonal)
-//   Tt = L_o1 (M_o2 u_c) + M_o1 (L_o2 u_c)  (DG SIPG, block tridiagonal)
-//   y_c = L_c S + M_c Tt + D_c^T (M_o1 M_o2 p)   (C0 stiffness/mass, divergence transpose)
-//   y_p += D_c S
-// One CTA owns a brick of TX x TY x TZ cells. It stages the input brick plus the halo each banded
-// operator needs in shared memory once, performs the seven sum-factorised 1D contractions per
-// component in shared memory, and writes each output DoF exactly once: HBM traffic is one read of x
-// and one write of y (16 B/DoF in fp64); halo re-reads are served from L2.
+// (re-verified by the GPU-vs-Alg.1-oracle parity tests to 1e-13). Per velocity
+// component c with orthogonal axes o1, o2 (all 1D blocks at reference size h = 1, see
+// setup1d.hpp reference_cell_tables; level scaling applied once at the output):
+//   pass 1 (along o2):  A1 = M_o2 u_c,            B1 = L_o2 u_c
+//   pass 2 (along o1):  S  = M_o1 A1,             T  = L_o1 A1 + M_o1 B1
+//   pass 3 (along c) :  y_c = h (L_c S + M_c T) + h^2 D_c^T Q,   y_p += h^2 D_c S
+// with Q = M_o1 M_o2 p. Every pass is "one thread per pencil": a thread loads a 1D line of the
+// brick from shared memory into registers, applies the banded cell-block operator with fully
+// unrolled loops whose coefficients are compile-time offsets into __constant__ memory (so they are
+// DFMA constant-bank operands, no loads), and writes the result line back. Index arithmetic is per
+// pencil, never per element. Domain-boundary Nitsche rows are a CTA-uniform correction applied only
+// by bricks that touch the boundary; constrained (boundary-normal) rows / inputs are masked.
+//
+// One CTA owns a brick of BX x BY x BZ cells. HBM traffic is one read of x and one write of y
+// (16 B/DoF in fp64); the one-cell halos of neighbouring bricks are re-read from L2.
 #include <cuda_runtime.h>
 
 #include "smg_internal.cuh"
 
 namespace smg {
+
+__constant__ double c_ref_d[kRefTotal];
+__constant__ float c_ref_f[kRefTotal];
+
 namespace {
 
-struct Box {
-  int lo[3];
-  int n[3];
-  __device__ int size() const { return n[0] * n[1] * n[2]; }
-  __device__ int idx(int x, int y, int z) const { return ((z - lo[2]) * n[1] + (y - lo[1])) * n[0] + (x - lo[0]); }
+template <typename T>
+__device__ __forceinline__ T cref(int i);
+template <>
+__device__ __forceinline__ double cref<double>(int i) { return c_ref_d[i]; }
+template <>
+__device__ __forceinline__ float cref<float>(int i) { return c_ref_f[i]; }
+
+template <int K>
+struct Ref {
+  static constexpr int H = K + 1, P = K + 2;
+  static constexpr int MO = ref_base(K);
+  static constexpr int LO0 = MO + H * H;
+  static constexpr int LOM = LO0 + H * H;
+  static constexpr int LOP = LOM + H * H;
+  static constexpr int DLF = LOP + H * H;
+  static constexpr int DLL = DLF + H * H;
+  static constexpr int MP = DLL + H * H;
+  static constexpr int LP = MP + P * P;
+  static constexpr int D = LP + P * P;
 };
 
-__device__ __forceinline__ int floor_div(int a, int b) { return (a >= 0) ? a / b : -((-a + b - 1) / b); }
+constexpr int odd(int v) { return v | 1; }
 
-// Banded 1D contraction along axis AX in shared memory:
-//   dst(q) (+)= sum_{delta, b} W[var][delta][a][b] * src(q with q[AX] = (e+delta)(K+1)+b)
-// where q[AX] = e (K+1) + a, var = first/interior/last of the global cell e + cell0.
-template <typename T, int K, int NB, int AX, int DMIN, int DMAX, bool ACC>
-__device__ __forceinline__ void contract(const T* __restrict__ src, const Box& sb, T* __restrict__ dst,
-                                         const Box& db, const T* __restrict__ W, int cell0, int m) {
+// ---------------------------------------------------------------------------------------------
+// register-pencil banded operators
+// ---------------------------------------------------------------------------------------------
+// DG mass (block diagonal): out[e*H+a] = sum_b MO[a][b] in[(e+OFF)*H+b]
+template <typename T, int K, int NC, int OFF, int LIN>
+__device__ __forceinline__ void dg_mass(const T (&in)[LIN], T (&out)[NC * (K + 1)]) {
   constexpr int H = K + 1;
-  const int total = db.size();
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    int q[3];
-    q[0] = db.lo[0] + i % db.n[0];
-    q[1] = db.lo[1] + (i / db.n[0]) % db.n[1];
-    q[2] = db.lo[2] + i / (db.n[0] * db.n[1]);
-    const int g = q[AX];
-    const int e = floor_div(g, H);
-    const int a = g - e * H;
-    const int E = cell0 + e;
-    T sum = T(0);
-    if (E >= 0 && E < m) {
-      const int var = (E == 0) ? 0 : (E == m - 1 ? 2 : 1);
-      int sq[3] = {q[0], q[1], q[2]};
 #pragma unroll
-      for (int d = DMIN; d <= DMAX; ++d) {
-        const T* w = W + ((var * 3 + d + 1) * H + a) * (K + 2);
-        const int base = (e + d) * H;
+  for (int e = 0; e < NC; ++e)
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          const int s = base + b;
-          if (s >= sb.lo[AX] && s < sb.lo[AX] + sb.n[AX]) {
-            sq[AX] = s;
-            sum += w[b] * src[sb.idx(sq[0], sq[1], sq[2])];
-          }
+    for (int a = 0; a < H; ++a) {
+      T s = T(0);
+#pragma unroll
+      for (int b = 0; b < H; ++b) s += cref<T>(Ref<K>::MO + a * H + b) * in[(e + OFF) * H + b];
+      out[e * H + a] = s;
+    }
+}
+
+// DG SIPG Laplacian (block tridiagonal; the off-diagonal blocks are "cross shaped" for the
+// Gauss-Lobatto nodal basis: LOM[a][b] != 0 only if a == 0 or b == K, LOP[a][b] only if a == K or
+// b == 0). in holds one halo cell on each side: cell e is in[(e+1)*H ...]. Output cells whose
+// global index is 0 / m-1 get the Nitsche correction (efirst / elast local cell, -1 if none).
+template <typename T, int K, int NC, bool BND>
+__device__ __forceinline__ void dg_sipg(const T (&in)[(NC + 2) * (K + 1)], T (&out)[NC * (K + 1)], int efirst,
+                                        int elast) {
+  constexpr int H = K + 1;
+  using R = Ref<K>;
+#pragma unroll
+  for (int e = 0; e < NC; ++e)
+#pragma unroll
+    for (int a = 0; a < H; ++a) {
+      T s = T(0);
+#pragma unroll
+      for (int b = 0; b < H; ++b) s += cref<T>(R::LO0 + a * H + b) * in[(e + 1) * H + b];
+#pragma unroll
+      for (int b = 0; b < H; ++b)
+        if (a == 0 || b == K) s += cref<T>(R::LOM + a * H + b) * in[e * H + b];
+#pragma unroll
+      for (int b = 0; b < H; ++b)
+        if (a == K || b == 0) s += cref<T>(R::LOP + a * H + b) * in[(e + 2) * H + b];
+      if (BND) {
+        if (e == efirst) {
+#pragma unroll
+          for (int b = 0; b < H; ++b) s += cref<T>(R::DLF + a * H + b) * in[(e + 1) * H + b];
+        }
+        if (e == elast) {
+#pragma unroll
+          for (int b = 0; b < H; ++b) s += cref<T>(R::DLL + a * H + b) * in[(e + 1) * H + b];
         }
       }
+      out[e * H + a] = s;
     }
-    const int o = db.idx(q[0], q[1], q[2]);
-    dst[o] = ACC ? dst[o] + sum : sum;
-  }
 }
 
-template <int K, int TX, int TY, int TZ>
-struct Plan {
+// ---------------------------------------------------------------------------------------------
+// brick geometry
+// ---------------------------------------------------------------------------------------------
+template <int K, int BX, int BY, int BZ>
+struct Brick {
   static constexpr int H = K + 1;
-  static constexpr int Nax(int a) { return (a == 0 ? TX : (a == 1 ? TY : TZ)) * H; }
-  static constexpr int o1(int c) { return c == 0 ? 1 : 0; }
-  static constexpr int o2(int c) { return c == 2 ? 1 : 2; }
-  static constexpr int par_n(int c) { return Nax(c) + K + 2; }  // [-H, N_c]
-  static constexpr int halo_n(int a) { return Nax(a) + 2 * H; }  // [-H, N+H)
-  static constexpr int sizeU(int c) { return par_n(c) * halo_n(o1(c)) * halo_n(o2(c)); }
-  static constexpr int sizeA1(int c) { return par_n(c) * halo_n(o1(c)) * Nax(o2(c)); }
-  static constexpr int sizeB1(int c) { return par_n(c) * Nax(o1(c)) * Nax(o2(c)); }
-  static constexpr int sizeQ(int c) { return (Nax(c) + H) * Nax(o1(c)) * Nax(o2(c)); }
-  static constexpr int mx(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
-  static constexpr int U = mx(sizeU(0), sizeU(1), sizeU(2));
-  static constexpr int A1 = mx(mx(sizeA1(0), sizeA1(1), sizeA1(2)), sizeQ(0), mx(sizeQ(1), sizeQ(2), 0));
-  static constexpr int B1 = mx(sizeB1(0), sizeB1(1), sizeB1(2));
-  static constexpr int Q = mx(sizeQ(0), sizeQ(1), sizeQ(2));
-  static constexpr int P = (Nax(0) + H) * (Nax(1) + H) * (Nax(2) + H);
-  static constexpr int YP = Nax(0) * Nax(1) * Nax(2);
-  static constexpr int TAB = N_OPS * 9 * (K + 1) * (K + 2);
-  static constexpr bool ALIAS = 2 * B1 <= U;  // S, Tt live in the dead U buffer when they fit
-  static constexpr int TOTAL = TAB + P + YP + Q + U + A1 + B1 + (ALIAS ? 0 : 2 * B1);
+  static constexpr int B(int a) { return a == 0 ? BX : (a == 1 ? BY : BZ); }
+  static constexpr int N(int a) { return B(a) * H; }
+  static constexpr int O1(int c) { return c == 0 ? 1 : 0; }
+  static constexpr int O2(int c) { return c == 2 ? 1 : 2; }
+  static constexpr int LC(int c) { return N(c) + H + 1; }       // c range [-H, N_c]
+  static constexpr int PC(int c) { return odd(LC(c)); }         // padded c extent
+  static constexpr int LO1H(int c) { return N(O1(c)) + 2 * H; }  // o1 range [-H, N + H)
+  static constexpr int LO2H(int c) { return N(O2(c)) + 2 * H; }
+  static constexpr int sizeU(int c) { return LO2H(c) * LO1H(c) * PC(c); }
+  static constexpr int sizeA1(int c) { return N(O2(c)) * LO1H(c) * PC(c); }
+  static constexpr int sizeST(int c) { return N(O2(c)) * N(O1(c)) * PC(c); }
+  static constexpr int mx3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
+  static constexpr int U = mx3(sizeU(0), sizeU(1), sizeU(2));
+  static constexpr int A1 = mx3(sizeA1(0), sizeA1(1), sizeA1(2));
+  static constexpr int ST = mx3(sizeST(0), sizeST(1), sizeST(2));
+  static constexpr int PX = odd(N(0) + H);  // pressure box, low halo on every axis
+  static constexpr int PBOX = (N(2) + H) * (N(1) + H) * PX;
+  static constexpr int YX = odd(N(0));
+  static constexpr int YP = N(2) * N(1) * YX;
+  static constexpr bool ALIAS = 2 * ST <= U;  // S and T overwrite the dead U buffer
+  // layout: [U][A1 (also Q2)][B1][Q][P box][YP][S,T if no alias]
+  static constexpr int OFF_A1 = U;
+  static constexpr int OFF_B1 = OFF_A1 + A1;
+  static constexpr int OFF_Q = OFF_B1 + ST;
+  static constexpr int OFF_P = OFF_Q + ST;
+  static constexpr int OFF_YP = OFF_P + PBOX;
+  static constexpr int OFF_ST = ALIAS ? 0 : OFF_YP + YP;
+  static constexpr int TOTAL = OFF_YP + YP + (ALIAS ? 0 : 2 * ST);
+  static constexpr int stride(int axis, int a0, int a1) { return axis == 0 ? 1 : (axis == 1 ? a0 : a0 * a1); }
 };
 
-template <typename T, int K, int TX, int TY, int TZ, bool RESID>
-__global__ void __launch_bounds__(256) stokes_vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                                           const T* __restrict__ b, const T* __restrict__ ops,
-                                                           int m) {
-  using PL = Plan<K, TX, TY, TZ>;
+struct Geo {
+  int m, n;
+  int c0[3];  // brick cell origin
+  int g0[3];  // brick node origin
+  const void* x;
+  void* y;
+  const void* b;
+};
+
+// ---------------------------------------------------------------------------------------------
+// one velocity component
+// ---------------------------------------------------------------------------------------------
+template <typename T, int K, int BX, int BY, int BZ, int NT, int C, bool RESID>
+__device__ __forceinline__ void component(T* sm, const Geo& G, T h) {
+  using BR = Brick<K, BX, BY, BZ>;
   constexpr int H = K + 1;
-  constexpr int OPS = 9 * (K + 1) * (K + 2);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* W = reinterpret_cast<T*>(smem_raw);
-  T* sP = W + PL::TAB;
-  T* sYP = sP + PL::P;
-  T* sQ = sYP + PL::YP;
-  T* sU = sQ + PL::Q;
-  T* sA1 = sU + PL::U;
-  T* sB1 = sA1 + PL::A1;
-  T* sS = PL::ALIAS ? sU : sB1 + PL::B1;  // U is dead once A1, B1 exist
-  T* sT = sS + PL::B1;
-
-  const int n = m * H;
-  const int c0[3] = {static_cast<int>(blockIdx.x) * TX, static_cast<int>(blockIdx.y) * TY,
-                     static_cast<int>(blockIdx.z) * TZ};
-  const int g0[3] = {c0[0] * H, c0[1] * H, c0[2] * H};
+  constexpr int O1 = BR::O1(C), O2 = BR::O2(C);
+  constexpr int NCc = BR::B(C), NO1 = BR::B(O1), NO2 = BR::B(O2);
+  constexpr int Nc = BR::N(C), No1 = BR::N(O1), No2 = BR::N(O2);
+  constexpr int LC = BR::LC(C), PC = BR::PC(C), LO1H = BR::LO1H(C), LO2H = BR::LO2H(C);
+  const int tid = threadIdx.x;
+  const int n = G.n, m = G.m;
+  const T* __restrict__ x = static_cast<const T*>(G.x);
+  T* __restrict__ y = static_cast<T*>(G.y);
   const int64_t sizeV = static_cast<int64_t>(n + 1) * n * n;
-  const int64_t offP = 3 * sizeV;
+  int64_t gd[3] = {n, n, n};
+  gd[C] = n + 1;
+  const int64_t st[3] = {1, gd[0], gd[0] * gd[1]};
+  const T* __restrict__ xc = x + C * sizeV;
 
-  for (int i = threadIdx.x; i < PL::TAB; i += blockDim.x) W[i] = ops[i];
-  // pressure box with a one-cell halo on the low side of every axis
-  Box bP;
-  for (int a = 0; a < 3; ++a) { bP.lo[a] = -H; bP.n[a] = PL::Nax(a) + H; }
-  for (int i = threadIdx.x; i < PL::P; i += blockDim.x) {
-    const int lx = i % bP.n[0] - H, ly = (i / bP.n[0]) % bP.n[1] - H, lz = i / (bP.n[0] * bP.n[1]) - H;
-    const int gx = g0[0] + lx, gy = g0[1] + ly, gz = g0[2] + lz;
-    T v = T(0);
-    if (gx >= 0 && gx < n && gy >= 0 && gy < n && gz >= 0 && gz < n)
-      v = x[offP + (static_cast<int64_t>(gz) * n + gy) * n + gx];
-    sP[i] = v;
-  }
-  for (int i = threadIdx.x; i < PL::YP; i += blockDim.x) sYP[i] = T(0);
-  __syncthreads();
+  T* sU = sm;
+  T* sA1 = sm + BR::OFF_A1;
+  T* sB1 = sm + BR::OFF_B1;
+  T* sQ = sm + BR::OFF_Q;
+  const T* sP = sm + BR::OFF_P;
+  T* sYP = sm + BR::OFF_YP;
+  T* sS = sm + BR::OFF_ST;
+  T* sT = sS + BR::ST;
 
-#pragma unroll 1
-  for (int c = 0; c < 3; ++c) {
-    const int o1 = PL::o1(c), o2 = PL::o2(c);
-    const int64_t offc = c * sizeV;
-    int64_t gd[3] = {n, n, n};
-    gd[c] = n + 1;
-    // ---- stage U (x_c with halos; constrained boundary-normal entries read as 0) ----
-    Box bU;
-    bU.lo[c] = -H; bU.n[c] = PL::Nax(c) + K + 2;
-    bU.lo[o1] = -H; bU.n[o1] = PL::Nax(o1) + 2 * H;
-    bU.lo[o2] = -H; bU.n[o2] = PL::Nax(o2) + 2 * H;
-    for (int i = threadIdx.x; i < bU.size(); i += blockDim.x) {
-      int l[3] = {i % bU.n[0] + bU.lo[0], (i / bU.n[0]) % bU.n[1] + bU.lo[1], i / (bU.n[0] * bU.n[1]) + bU.lo[2]};
-      int g[3] = {g0[0] + l[0], g0[1] + l[1], g0[2] + l[2]};
+  // ---- stage U: box [-H, N_c] x [-H, N_o1+H) x [-H, N_o2+H) in global axis order (x fastest) ----
+  {
+    constexpr int E0 = C == 0 ? LC : (O1 == 0 ? LO1H : LO2H);
+    constexpr int E1 = C == 1 ? LC : (O1 == 1 ? LO1H : LO2H);
+    constexpr int E2 = C == 2 ? LC : (O1 == 2 ? LO1H : LO2H);
+    for (int i = tid; i < E0 * E1 * E2; i += NT) {
+      const int l[3] = {i % E0 - H, (i / E0) % E1 - H, i / (E0 * E1) - H};
+      const int g[3] = {G.g0[0] + l[0], G.g0[1] + l[1], G.g0[2] + l[2]};
       bool ok = g[0] >= 0 && g[1] >= 0 && g[2] >= 0 && g[0] < gd[0] && g[1] < gd[1] && g[2] < gd[2];
-      ok = ok && g[c] != 0 && g[c] != n;
-      sU[i] = ok ? x[offc + (static_cast<int64_t>(g[2]) * gd[1] + g[1]) * gd[0] + g[0]] : T(0);
+      ok = ok && g[C] != 0 && g[C] != n;
+      const T v = ok ? __ldg(xc + g[0] + g[1] * st[1] + g[2] * st[2]) : T(0);
+      sU[((l[O2] + H) * LO1H + (l[O1] + H)) * PC + (l[C] + H)] = v;
     }
-    // ---- Q = M_o1 M_o2 p over [-H, N_c) x owned x owned ----
-    Box bQ2;
-    bQ2.lo[c] = -H; bQ2.n[c] = PL::Nax(c) + H;
-    bQ2.lo[o1] = 0; bQ2.n[o1] = PL::Nax(o1);
-    bQ2.lo[o2] = 0; bQ2.n[o2] = PL::Nax(o2);
+  }
+  // ---- Q2 = M_o2 p over c in [-H, N_c), o1 owned, o2 owned  (pencils along o2, from the P box) ----
+  {
     T* sQ2 = sA1;
-    if (o2 == 1) contract<T, K, K + 1, 1, 0, 0, false>(sP, bP, sQ2, bQ2, W + OP_MO * OPS, c0[1], m);
-    else contract<T, K, K + 1, 2, 0, 0, false>(sP, bP, sQ2, bQ2, W + OP_MO * OPS, c0[2], m);
-    __syncthreads();
-    if (o1 == 0) contract<T, K, K + 1, 0, 0, 0, false>(sQ2, bQ2, sQ, bQ2, W + OP_MO * OPS, c0[0], m);
-    else contract<T, K, K + 1, 1, 0, 0, false>(sQ2, bQ2, sQ, bQ2, W + OP_MO * OPS, c0[1], m);
-    __syncthreads();
-    // ---- A1 = M_o2 U (o1 keeps its halo), B1 = L_o2 U ----
-    Box bA1 = bU;
-    bA1.lo[o2] = 0; bA1.n[o2] = PL::Nax(o2);
-    Box bB1 = bA1;
-    bB1.lo[o1] = 0; bB1.n[o1] = PL::Nax(o1);
-    if (o2 == 1) {
-      contract<T, K, K + 1, 1, 0, 0, false>(sU, bU, sA1, bA1, W + OP_MO * OPS, c0[1], m);
-      contract<T, K, K + 1, 1, -1, 1, false>(sU, bU, sB1, bB1, W + OP_LO * OPS, c0[1], m);
-    } else {
-      contract<T, K, K + 1, 2, 0, 0, false>(sU, bU, sA1, bA1, W + OP_MO * OPS, c0[2], m);
-      contract<T, K, K + 1, 2, -1, 1, false>(sU, bU, sB1, bB1, W + OP_LO * OPS, c0[2], m);
+    constexpr int E1P = BR::N(1) + H;
+    constexpr int PSC = BR::stride(C, BR::PX, E1P), PSO1 = BR::stride(O1, BR::PX, E1P),
+                  PSO2 = BR::stride(O2, BR::PX, E1P);
+    constexpr int NPEN = (Nc + H) * No1;
+    for (int p = tid; p < NPEN; p += NT) {
+      const int ci = p % (Nc + H), oi = p / (Nc + H);  // ci is the 0-based index of c in [-H, N_c)
+      const T* src = sP + ci * PSC + (oi + H) * PSO1 + H * PSO2;
+      T in[No2];
+#pragma unroll
+      for (int j = 0; j < No2; ++j) in[j] = src[j * PSO2];
+      T out[No2];
+      dg_mass<T, K, NO2, 0>(in, out);
+#pragma unroll
+      for (int j = 0; j < No2; ++j) sQ2[(j * No1 + oi) * PC + ci] = out[j];
     }
     __syncthreads();
-    // ---- S = M_o1 A1 ; Tt = L_o1 A1 + M_o1 B1 ----
-    if (o1 == 0) {
-      contract<T, K, K + 1, 0, 0, 0, false>(sA1, bA1, sS, bB1, W + OP_MO * OPS, c0[0], m);
-      contract<T, K, K + 1, 0, -1, 1, false>(sA1, bA1, sT, bB1, W + OP_LO * OPS, c0[0], m);
-    } else {
-      contract<T, K, K + 1, 1, 0, 0, false>(sA1, bA1, sS, bB1, W + OP_MO * OPS, c0[1], m);
-      contract<T, K, K + 1, 1, -1, 1, false>(sA1, bA1, sT, bB1, W + OP_LO * OPS, c0[1], m);
+    // Q = M_o1 Q2 (pencils along o1)
+    constexpr int NPEN2 = (Nc + H) * No2;
+    for (int p = tid; p < NPEN2; p += NT) {
+      const int ci = p % (Nc + H), oj = p / (Nc + H);
+      T in[No1];
+#pragma unroll
+      for (int j = 0; j < No1; ++j) in[j] = sQ2[(oj * No1 + j) * PC + ci];
+      T out[No1];
+      dg_mass<T, K, NO1, 0>(in, out);
+#pragma unroll
+      for (int j = 0; j < No1; ++j) sQ[(oj * No1 + j) * PC + ci] = out[j];
     }
     __syncthreads();
-    if (o1 == 0) contract<T, K, K + 1, 0, 0, 0, true>(sB1, bB1, sT, bB1, W + OP_MO * OPS, c0[0], m);
-    else contract<T, K, K + 1, 1, 0, 0, true>(sB1, bB1, sT, bB1, W + OP_MO * OPS, c0[1], m);
-    __syncthreads();
-    // ---- y_c = L_c S + M_c Tt + D_c^T Q over the owned box; y_p += D_c S ----
-    Box bY;
-    for (int a = 0; a < 3; ++a) { bY.lo[a] = 0; bY.n[a] = PL::Nax(a); }
-    // reuse sA1 (dead) for the three contributions, then write out
-    T* sY = sA1;
-    if (c == 0) {
-      contract<T, K, K + 2, 0, -1, 0, false>(sS, bB1, sY, bY, W + OP_LP * OPS, c0[0], m);
-      contract<T, K, K + 2, 0, -1, 0, true>(sT, bB1, sY, bY, W + OP_MP * OPS, c0[0], m);
-      contract<T, K, K + 1, 0, -1, 0, true>(sQ, bQ2, sY, bY, W + OP_DT * OPS, c0[0], m);
-      contract<T, K, K + 2, 0, 0, 0, true>(sS, bB1, sYP, bY, W + OP_D * OPS, c0[0], m);
-    } else if (c == 1) {
-      contract<T, K, K + 2, 1, -1, 0, false>(sS, bB1, sY, bY, W + OP_LP * OPS, c0[1], m);
-      contract<T, K, K + 2, 1, -1, 0, true>(sT, bB1, sY, bY, W + OP_MP * OPS, c0[1], m);
-      contract<T, K, K + 1, 1, -1, 0, true>(sQ, bQ2, sY, bY, W + OP_DT * OPS, c0[1], m);
-      contract<T, K, K + 2, 1, 0, 0, true>(sS, bB1, sYP, bY, W + OP_D * OPS, c0[1], m);
-    } else {
-      contract<T, K, K + 2, 2, -1, 0, false>(sS, bB1, sY, bY, W + OP_LP * OPS, c0[2], m);
-      contract<T, K, K + 2, 2, -1, 0, true>(sT, bB1, sY, bY, W + OP_MP * OPS, c0[2], m);
-      contract<T, K, K + 1, 2, -1, 0, true>(sQ, bQ2, sY, bY, W + OP_DT * OPS, c0[2], m);
-      contract<T, K, K + 2, 2, 0, 0, true>(sS, bB1, sYP, bY, W + OP_D * OPS, c0[2], m);
-    }
-    // (each thread reads back exactly the sY / sYP entries it wrote: no barrier needed here)
-    for (int i = threadIdx.x; i < bY.size(); i += blockDim.x) {
-      int l[3] = {i % bY.n[0], (i / bY.n[0]) % bY.n[1], i / (bY.n[0] * bY.n[1])};
-      int g[3] = {g0[0] + l[0], g0[1] + l[1], g0[2] + l[2]};
-      if (g[0] >= n || g[1] >= n || g[2] >= n) continue;  // partial brick beyond the mesh
-      const int64_t gi = offc + (static_cast<int64_t>(g[2]) * gd[1] + g[1]) * gd[0] + g[0];
-      T v = sY[i];
-      if (g[c] == 0) v = T(0);  // constrained
-      else if (RESID) v = b[gi] - v;
-      y[gi] = v;
-    }
-    // the constrained plane g_c = n belongs to the last brick along c
-    if (c0[c] + (c == 0 ? TX : (c == 1 ? TY : TZ)) >= m) {
-      const int na = PL::Nax(o1), nb = PL::Nax(o2);
-      for (int i = threadIdx.x; i < na * nb; i += blockDim.x) {
-        int g[3];
-        g[c] = n;
-        g[o1] = g0[o1] + i % na;
-        g[o2] = g0[o2] + i / na;
-        if (g[o1] >= n || g[o2] >= n) continue;
-        y[offc + (static_cast<int64_t>(g[2]) * gd[1] + g[1]) * gd[0] + g[0]] = T(0);
+  }
+  // ---- pass 1 (along o2): A1 = M_o2 U  (c full, o1 with halo, o2 owned);  B1 = L_o2 U (o1 owned) ----
+  {
+    const int cell_o2 = G.c0[O2];
+    const bool bnd = (cell_o2 == 0) || (cell_o2 + NO2 >= m);
+    const int efirst = (cell_o2 == 0) ? 0 : -1;
+    const int elast = (m - 1 - cell_o2 < NO2) ? m - 1 - cell_o2 : -1;
+    constexpr int NPEN = LC * LO1H;
+    for (int p = tid; p < NPEN; p += NT) {
+      const int ci = p % LC, oi = p / LC;  // 0-based indices in the halo box
+      T in[(NO2 + 2) * H];
+#pragma unroll
+      for (int j = 0; j < (NO2 + 2) * H; ++j) in[j] = sU[(j * LO1H + oi) * PC + ci];
+      T a1[No2];
+      dg_mass<T, K, NO2, 1>(in, a1);
+#pragma unroll
+      for (int j = 0; j < No2; ++j) sA1[(j * LO1H + oi) * PC + ci] = a1[j];
+      if (oi >= H && oi < H + No1) {
+        T b1[No2];
+        if (bnd) dg_sipg<T, K, NO2, true>(in, b1, efirst, elast);
+        else dg_sipg<T, K, NO2, false>(in, b1, -1, -1);
+#pragma unroll
+        for (int j = 0; j < No2; ++j) sB1[(j * No1 + (oi - H)) * PC + ci] = b1[j];
       }
     }
-    __syncthreads();
   }
-  // ---- pressure rows ----
-  for (int i = threadIdx.x; i < PL::YP; i += blockDim.x) {
-    const int lx = i % PL::Nax(0), ly = (i / PL::Nax(0)) % PL::Nax(1), lz = i / (PL::Nax(0) * PL::Nax(1));
-    const int gx = g0[0] + lx, gy = g0[1] + ly, gz = g0[2] + lz;
-    if (gx >= n || gy >= n || gz >= n) continue;
-    const int64_t gi = offP + (static_cast<int64_t>(gz) * n + gy) * n + gx;
-    y[gi] = RESID ? b[gi] - sYP[i] : sYP[i];
+  __syncthreads();
+  // ---- pass 2 (along o1): S = M_o1 A1, T = L_o1 A1 + M_o1 B1  (c full, o1/o2 owned) ----
+  {
+    const int cell_o1 = G.c0[O1];
+    const bool bnd = (cell_o1 == 0) || (cell_o1 + NO1 >= m);
+    const int efirst = (cell_o1 == 0) ? 0 : -1;
+    const int elast = (m - 1 - cell_o1 < NO1) ? m - 1 - cell_o1 : -1;
+    constexpr int NPEN = LC * No2;
+    for (int p = tid; p < NPEN; p += NT) {
+      const int ci = p % LC, oj = p / LC;
+      T in[(NO1 + 2) * H];
+#pragma unroll
+      for (int j = 0; j < (NO1 + 2) * H; ++j) in[j] = sA1[(oj * LO1H + j) * PC + ci];
+      T s[No1], t[No1];
+      dg_mass<T, K, NO1, 1>(in, s);
+      if (bnd) dg_sipg<T, K, NO1, true>(in, t, efirst, elast);
+      else dg_sipg<T, K, NO1, false>(in, t, -1, -1);
+      T bb[No1];
+#pragma unroll
+      for (int j = 0; j < No1; ++j) bb[j] = sB1[(oj * No1 + j) * PC + ci];
+      T mb[No1];
+      dg_mass<T, K, NO1, 0>(bb, mb);
+#pragma unroll
+      for (int j = 0; j < No1; ++j) {
+        sS[(oj * No1 + j) * PC + ci] = s[j];
+        sT[(oj * No1 + j) * PC + ci] = t[j] + mb[j];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- pass 3 (along c): y_c = h (L_c S + M_c T) + h^2 D^T Q ;  y_p += h^2 D S ----
+  {
+    using R = Ref<K>;
+    constexpr int P = K + 2;
+    const T h2 = h * h;
+    const T* __restrict__ bc = RESID ? static_cast<const T*>(G.b) + C * sizeV : nullptr;
+    T* __restrict__ yc = y + C * sizeV;
+    constexpr int NPEN = No1 * No2;
+    constexpr int YSC = BR::stride(C, BR::YX, BR::N(1)), YSO1 = BR::stride(O1, BR::YX, BR::N(1)),
+                  YSO2 = BR::stride(O2, BR::YX, BR::N(1));
+    for (int p = tid; p < NPEN; p += NT) {
+      const int oi = p % No1, oj = p / No1;
+      T s[LC], t[LC], q[LC - 1];
+      const int base = (oj * No1 + oi) * PC;
+#pragma unroll
+      for (int j = 0; j < LC; ++j) {
+        s[j] = sS[base + j];
+        t[j] = sT[base + j];
+      }
+#pragma unroll
+      for (int j = 0; j < LC - 1; ++j) q[j] = sQ[base + j];
+      int g[3];
+      g[O1] = G.g0[O1] + oi;
+      g[O2] = G.g0[O2] + oj;
+      const bool inside = g[O1] < n && g[O2] < n;
+      T* yp = sYP + oi * YSO1 + oj * YSO2;
+#pragma unroll
+      for (int e = 0; e < NCc; ++e) {
+#pragma unroll
+        for (int a = 0; a < H; ++a) {
+          const int j = e * H + a + H;  // pencil index of the output node
+          T v = T(0), w = T(0);
+#pragma unroll
+          for (int bq = 0; bq < P; ++bq) {
+            v += cref<T>(R::LP + a * P + bq) * s[j - a + bq] + cref<T>(R::MP + a * P + bq) * t[j - a + bq];
+            if (a == 0)
+              v += cref<T>(R::LP + (K + 1) * P + bq) * s[j - H + bq] + cref<T>(R::MP + (K + 1) * P + bq) * t[j - H + bq];
+          }
+#pragma unroll
+          for (int i = 0; i < H; ++i) {
+            w += cref<T>(R::D + i * P + a) * q[j - a + i];
+            if (a == 0) w += cref<T>(R::D + i * P + H) * q[j - H + i];
+          }
+          g[C] = G.g0[C] + e * H + a;
+          if (inside && g[C] < n) {
+            const int64_t gi = g[0] * st[0] + g[1] * st[1] + g[2] * st[2];
+            T r = h * v + h2 * w;
+            if (g[C] == 0) r = T(0);  // constrained boundary-normal row
+            else if (RESID) r = bc[gi] - r;
+            yc[gi] = r;
+          }
+        }
+        // pressure rows of cell e: y_p += h^2 D S
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+          T z = T(0);
+#pragma unroll
+          for (int bq = 0; bq < P; ++bq) z += cref<T>(R::D + i * P + bq) * s[e * H + H + bq];
+          yp[(e * H + i) * YSC] += h2 * z;
+        }
+      }
+      // the constrained plane g_c = n belongs to the brick holding the last cell along c
+      if (inside && G.c0[C] + NCc >= m) {
+        g[C] = n;
+        yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T, int K, int BX, int BY, int BZ, int NT, bool RESID>
+__global__ void __launch_bounds__(NT) stokes_vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                          const T* __restrict__ b, int m, T h) {
+  using BR = Brick<K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  Geo G;
+  G.m = m;
+  G.n = m * H;
+  G.c0[0] = blockIdx.x * BX;
+  G.c0[1] = blockIdx.y * BY;
+  G.c0[2] = blockIdx.z * BZ;
+  for (int a = 0; a < 3; ++a) G.g0[a] = G.c0[a] * H;
+  G.x = x;
+  G.y = y;
+  G.b = b;
+  const int n = G.n;
+  const int64_t offP = 3 * static_cast<int64_t>(n + 1) * n * n;
+  // pressure box [-H, N_a) on every axis, x fastest (padded rows), and zeroed y_p accumulator
+  {
+    T* sP = sm + BR::OFF_P;
+    constexpr int E0 = BR::N(0) + H, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
+    for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
+      const int lx = i % E0, ly = (i / E0) % E1, lz = i / (E0 * E1);
+      const int gx = G.g0[0] + lx - H, gy = G.g0[1] + ly - H, gz = G.g0[2] + lz - H;
+      T v = T(0);
+      if (gx >= 0 && gy >= 0 && gz >= 0 && gx < n && gy < n && gz < n)
+        v = __ldg(x + offP + (static_cast<int64_t>(gz) * n + gy) * n + gx);
+      sP[(lz * E1 + ly) * BR::PX + lx] = v;
+    }
+    T* sYP = sm + BR::OFF_YP;
+    for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
+  }
+  __syncthreads();
+  component<T, K, BX, BY, BZ, NT, 0, RESID>(sm, G, h);
+  component<T, K, BX, BY, BZ, NT, 1, RESID>(sm, G, h);
+  component<T, K, BX, BY, BZ, NT, 2, RESID>(sm, G, h);
+  // write the pressure rows
+  {
+    const T* sYP = sm + BR::OFF_YP;
+    constexpr int N0 = BR::N(0), N1 = BR::N(1), N2 = BR::N(2);
+    for (int i = threadIdx.x; i < N0 * N1 * N2; i += NT) {
+      const int lx = i % N0, ly = (i / N0) % N1, lz = i / (N0 * N1);
+      const int gx = G.g0[0] + lx, gy = G.g0[1] + ly, gz = G.g0[2] + lz;
+      if (gx >= n || gy >= n || gz >= n) continue;
+      const int64_t gi = offP + (static_cast<int64_t>(gz) * n + gy) * n + gx;
+      const T v = sYP[(lz * N1 + ly) * BR::YX + lx];
+      y[gi] = RESID ? b[gi] - v : v;
+    }
   }
 }
 
-template <typename T, int K, int TX, int TY, int TZ>
+template <typename T, int K, int BX, int BY, int BZ, int NT>
 void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
-  using PL = Plan<K, TX, TY, TZ>;
+  using BR = Brick<K, BX, BY, BZ>;
   const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
   const int m = dl.lay.m;
-  dim3 grid((m + TX - 1) / TX, (m + TY - 1) / TY, (m + TZ - 1) / TZ);
-  const size_t smem = sizeof(T) * PL::TOTAL;
+  const T h = static_cast<T>(1.0 / m);
+  dim3 grid((m + BX - 1) / BX, (m + BY - 1) / BY, (m + BZ - 1) / BZ);
+  const size_t smem = sizeof(T) * BR::TOTAL;
   if (b) {
-    auto kern = stokes_vmult_kernel<T, K, TX, TY, TZ, true>;
+    auto kern = stokes_vmult_kernel<T, K, BX, BY, BZ, NT, true>;
     SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, 256, smem, ctx.stream>>>(static_cast<const T*>(x), static_cast<T*>(y), static_cast<const T*>(b),
-                                          static_cast<const T*>(dl.ops), m);
+    kern<<<grid, NT, smem, ctx.stream>>>(static_cast<const T*>(x), static_cast<T*>(y), static_cast<const T*>(b), m,
+                                         h);
   } else {
-    auto kern = stokes_vmult_kernel<T, K, TX, TY, TZ, false>;
+    auto kern = stokes_vmult_kernel<T, K, BX, BY, BZ, NT, false>;
     SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, 256, smem, ctx.stream>>>(static_cast<const T*>(x), static_cast<T*>(y), nullptr,
-                                          static_cast<const T*>(dl.ops), m);
+    kern<<<grid, NT, smem, ctx.stream>>>(static_cast<const T*>(x), static_cast<T*>(y), nullptr, m, h);
   }
   SMG_CUDA(cudaGetLastError());
   ++ctx.launches;
@@ -268,18 +432,25 @@ void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
 template <typename T>
 void launch_prec(Context& ctx, int level, void* y, const void* x, const void* b) {
   switch (ctx.cfg.degree) {
-    case 1: launch_t<T, 1, 8, 4, 4>(ctx, level, y, x, b); break;
-    case 2: launch_t<T, 2, 4, 4, 4>(ctx, level, y, x, b); break;
-    case 3: launch_t<T, 3, 4, 2, 2>(ctx, level, y, x, b); break;
-    case 4: launch_t<T, 4, 2, 2, 2>(ctx, level, y, x, b); break;
-    case 5: launch_t<T, 5, 2, 2, 1>(ctx, level, y, x, b); break;
-    case 6: launch_t<T, 6, 2, 1, 1>(ctx, level, y, x, b); break;
-    case 7: launch_t<T, 7, 2, 1, 1>(ctx, level, y, x, b); break;
+    case 1: launch_t<T, 1, 8, 4, 4, 256>(ctx, level, y, x, b); break;
+    case 2: launch_t<T, 2, 4, 4, 4, 256>(ctx, level, y, x, b); break;
+    case 3: launch_t<T, 3, 4, 2, 2, 256>(ctx, level, y, x, b); break;
+    case 4: launch_t<T, 4, 2, 2, 2, 256>(ctx, level, y, x, b); break;
+    case 5: launch_t<T, 5, 2, 2, 1, 256>(ctx, level, y, x, b); break;
+    case 6: launch_t<T, 6, 2, 1, 1, 256>(ctx, level, y, x, b); break;
+    case 7: launch_t<T, 7, 2, 1, 1, 256>(ctx, level, y, x, b); break;
     default: throw std::invalid_argument("degree not supported by the vmult kernel (1..7)");
   }
 }
 
 }  // namespace
+
+void upload_reference_tables() {
+  const std::vector<double> t = reference_cell_tables();
+  std::vector<float> f(t.begin(), t.end());
+  SMG_CUDA(cudaMemcpyToSymbol(c_ref_d, t.data(), sizeof(double) * t.size()));
+  SMG_CUDA(cudaMemcpyToSymbol(c_ref_f, f.data(), sizeof(float) * f.size()));
+}
 
 void launch_vmult(Context& ctx, int level, int prec, void* y, const void* x, const void* b) {
   if (prec == SMG_F64) launch_prec<double>(ctx, level, y, x, b);
