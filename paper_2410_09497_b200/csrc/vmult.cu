@@ -19,6 +19,8 @@
 // (16 B/DoF in fp64); the one-cell halos of neighbouring bricks are re-read from L2.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "smg_internal.cuh"
 
 namespace smg {
@@ -50,6 +52,22 @@ struct Ref {
 };
 
 constexpr int odd(int v) { return v | 1; }
+
+// Asynchronous global->shared copy of one element with zero fill (cp.async, LDGSTS): when `ok` is
+// false nothing is read and the destination is zeroed -- this implements the halo outside the
+// domain and the constrained boundary-normal entries without any masking pass.
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* dst, const T* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int n = ok ? static_cast<int>(sizeof(T)) : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(src), "n"(sizeof(T)), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 // ---------------------------------------------------------------------------------------------
 // register-pencil banded operators
@@ -130,14 +148,15 @@ struct Brick {
   static constexpr int PBOX = (N(2) + H) * (N(1) + H) * PX;
   static constexpr int YX = odd(N(0));
   static constexpr int YP = N(2) * N(1) * YX;
-  static constexpr bool ALIAS = 2 * ST <= U;  // S and T overwrite the dead U buffer
-  // layout: [U][A1 (also Q2)][B1][Q][P box][YP][S,T if no alias]
-  static constexpr int OFF_A1 = U;
+  static constexpr bool ALIAS = 2 * ST <= U;  // S and T overwrite the dead U buffer of the component
+  // layout: [U buffer 0][U buffer 1][A1 (also Q2)][B1][Q][P box][YP][S,T if no alias]
+  static constexpr int OFF_U1 = U;
+  static constexpr int OFF_A1 = 2 * U;
   static constexpr int OFF_B1 = OFF_A1 + A1;
   static constexpr int OFF_Q = OFF_B1 + ST;
   static constexpr int OFF_P = OFF_Q + ST;
   static constexpr int OFF_YP = OFF_P + PBOX;
-  static constexpr int OFF_ST = ALIAS ? 0 : OFF_YP + YP;
+  static constexpr int OFF_ST = OFF_YP + YP;  // only used when !ALIAS
   static constexpr int TOTAL = OFF_YP + YP + (ALIAS ? 0 : 2 * ST);
   static constexpr int stride(int axis, int a0, int a1) { return axis == 0 ? 1 : (axis == 1 ? a0 : a0 * a1); }
 };
@@ -152,49 +171,78 @@ struct Geo {
 };
 
 // ---------------------------------------------------------------------------------------------
-// one velocity component
+// asynchronous staging (cp.async with zero fill)
+// ---------------------------------------------------------------------------------------------
+// U box of component C: [-H, N_c] x [-H, N_o1+H) x [-H, N_o2+H), walked in global axis order
+// (x fastest, coalesced), stored c-fastest with an odd (bank-conflict-free) c pitch.
+template <typename T, int K, int BX, int BY, int BZ, int NT, int C>
+__device__ __forceinline__ void issue_u(T* sU, const T* __restrict__ x, const Geo& G) {
+  using BR = Brick<K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  constexpr int O1 = BR::O1(C), O2 = BR::O2(C);
+  constexpr int LC = BR::LC(C), PC = BR::PC(C), LO1H = BR::LO1H(C), LO2H = BR::LO2H(C);
+  constexpr int E0 = C == 0 ? LC : (O1 == 0 ? LO1H : LO2H);
+  constexpr int E1 = C == 1 ? LC : (O1 == 1 ? LO1H : LO2H);
+  constexpr int E2 = C == 2 ? LC : (O1 == 2 ? LO1H : LO2H);
+  const int n = G.n;
+  int gd[3] = {n, n, n};
+  gd[C] = n + 1;
+  const T* xc = x + C * (static_cast<int64_t>(n + 1) * n * n);
+  for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
+    const int l[3] = {i % E0 - H, (i / E0) % E1 - H, i / (E0 * E1) - H};
+    const int g[3] = {G.g0[0] + l[0], G.g0[1] + l[1], G.g0[2] + l[2]};
+    bool ok = g[0] >= 0 && g[1] >= 0 && g[2] >= 0 && g[0] < gd[0] && g[1] < gd[1] && g[2] < gd[2];
+    ok = ok && g[C] != 0 && g[C] != n;  // constrained boundary-normal entries read as 0
+    const T* src = ok ? xc + (static_cast<int64_t>(g[2]) * gd[1] + g[1]) * gd[0] + g[0] : xc;
+    cp_async_elem(sU + ((l[O2] + H) * LO1H + (l[O1] + H)) * PC + (l[C] + H), src, ok);
+  }
+}
+
+// pressure box [-H, N_a) on every axis, x fastest with an odd row pitch
+template <typename T, int K, int BX, int BY, int BZ, int NT>
+__device__ __forceinline__ void issue_p(T* sP, const T* __restrict__ x, const Geo& G) {
+  using BR = Brick<K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  constexpr int E0 = BR::N(0) + H, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
+  const int n = G.n;
+  const T* xp = x + 3 * (static_cast<int64_t>(n + 1) * n * n);
+  for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
+    const int lx = i % E0, ly = (i / E0) % E1, lz = i / (E0 * E1);
+    const int gx = G.g0[0] + lx - H, gy = G.g0[1] + ly - H, gz = G.g0[2] + lz - H;
+    const bool ok = gx >= 0 && gy >= 0 && gz >= 0 && gx < n && gy < n && gz < n;
+    const T* src = ok ? xp + (static_cast<int64_t>(gz) * n + gy) * n + gx : xp;
+    cp_async_elem(sP + (lz * E1 + ly) * BR::PX + lx, src, ok);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// one velocity component (U already staged in sU); if C == 2 and Gn != nullptr, the next brick's
+// pressure box is issued as soon as this brick's P box is dead.
 // ---------------------------------------------------------------------------------------------
 template <typename T, int K, int BX, int BY, int BZ, int NT, int C, bool RESID>
-__device__ __forceinline__ void component(T* sm, const Geo& G, T h) {
+__device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const Geo* Gn) {
   using BR = Brick<K, BX, BY, BZ>;
   constexpr int H = K + 1;
   constexpr int O1 = BR::O1(C), O2 = BR::O2(C);
   constexpr int NCc = BR::B(C), NO1 = BR::B(O1), NO2 = BR::B(O2);
   constexpr int Nc = BR::N(C), No1 = BR::N(O1), No2 = BR::N(O2);
-  constexpr int LC = BR::LC(C), PC = BR::PC(C), LO1H = BR::LO1H(C), LO2H = BR::LO2H(C);
+  constexpr int LC = BR::LC(C), PC = BR::PC(C), LO1H = BR::LO1H(C);
   const int tid = threadIdx.x;
   const int n = G.n, m = G.m;
-  const T* __restrict__ x = static_cast<const T*>(G.x);
   T* __restrict__ y = static_cast<T*>(G.y);
   const int64_t sizeV = static_cast<int64_t>(n + 1) * n * n;
   int64_t gd[3] = {n, n, n};
   gd[C] = n + 1;
   const int64_t st[3] = {1, gd[0], gd[0] * gd[1]};
-  const T* __restrict__ xc = x + C * sizeV;
 
-  T* sU = sm;
   T* sA1 = sm + BR::OFF_A1;
   T* sB1 = sm + BR::OFF_B1;
   T* sQ = sm + BR::OFF_Q;
-  const T* sP = sm + BR::OFF_P;
+  T* sP = sm + BR::OFF_P;
   T* sYP = sm + BR::OFF_YP;
-  T* sS = sm + BR::OFF_ST;
+  T* sS = BR::ALIAS ? sU : sm + BR::OFF_ST;
   T* sT = sS + BR::ST;
 
-  // ---- stage U: box [-H, N_c] x [-H, N_o1+H) x [-H, N_o2+H) in global axis order (x fastest) ----
-  {
-    constexpr int E0 = C == 0 ? LC : (O1 == 0 ? LO1H : LO2H);
-    constexpr int E1 = C == 1 ? LC : (O1 == 1 ? LO1H : LO2H);
-    constexpr int E2 = C == 2 ? LC : (O1 == 2 ? LO1H : LO2H);
-    for (int i = tid; i < E0 * E1 * E2; i += NT) {
-      const int l[3] = {i % E0 - H, (i / E0) % E1 - H, i / (E0 * E1) - H};
-      const int g[3] = {G.g0[0] + l[0], G.g0[1] + l[1], G.g0[2] + l[2]};
-      bool ok = g[0] >= 0 && g[1] >= 0 && g[2] >= 0 && g[0] < gd[0] && g[1] < gd[1] && g[2] < gd[2];
-      ok = ok && g[C] != 0 && g[C] != n;
-      const T v = ok ? __ldg(xc + g[0] + g[1] * st[1] + g[2] * st[2]) : T(0);
-      sU[((l[O2] + H) * LO1H + (l[O1] + H)) * PC + (l[C] + H)] = v;
-    }
-  }
   // ---- Q2 = M_o2 p over c in [-H, N_c), o1 owned, o2 owned  (pencils along o2, from the P box) ----
   {
     T* sQ2 = sA1;
@@ -214,6 +262,8 @@ __device__ __forceinline__ void component(T* sm, const Geo& G, T h) {
       for (int j = 0; j < No2; ++j) sQ2[(j * No1 + oi) * PC + ci] = out[j];
     }
     __syncthreads();
+    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, NT>(sP, static_cast<const T*>(G.x), *Gn);
+    if (C == 2) cp_async_commit();
     // Q = M_o1 Q2 (pencils along o1)
     constexpr int NPEN2 = (Nc + H) * No2;
     for (int p = tid; p < NPEN2; p += NT) {
@@ -354,57 +404,82 @@ __device__ __forceinline__ void component(T* sm, const Geo& G, T h) {
   __syncthreads();
 }
 
+__device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, int bx, int by, int bz, int H) {
+  const int ix = brick % nbx, iy = (brick / nbx) % nby, iz = brick / (nbx * nby);
+  G.c0[0] = ix * bx;
+  G.c0[1] = iy * by;
+  G.c0[2] = iz * bz;
+  for (int a = 0; a < 3; ++a) G.g0[a] = G.c0[a] * H;
+}
+
+// Persistent kernel: each CTA walks bricks blockIdx.x, blockIdx.x + gridDim.x, ... The three
+// component boxes of a brick alternate between two U buffers so that the cp.async staging of the
+// next component (and of the next brick's first component and pressure box) overlaps compute.
 template <typename T, int K, int BX, int BY, int BZ, int NT, bool RESID>
-__global__ void __launch_bounds__(NT) stokes_vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                                          const T* __restrict__ b, int m, T h) {
+__global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                             const T* __restrict__ b, int m, T h) {
   using BR = Brick<K, BX, BY, BZ>;
   constexpr int H = K + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  Geo G;
-  G.m = m;
-  G.n = m * H;
-  G.c0[0] = blockIdx.x * BX;
-  G.c0[1] = blockIdx.y * BY;
-  G.c0[2] = blockIdx.z * BZ;
-  for (int a = 0; a < 3; ++a) G.g0[a] = G.c0[a] * H;
-  G.x = x;
-  G.y = y;
-  G.b = b;
+  const int nbx = (m + BX - 1) / BX, nby = (m + BY - 1) / BY, nbz = (m + BZ - 1) / BZ;
+  const int nbricks = nbx * nby * nbz;
+  Geo G, Gn;
+  G.m = Gn.m = m;
+  G.n = Gn.n = m * H;
+  G.x = Gn.x = x;
+  G.y = Gn.y = y;
+  G.b = Gn.b = b;
   const int n = G.n;
   const int64_t offP = 3 * static_cast<int64_t>(n + 1) * n * n;
-  // pressure box [-H, N_a) on every axis, x fastest (padded rows), and zeroed y_p accumulator
-  {
-    T* sP = sm + BR::OFF_P;
-    constexpr int E0 = BR::N(0) + H, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
-    for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
-      const int lx = i % E0, ly = (i / E0) % E1, lz = i / (E0 * E1);
-      const int gx = G.g0[0] + lx - H, gy = G.g0[1] + ly - H, gz = G.g0[2] + lz - H;
-      T v = T(0);
-      if (gx >= 0 && gy >= 0 && gz >= 0 && gx < n && gy < n && gz < n)
-        v = __ldg(x + offP + (static_cast<int64_t>(gz) * n + gy) * n + gx);
-      sP[(lz * E1 + ly) * BR::PX + lx] = v;
-    }
-    T* sYP = sm + BR::OFF_YP;
+  T* sP = sm + BR::OFF_P;
+  T* sYP = sm + BR::OFF_YP;
+  int brick = blockIdx.x;
+  if (brick >= nbricks) return;
+  brick_geo(G, brick, nbx, nby, BX, BY, BZ, H);
+  issue_p<T, K, BX, BY, BZ, NT>(sP, x, G);
+  issue_u<T, K, BX, BY, BZ, NT, 0>(sm, x, G);
+  cp_async_commit();
+  int u0 = 0;
+  for (; brick < nbricks; brick += gridDim.x) {
+    T* bufA = sm + (u0 ? BR::OFF_U1 : 0);  // components 0 and 2 of this brick
+    T* bufB = sm + (u0 ? 0 : BR::OFF_U1);  // component 1, then component 0 of the next brick
+    const int next = brick + gridDim.x;
+    const bool has_next = next < nbricks;
+    if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H);
+    issue_u<T, K, BX, BY, BZ, NT, 1>(bufB, x, G);
+    cp_async_commit();
     for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
-  }
-  __syncthreads();
-  component<T, K, BX, BY, BZ, NT, 0, RESID>(sm, G, h);
-  component<T, K, BX, BY, BZ, NT, 1, RESID>(sm, G, h);
-  component<T, K, BX, BY, BZ, NT, 2, RESID>(sm, G, h);
-  // write the pressure rows
-  {
-    const T* sYP = sm + BR::OFF_YP;
-    constexpr int N0 = BR::N(0), N1 = BR::N(1), N2 = BR::N(2);
-    for (int i = threadIdx.x; i < N0 * N1 * N2; i += NT) {
-      const int lx = i % N0, ly = (i / N0) % N1, lz = i / (N0 * N1);
-      const int gx = G.g0[0] + lx, gy = G.g0[1] + ly, gz = G.g0[2] + lz;
-      if (gx >= n || gy >= n || gz >= n) continue;
-      const int64_t gi = offP + (static_cast<int64_t>(gz) * n + gy) * n + gx;
-      const T v = sYP[(lz * N1 + ly) * BR::YX + lx];
-      y[gi] = RESID ? b[gi] - v : v;
+    cp_async_wait<1>();  // P box and U_0 of this brick
+    __syncthreads();
+    component<T, K, BX, BY, BZ, NT, 0, RESID>(sm, bufA, G, h, nullptr);
+    issue_u<T, K, BX, BY, BZ, NT, 2>(bufA, x, G);
+    cp_async_commit();
+    cp_async_wait<1>();  // U_1
+    __syncthreads();
+    component<T, K, BX, BY, BZ, NT, 1, RESID>(sm, bufB, G, h, nullptr);
+    if (has_next) issue_u<T, K, BX, BY, BZ, NT, 0>(bufB, x, Gn);
+    cp_async_commit();
+    cp_async_wait<1>();  // U_2
+    __syncthreads();
+    component<T, K, BX, BY, BZ, NT, 2, RESID>(sm, bufA, G, h, has_next ? &Gn : nullptr);
+    // write the pressure rows of this brick
+    {
+      constexpr int N0 = BR::N(0), N1 = BR::N(1), N2 = BR::N(2);
+      for (int i = threadIdx.x; i < N0 * N1 * N2; i += NT) {
+        const int lx = i % N0, ly = (i / N0) % N1, lz = i / (N0 * N1);
+        const int gx = G.g0[0] + lx, gy = G.g0[1] + ly, gz = G.g0[2] + lz;
+        if (gx >= n || gy >= n || gz >= n) continue;
+        const int64_t gi = offP + (static_cast<int64_t>(gz) * n + gy) * n + gx;
+        const T v = sYP[(lz * N1 + ly) * BR::YX + lx];
+        y[gi] = RESID ? b[gi] - v : v;
+      }
     }
+    __syncthreads();  // y_p accumulator is re-zeroed by the next brick
+    G = Gn;
+    u0 ^= 1;
   }
+  cp_async_wait<0>();
 }
 
 template <typename T, int K, int BX, int BY, int BZ, int NT>
@@ -413,7 +488,10 @@ void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
   const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
   const int m = dl.lay.m;
   const T h = static_cast<T>(1.0 / m);
-  dim3 grid((m + BX - 1) / BX, (m + BY - 1) / BY, (m + BZ - 1) / BZ);
+  const int nbricks = ((m + BX - 1) / BX) * ((m + BY - 1) / BY) * ((m + BZ - 1) / BZ);
+  static int num_sms = 0;
+  if (num_sms == 0) SMG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ctx.device));
+  const dim3 grid(std::min(nbricks, num_sms));
   const size_t smem = sizeof(T) * BR::TOTAL;
   if (b) {
     auto kern = stokes_vmult_kernel<T, K, BX, BY, BZ, NT, true>;
