@@ -1,319 +1,333 @@
 // K3: vertex-patch multiplicative Schwarz smoother, one colour per launch (smooth SPEC.md:400-408,
-// Alg. 2). One CTA owns one patch (the 8 cells around an interior vertex) of the
-// colour; it gathers the patch residual into shared memory, runs the local Schur-complement solve
-// (schur_solve SPEC.md:356-364) entirely in shared memory —
-//   S P = B A^-1 F - G,  S = B A^-1 B^T (fast diagonalisation, Eq. 9), projected CG with
-//   the pressure-mass preconditioner —
-// and adds R^T (U, P) into x. Same-colour patches write disjoint DoFs, so the update is
-// race-free and independent of CTA order. The residual r = b - A x is refreshed per colour by the
-// vmult kernel in residual mode.
+// Alg. 2), local solver = Schur complement + fast diagonalisation
+// (schur_solve SPEC.md:356-364, Eq. 9):
+//   S P = B A^-1 F - G,   S = B A^-1 B^T,   U = A^-1 (F - B^T P),
+// with projected, pressure-mass-preconditioned CG on the patch pressure.
+//
+// B200 design: ONE WARP PER PATCH. All patch vectors live in the warp's slice of shared memory;
+// every step is a warp-synchronous pencil contraction with compile-time shapes (no CTA barriers).
+// Per component c and axis a, the fast-diagonalisation eigenvectors S_a are pre-multiplied with
+// the divergence factor of that axis at setup (G_a = D S_par along c, G_a = M' S_orth otherwise),
+// so B_c A_c^-1 B_c^T = (G (x) G (x) G) Lambda_c^-1 (G (x) G (x) G)^T costs 6 contractions instead of
+// 12, and the final velocity is U_c = (S (x) S (x) S) Lambda_c^-1 [S^T F_c - G^T P] re-using the
+// eigen-coefficients of F computed once. Same-colour patches write disjoint DoFs, so
+// the scatter is race-free and order-independent. The residual r = b - A x is refreshed per colour by
+// the vmult kernel in residual mode.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "smg_internal.cuh"
 
 namespace smg {
 namespace {
 
-constexpr int kPatchThreads = 128;
-
 template <int K>
-struct PatchDims {
-  static constexpr int NP = 2 * K + 1;  // parallel (C0, interior nodes)
+struct PD {
+  static constexpr int NP = 2 * K + 1;  // parallel (C0 interior nodes of the 2-cell patch)
   static constexpr int NO = 2 * K + 2;  // orthogonal (DG) / pressure
   static constexpr int NV = NP * NO * NO;
   static constexpr int NPR = NO * NO * NO;
-  // packed table offsets
-  static constexpr int PAR_S = 0;
-  static constexpr int PAR_L = PAR_S + NP * NP;
-  static constexpr int ORTH_S = PAR_L + NP;
-  static constexpr int ORTH_L = ORTH_S + 4 * NO * NO;
-  static constexpr int DM = ORTH_L + 4 * NO;
-  static constexpr int MP = DM + NO * NP;
-  static constexpr int MPI = MP + NO * NO;
+  static constexpr int BIG = NV > NPR ? NV : NPR;
+  // packed table offsets (pack_patch_tables)
+  static constexpr int PAR_S = 0;                     // NP x NP
+  static constexpr int PAR_L = PAR_S + NP * NP;       // NP
+  static constexpr int ORTH_S = PAR_L + NP;           // 4 x NO x NO
+  static constexpr int ORTH_L = ORTH_S + 4 * NO * NO;  // 4 x NO
+  static constexpr int G_PAR = ORTH_L + 4 * NO;       // NO x NP  (D S_par)
+  static constexpr int G_ORTH = G_PAR + NO * NP;      // 4 x NO x NO (M' S_orth)
+  static constexpr int MPI = G_ORTH + 4 * NO * NO;    // NO x NO (M'^-1)
   static constexpr int TAB = MPI + NO * NO;
+  static constexpr int TABP = (TAB + 3) / 4 * 4;
+  // per-warp workspace: Fh (3 NV) | r z d q x (5 NPR) | T1 T2 (2 BIG)
+  static constexpr int WS = 3 * NV + 5 * NPR + 2 * BIG;
+  static constexpr int dv(int c, int a) { return a == c ? NP : NO; }
 };
 
-template <typename T>
-__device__ __forceinline__ T block_sum(T v, T* red) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();  // protect red from a previous use
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  T s = T(0);
+// out = (M applied along axis AX) in;  in dims (D0,D1,D2), out extent along AX = R.
+// M(i,j) = TRANS ? A[j*LDA + i] : A[i*LDA + j]. One pencil per lane, coefficients broadcast from SMEM.
+template <typename T, int D0, int D1, int D2, int AX, int R, int LDA, bool TRANS>
+__device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __restrict__ A, T* __restrict__ out,
+                                          int lane) {
+  constexpr int DI[3] = {D0, D1, D2};
+  constexpr int C = DI[AX];
+  constexpr int DO0 = AX == 0 ? R : D0, DO1 = AX == 1 ? R : D1;
+  constexpr int SI = AX == 0 ? 1 : (AX == 1 ? D0 : D0 * D1);
+  constexpr int SO = AX == 0 ? 1 : (AX == 1 ? DO0 : DO0 * DO1);
+  constexpr int QA = AX == 0 ? D1 : D0;  // the two other axes, in order
+  constexpr int NPEN = D0 * D1 * D2 / C;
+  for (int p = lane; p < NPEN; p += 32) {
+    const int u = p % QA, v = p / QA;
+    int bi, bo;
+    if (AX == 0) {
+      bi = (v * D1 + u) * D0;
+      bo = (v * DO1 + u) * DO0;
+    } else if (AX == 1) {
+      bi = v * D0 * D1 + u;
+      bo = v * DO0 * DO1 + u;
+    } else {
+      bi = v * D0 + u;
+      bo = v * DO0 + u;
+    }
+    T x[C];
 #pragma unroll
-  for (int w = 0; w < kPatchThreads / 32; ++w) s += red[w];
-  return s;
+    for (int j = 0; j < C; ++j) x[j] = in[bi + j * SI];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      T s = T(0);
+#pragma unroll
+      for (int j = 0; j < C; ++j) s += (TRANS ? A[j * LDA + i] : A[i * LDA + j]) * x[j];
+      out[bo + i * SO] = s;
+    }
+  }
 }
 
-// out (dims with axis ax replaced by R) = M applied along axis ax of in (dims d)
-// M(i,j) = trans ? A[j*lda + i] : A[i*lda + j], j < C = d[ax]
 template <typename T>
-__device__ void axis_apply(const T* __restrict__ in, int d0, int d1, int d2, int ax, const T* __restrict__ A, int lda,
-                           int R, bool trans, T* __restrict__ out) {
-  int din[3] = {d0, d1, d2};
-  int dout[3] = {d0, d1, d2};
-  const int C = din[ax];
-  dout[ax] = R;
-  const int sin_ax = ax == 0 ? 1 : (ax == 1 ? d0 : d0 * d1);
-  const int total = dout[0] * dout[1] * dout[2];
-  for (int o = threadIdx.x; o < total; o += blockDim.x) {
-    const int x = o % dout[0], y = (o / dout[0]) % dout[1], z = o / (dout[0] * dout[1]);
-    const int q[3] = {x, y, z};
-    const int i = q[ax];
-    int base[3] = {x, y, z};
-    base[ax] = 0;
-    const T* src = in + (base[2] * din[1] + base[1]) * din[0] + base[0];
-    T s = T(0);
-    if (trans)
-      for (int j = 0; j < C; ++j) s += A[j * lda + i] * src[j * sin_ax];
-    else
-      for (int j = 0; j < C; ++j) s += A[i * lda + j] * src[j * sin_ax];
-    out[o] = s;
-  }
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
 template <typename T, int K>
-struct PatchSolver {
-  using PD = PatchDims<K>;
+struct Patch {
+  using P = PD<K>;
   const T* tab;
-  int var[3];  // orthogonal-axis variant per axis
-  T* red;
+  int var[3];
+  int lane;
 
   __device__ const T* S(int c, int a) const {
-    return a == c ? tab + PD::PAR_S : tab + PD::ORTH_S + var[a] * PD::NO * PD::NO;
+    return a == c ? tab + P::PAR_S : tab + P::ORTH_S + var[a] * P::NO * P::NO;
   }
-  __device__ const T* L(int c, int a) const { return a == c ? tab + PD::PAR_L : tab + PD::ORTH_L + var[a] * PD::NO; }
-  __device__ int dim(int c, int a) const { return a == c ? PD::NP : PD::NO; }
+  __device__ const T* L(int c, int a) const { return a == c ? tab + P::PAR_L : tab + P::ORTH_L + var[a] * P::NO; }
+  __device__ const T* G(int c, int a) const {
+    return a == c ? tab + P::G_PAR : tab + P::G_ORTH + var[a] * P::NO * P::NO;
+  }
 
-  // out = A_c^-1 in (fast diagonalisation); t is scratch of NV. in may alias out.
-  __device__ void ainv(int c, const T* in, T* out, T* t) const {
-    const int d0 = dim(c, 0), d1 = dim(c, 1), d2 = dim(c, 2);
-    axis_apply(in, d0, d1, d2, 0, S(c, 0), d0, d0, true, t);
-    __syncthreads();
-    axis_apply(t, d0, d1, d2, 1, S(c, 1), d1, d1, true, out);
-    __syncthreads();
-    axis_apply(out, d0, d1, d2, 2, S(c, 2), d2, d2, true, t);
-    __syncthreads();
-    const T* l0 = L(c, 0);
-    const T* l1 = L(c, 1);
-    const T* l2 = L(c, 2);
-    for (int o = threadIdx.x; o < PD::NV; o += blockDim.x) {
-      const int x = o % d0, y = (o / d0) % d1, z = o / (d0 * d1);
-      t[o] /= (l0[x] + l1[y] + l2[z]);
+  // eigen-space transforms of a velocity-shaped array of component C (S square per axis):
+  // out = (S0 (x) S1 (x) S2)^T in (TR = true) or (S0 (x) S1 (x) S2) in; uses tmp; out != in.
+  template <int C, bool TR>
+  __device__ void s3(const T* in, T* out, T* tmp) const {
+    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
+    warp_axis<T, A0, A1, A2, 0, A0, A0, TR>(in, S(C, 0), out, lane);
+    __syncwarp();
+    warp_axis<T, A0, A1, A2, 1, A1, A1, TR>(out, S(C, 1), tmp, lane);
+    __syncwarp();
+    warp_axis<T, A0, A1, A2, 2, A2, A2, TR>(tmp, S(C, 2), out, lane);
+    __syncwarp();
+  }
+  // pressure (NO^3) -> eigen space of component C: out = (G0 (x) G1 (x) G2)^T in
+  template <int C>
+  __device__ void gt3(const T* in, T* out, T* tmp) const {
+    constexpr int NO = P::NO;
+    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
+    warp_axis<T, NO, NO, NO, 0, A0, A0, true>(in, G(C, 0), out, lane);
+    __syncwarp();
+    warp_axis<T, A0, NO, NO, 1, A1, A1, true>(out, G(C, 1), tmp, lane);
+    __syncwarp();
+    warp_axis<T, A0, A1, NO, 2, A2, A2, true>(tmp, G(C, 2), out, lane);
+    __syncwarp();
+  }
+  // eigen space of component C -> pressure: out = (G0 (x) G1 (x) G2) in
+  template <int C>
+  __device__ void g3(const T* in, T* out, T* tmp) const {
+    constexpr int NO = P::NO;
+    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
+    warp_axis<T, A0, A1, A2, 0, NO, A0, false>(in, G(C, 0), out, lane);
+    __syncwarp();
+    warp_axis<T, NO, A1, A2, 1, NO, A1, false>(out, G(C, 1), tmp, lane);
+    __syncwarp();
+    warp_axis<T, NO, NO, A2, 2, NO, A2, false>(tmp, G(C, 2), out, lane);
+    __syncwarp();
+  }
+  // t *= Lambda_C^-1 (eigen space of component C)
+  template <int C>
+  __device__ void lam_inv(T* t) const {
+    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1);
+    const T* l0 = L(C, 0);
+    const T* l1 = L(C, 1);
+    const T* l2 = L(C, 2);
+    for (int o = lane; o < P::NV; o += 32) {
+      const int x = o % A0, y = (o / A0) % A1, z = o / (A0 * A1);
+      t[o] = t[o] / (l0[x] + l1[y] + l2[z]);
     }
-    __syncthreads();
-    axis_apply(t, d0, d1, d2, 2, S(c, 2), d2, d2, false, out);
-    __syncthreads();
-    axis_apply(out, d0, d1, d2, 1, S(c, 1), d1, d1, false, t);
-    __syncthreads();
-    axis_apply(t, d0, d1, d2, 0, S(c, 0), d0, d0, false, out);
-    __syncthreads();
-  }
-  // p (NPR) = B_c u ; t scratch of max(NV,NPR)*... two buffers t1,t2 of NPR
-  __device__ void bmul(int c, const T* u, T* p, T* t1) const {
-    // along c: D (NO x NP); others: Mp (NO x NO)
-    int d[3] = {dim(c, 0), dim(c, 1), dim(c, 2)};
-    const T* Dm = tab + PD::DM;
-    const T* Mp = tab + PD::MP;
-    axis_apply(u, d[0], d[1], d[2], 0, c == 0 ? Dm : Mp, c == 0 ? PD::NP : PD::NO, PD::NO, false, t1);
-    d[0] = PD::NO;
-    __syncthreads();
-    axis_apply(t1, d[0], d[1], d[2], 1, c == 1 ? Dm : Mp, c == 1 ? PD::NP : PD::NO, PD::NO, false, p);
-    d[1] = PD::NO;
-    __syncthreads();
-    axis_apply(p, d[0], d[1], d[2], 2, c == 2 ? Dm : Mp, c == 2 ? PD::NP : PD::NO, PD::NO, false, t1);
-    __syncthreads();
-    for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) p[o] = t1[o];
-    __syncthreads();
-  }
-  // u (NV) = B_c^T p
-  __device__ void btmul(int c, const T* p, T* u, T* t1) const {
-    const T* Dm = tab + PD::DM;
-    const T* Mp = tab + PD::MP;
-    int d[3] = {PD::NO, PD::NO, PD::NO};
-    axis_apply(p, d[0], d[1], d[2], 2, c == 2 ? Dm : Mp, c == 2 ? PD::NP : PD::NO, dim(c, 2), true, t1);
-    d[2] = dim(c, 2);
-    __syncthreads();
-    axis_apply(t1, d[0], d[1], d[2], 1, c == 1 ? Dm : Mp, c == 1 ? PD::NP : PD::NO, dim(c, 1), true, u);
-    d[1] = dim(c, 1);
-    __syncthreads();
-    axis_apply(u, d[0], d[1], d[2], 0, c == 0 ? Dm : Mp, c == 0 ? PD::NP : PD::NO, dim(c, 0), true, t1);
-    __syncthreads();
-    for (int o = threadIdx.x; o < PD::NV; o += blockDim.x) u[o] = t1[o];
-    __syncthreads();
+    __syncwarp();
   }
   __device__ void project(T* p) const {
     T s = T(0);
-    for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) s += p[o];
-    s = block_sum(s, red) / T(PD::NPR);
-    for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) p[o] -= s;
-    __syncthreads();
+    for (int o = lane; o < P::NPR; o += 32) s += p[o];
+    s = warp_sum(s) / T(P::NPR);
+    __syncwarp();
+    for (int o = lane; o < P::NPR; o += 32) p[o] -= s;
+    __syncwarp();
   }
-  __device__ T dotp(const T* a, const T* b) const {
+  __device__ T dot(const T* a, const T* b) const {
     T s = T(0);
-    for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) s += a[o] * b[o];
-    return block_sum(s, red);
+    for (int o = lane; o < P::NPR; o += 32) s += a[o] * b[o];
+    return warp_sum(s);
   }
 };
 
-template <typename T, int K>
-__global__ void __launch_bounds__(kPatchThreads) patch_smooth_kernel(T* __restrict__ x, const T* __restrict__ r,
-                                                                     const T* __restrict__ ptab, int m, int colour,
-                                                                     int cg_max_iter, T cg_tol, int cg_fixed,
-                                                                     int cg_precond) {
-  using PD = PatchDims<K>;
-  constexpr int H = K + 1;
+template <typename T, int K, int W>
+__global__ void __launch_bounds__(32 * W) patch_smooth_kernel(T* __restrict__ x, const T* __restrict__ r,
+                                                              const T* __restrict__ ptab, int m, int colour,
+                                                              int cg_max_iter, T cg_tol, int cg_fixed,
+                                                              int cg_precond) {
+  using P = PD<K>;
+  constexpr int H = K + 1, NO = P::NO;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tab = reinterpret_cast<T*>(smem_raw);
-  T* F = tab + ((PD::TAB + 1) / 2) * 2;  // 3 x NV
-  constexpr int BIG = PD::NV > PD::NPR ? PD::NV : PD::NPR;
-  T* V1 = F + 3 * PD::NV;  // velocity scratch (holds NO^3 intermediates of B^T)
-  T* V2 = V1 + BIG;        // scratch
-  T* Pr = V2 + BIG;       // rhs / residual
-  T* Pz = Pr + PD::NPR;   // preconditioned residual
-  T* Pd = Pz + PD::NPR;   // search direction
-  T* Pq = Pd + PD::NPR;   // S d
-  T* Px = Pq + PD::NPR;   // solution
-  T* Pt = Px + PD::NPR;   // scratch
-  T* red = Pt + PD::NPR;  // 32
+  for (int i = threadIdx.x; i < P::TAB; i += blockDim.x) tab[i] = ptab[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cnt[3] = {(colour & 1) ? m / 2 : m / 2 - 1, ((colour >> 1) & 1) ? m / 2 : m / 2 - 1,
+                      ((colour >> 2) & 1) ? m / 2 : m / 2 - 1};
+  const int npatch = cnt[0] * cnt[1] * cnt[2];
+  const int pid = blockIdx.x * W + warp;
+  if (pid >= npatch) return;
+  const int v[3] = {((colour & 1) ? 1 : 2) + 2 * (pid % cnt[0]), (((colour >> 1) & 1) ? 1 : 2) + 2 * ((pid / cnt[0]) % cnt[1]),
+                    (((colour >> 2) & 1) ? 1 : 2) + 2 * (pid / (cnt[0] * cnt[1]))};
+  T* ws = tab + P::TABP + warp * P::WS;
+  T* Fh = ws;                // 3 x NV eigen coefficients of F_c
+  T* Pr = Fh + 3 * P::NV;    // CG residual
+  T* Pz = Pr + P::NPR;       // preconditioned residual
+  T* Pd = Pz + P::NPR;       // search direction
+  T* Pq = Pd + P::NPR;       // S d
+  T* Px = Pq + P::NPR;       // pressure iterate
+  T* T1 = Px + P::NPR;       // scratch (BIG)
+  T* T2 = T1 + P::BIG;       // scratch (BIG)
 
-  const int v[3] = {((colour & 1) ? 1 : 2) + 2 * static_cast<int>(blockIdx.x),
-                    (((colour >> 1) & 1) ? 1 : 2) + 2 * static_cast<int>(blockIdx.y),
-                    (((colour >> 2) & 1) ? 1 : 2) + 2 * static_cast<int>(blockIdx.z)};
+  Patch<T, K> ps;
+  ps.tab = tab;
+  ps.lane = lane;
+  for (int a = 0; a < 3; ++a) ps.var[a] = 2 * (v[a] == 1) + (v[a] == m - 1);
   const int n = m * H;
   const int64_t sizeV = static_cast<int64_t>(n + 1) * n * n;
 
-  for (int i = threadIdx.x; i < PD::TAB; i += blockDim.x) tab[i] = ptab[i];
-  PatchSolver<T, K> ps;
-  ps.tab = tab;
-  ps.red = red;
-  for (int a = 0; a < 3; ++a) ps.var[a] = 2 * (v[a] == 1) + (v[a] == m - 1);
-
-  // ---- gather R_j r ----
-  for (int c = 0; c < 3; ++c) {
-    const int d0 = ps.dim(c, 0), d1 = ps.dim(c, 1);
-    int64_t gd[3] = {n, n, n};
-    gd[c] = n + 1;
-    int base[3];
-    for (int a = 0; a < 3; ++a) base[a] = (v[a] - 1) * H + (a == c ? 1 : 0);
-    for (int o = threadIdx.x; o < PD::NV; o += blockDim.x) {
-      const int xx = o % d0, yy = (o / d0) % d1, zz = o / (d0 * d1);
-      F[c * PD::NV + o] =
-          r[c * sizeV + (static_cast<int64_t>(base[2] + zz) * gd[1] + base[1] + yy) * gd[0] + base[0] + xx];
-    }
-  }
-  for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) {
-    const int xx = o % PD::NO, yy = (o / PD::NO) % PD::NO, zz = o / (PD::NO * PD::NO);
-    const int gx = (v[0] - 1) * H + xx, gy = (v[1] - 1) * H + yy, gz = (v[2] - 1) * H + zz;
-    Pt[o] = r[3 * sizeV + (static_cast<int64_t>(gz) * n + gy) * n + gx];  // G
-    Pr[o] = T(0);
-  }
-  __syncthreads();
-  // ---- rhs = B A^-1 F - G (projected) ----
-  for (int c = 0; c < 3; ++c) {
-    ps.ainv(c, F + c * PD::NV, V1, V2);
-    ps.bmul(c, V1, Pq, V2);
-    for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) Pr[o] += Pq[o];
-    __syncthreads();
-  }
-  for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) Pr[o] -= Pt[o];
-  __syncthreads();
+  // ---- gather R_j r: velocity blocks -> T1 -> eigen coefficients Fh_c; pressure -> Pq (= G) ----
+  auto vel_index = [&](int c, int o) {
+    const int d0 = P::dv(c, 0), d1 = P::dv(c, 1);
+    const int xx = o % d0, yy = (o / d0) % d1, zz = o / (d0 * d1);
+    int64_t gd0 = n, gd1 = n;
+    if (c == 0) gd0 = n + 1;
+    if (c == 1) gd1 = n + 1;
+    const int b0 = (v[0] - 1) * H + (c == 0), b1 = (v[1] - 1) * H + (c == 1), b2 = (v[2] - 1) * H + (c == 2);
+    return c * sizeV + (static_cast<int64_t>(b2 + zz) * gd1 + b1 + yy) * gd0 + b0 + xx;
+  };
+  auto pres_index = [&](int o) {
+    const int xx = o % NO, yy = (o / NO) % NO, zz = o / (NO * NO);
+    return 3 * sizeV + (static_cast<int64_t>((v[2] - 1) * H + zz) * n + (v[1] - 1) * H + yy) * n + (v[0] - 1) * H + xx;
+  };
+#define SMG_FOR_C(...) \
+  { constexpr int C = 0; __VA_ARGS__ } { constexpr int C = 1; __VA_ARGS__ } { constexpr int C = 2; __VA_ARGS__ }
+  SMG_FOR_C({
+    for (int o = lane; o < P::NV; o += 32) T1[o] = r[vel_index(C, o)];
+    __syncwarp();
+    ps.template s3<C, true>(T1, Fh + C * P::NV, T2);
+  })
+  for (int o = lane; o < P::NPR; o += 32) Pq[o] = r[pres_index(o)];
+  // ---- rhs = sum_c G_c Lambda_c^-1 Fh_c - G  (projected) -> Pr ----
+  for (int o = lane; o < P::NPR; o += 32) Pr[o] = -Pq[o];
+  __syncwarp();
+  SMG_FOR_C({
+    for (int o = lane; o < P::NV; o += 32) T1[o] = Fh[C * P::NV + o];
+    __syncwarp();
+    ps.template lam_inv<C>(T1);
+    ps.template g3<C>(T1, T2, Pq);  // result in T2 (Pq used as scratch)
+    for (int o = lane; o < P::NPR; o += 32) Pr[o] += T2[o];
+    __syncwarp();
+  })
   ps.project(Pr);
   auto precond = [&](const T* rr, T* zz) {
     if (cg_precond) {
-      const T* Mi = tab + PD::MPI;
-      axis_apply(rr, PD::NO, PD::NO, PD::NO, 0, Mi, PD::NO, PD::NO, false, zz);
-      __syncthreads();
-      axis_apply(zz, PD::NO, PD::NO, PD::NO, 1, Mi, PD::NO, PD::NO, false, Pt);
-      __syncthreads();
-      axis_apply(Pt, PD::NO, PD::NO, PD::NO, 2, Mi, PD::NO, PD::NO, false, zz);
-      __syncthreads();
+      const T* Mi = tab + P::MPI;
+      warp_axis<T, NO, NO, NO, 0, NO, NO, false>(rr, Mi, zz, lane);
+      __syncwarp();
+      warp_axis<T, NO, NO, NO, 1, NO, NO, false>(zz, Mi, T1, lane);
+      __syncwarp();
+      warp_axis<T, NO, NO, NO, 2, NO, NO, false>(T1, Mi, zz, lane);
+      __syncwarp();
     } else {
-      for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) zz[o] = rr[o];
-      __syncthreads();
+      for (int o = lane; o < P::NPR; o += 32) zz[o] = rr[o];
+      __syncwarp();
     }
     ps.project(zz);
   };
   precond(Pr, Pz);
-  for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) {
+  for (int o = lane; o < P::NPR; o += 32) {
     Pd[o] = Pz[o];
     Px[o] = T(0);
   }
-  __syncthreads();
-  T rz = ps.dotp(Pr, Pz);
-  const T r0 = sqrt(ps.dotp(Pr, Pr));
+  __syncwarp();
+  T rz = ps.dot(Pr, Pz);
+  const T r0 = sqrt(ps.dot(Pr, Pr));
   for (int it = 0; it < cg_max_iter; ++it) {
     if (!cg_fixed) {
-      const T rr = sqrt(ps.dotp(Pr, Pr));
-      if (rr <= cg_tol * r0) break;
+      if (sqrt(ps.dot(Pr, Pr)) <= cg_tol * r0) break;
     }
-    // q = S d = sum_c B_c A_c^-1 B_c^T d
-    for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) Pq[o] = T(0);
-    __syncthreads();
-    for (int c = 0; c < 3; ++c) {
-      ps.btmul(c, Pd, V1, V2);
-      ps.ainv(c, V1, V1, V2);
-      ps.bmul(c, V1, Pt, V2);
-      for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) Pq[o] += Pt[o];
-      __syncthreads();
-    }
-    const T dq = ps.dotp(Pd, Pq);
+    // Pq = S Pd = sum_c G_c Lambda_c^-1 G_c^T Pd
+    for (int o = lane; o < P::NPR; o += 32) Pq[o] = T(0);
+    __syncwarp();
+    SMG_FOR_C({
+      ps.template gt3<C>(Pd, T1, T2);
+      ps.template lam_inv<C>(T1);
+      ps.template g3<C>(T1, T2, Pz);  // result in T2; Pz is free scratch here (recomputed below)
+      for (int o = lane; o < P::NPR; o += 32) Pq[o] += T2[o];
+      __syncwarp();
+    })
+    const T dq = ps.dot(Pd, Pq);
     if (!(dq > T(0)) || rz == T(0)) break;
     const T alpha = rz / dq;
-    for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) {
+    for (int o = lane; o < P::NPR; o += 32) {
       Px[o] += alpha * Pd[o];
       Pr[o] -= alpha * Pq[o];
     }
-    __syncthreads();
+    __syncwarp();
     ps.project(Pr);
     precond(Pr, Pz);
-    const T rzn = ps.dotp(Pr, Pz);
+    const T rzn = ps.dot(Pr, Pz);
     const T beta = rzn / rz;
     rz = rzn;
-    for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) Pd[o] = Pz[o] + beta * Pd[o];
-    __syncthreads();
+    for (int o = lane; o < P::NPR; o += 32) Pd[o] = Pz[o] + beta * Pd[o];
+    __syncwarp();
   }
   ps.project(Px);
-  // ---- U_c = A_c^-1 (F_c - B_c^T P); x += R^T (U, P) ----
-  for (int c = 0; c < 3; ++c) {
-    ps.btmul(c, Px, V1, V2);
-    T* Fc = F + c * PD::NV;
-    for (int o = threadIdx.x; o < PD::NV; o += blockDim.x) Fc[o] -= V1[o];
-    __syncthreads();
-    ps.ainv(c, Fc, Fc, V2);
-    const int d0 = ps.dim(c, 0), d1 = ps.dim(c, 1);
-    int64_t gd[3] = {n, n, n};
-    gd[c] = n + 1;
-    int base[3];
-    for (int a = 0; a < 3; ++a) base[a] = (v[a] - 1) * H + (a == c ? 1 : 0);
-    for (int o = threadIdx.x; o < PD::NV; o += blockDim.x) {
-      const int xx = o % d0, yy = (o / d0) % d1, zz = o / (d0 * d1);
-      x[c * sizeV + (static_cast<int64_t>(base[2] + zz) * gd[1] + base[1] + yy) * gd[0] + base[0] + xx] += Fc[o];
-    }
-  }
-  for (int o = threadIdx.x; o < PD::NPR; o += blockDim.x) {
-    const int xx = o % PD::NO, yy = (o / PD::NO) % PD::NO, zz = o / (PD::NO * PD::NO);
-    const int gx = (v[0] - 1) * H + xx, gy = (v[1] - 1) * H + yy, gz = (v[2] - 1) * H + zz;
-    x[3 * sizeV + (static_cast<int64_t>(gz) * n + gy) * n + gx] += Px[o];
-  }
+  // ---- U_c = (S (x) S (x) S) Lambda_c^-1 [Fh_c - G_c^T P];  x += R^T (U, P) ----
+  SMG_FOR_C({
+    ps.template gt3<C>(Px, T1, T2);
+    for (int o = lane; o < P::NV; o += 32) T1[o] = Fh[C * P::NV + o] - T1[o];
+    __syncwarp();
+    ps.template lam_inv<C>(T1);
+    ps.template s3<C, false>(T1, T2, Pz);
+    for (int o = lane; o < P::NV; o += 32) x[vel_index(C, o)] += T2[o];
+  })
+#undef SMG_FOR_C
+  for (int o = lane; o < P::NPR; o += 32) x[pres_index(o)] += Px[o];
+}
+
+template <typename T, int K>
+constexpr int warps_per_cta() {
+  // keep a CTA at <= ~100 KB so that two fit on an SM
+  constexpr int ws = PD<K>::WS * static_cast<int>(sizeof(T));
+  constexpr int w = 100 * 1024 / ws;
+  return w >= 8 ? 8 : (w >= 4 ? 4 : (w >= 2 ? 2 : 1));
 }
 
 template <typename T, int K>
 void launch_k(Context& ctx, int level, int colour, void* x, const void* r) {
-  using PD = PatchDims<K>;
+  using P = PD<K>;
+  constexpr int W = warps_per_cta<T, K>();
   const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
   const int m = dl.lay.m;
   auto cnt = [&](int bit) { return bit ? m / 2 : m / 2 - 1; };
-  dim3 grid(cnt(colour & 1), cnt((colour >> 1) & 1), cnt((colour >> 2) & 1));
-  if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
-  constexpr int BIG = PD::NV > PD::NPR ? PD::NV : PD::NPR;
-  const size_t smem = sizeof(T) * (((PD::TAB + 1) / 2) * 2 + 3 * PD::NV + 2 * BIG + 6 * PD::NPR + 32);
-  auto kern = patch_smooth_kernel<T, K>;
+  const int npatch = cnt(colour & 1) * cnt((colour >> 1) & 1) * cnt((colour >> 2) & 1);
+  if (npatch <= 0) return;
+  const size_t smem = sizeof(T) * (P::TABP + W * P::WS);
+  auto kern = patch_smooth_kernel<T, K, W>;
   SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  kern<<<grid, kPatchThreads, smem, ctx.stream>>>(static_cast<T*>(x), static_cast<const T*>(r),
-                                                 static_cast<const T*>(dl.patch), m, colour, ctx.cfg.cg_max_iter,
-                                                 static_cast<T>(ctx.cfg.cg_tol), ctx.cfg.cg_fixed,
-                                                 ctx.cfg.cg_precond);
+  kern<<<(npatch + W - 1) / W, 32 * W, smem, ctx.stream>>>(
+      static_cast<T*>(x), static_cast<const T*>(r), static_cast<const T*>(dl.patch), m, colour, ctx.cfg.cg_max_iter,
+      static_cast<T>(ctx.cfg.cg_tol), ctx.cfg.cg_fixed, ctx.cfg.cg_precond);
   SMG_CUDA(cudaGetLastError());
   ++ctx.launches;
 }
@@ -336,7 +350,7 @@ void launch_smooth_colour(Context& ctx, int level, int prec, int colour, void* x
   else launch_prec<float>(ctx, level, colour, x, r);
 }
 
-// packed patch table (same order as PatchDims offsets)
+// packed patch table (order of PD<K> offsets)
 std::vector<double> pack_patch_tables(const PatchTables& P) {
   const int k = P.k, NP = 2 * k + 1, NO = 2 * k + 2;
   std::vector<double> t;
@@ -348,10 +362,21 @@ std::vector<double> pack_patch_tables(const PatchTables& P) {
       for (int j = 0; j < NO; ++j) t.push_back(P.orth_S[v](i, j));
   for (int v = 0; v < 4; ++v)
     for (int i = 0; i < NO; ++i) t.push_back(P.orth_lam[v][i]);
+  // G_par = D S_par  (NO x NP)
   for (int i = 0; i < NO; ++i)
-    for (int j = 0; j < NP; ++j) t.push_back(P.D(i, j));
-  for (int i = 0; i < NO; ++i)
-    for (int j = 0; j < NO; ++j) t.push_back(P.Mp(i, j));
+    for (int j = 0; j < NP; ++j) {
+      double s = 0.0;
+      for (int l = 0; l < NP; ++l) s += P.D(i, l) * P.par_S(l, j);
+      t.push_back(s);
+    }
+  // G_orth[v] = M' S_orth[v]  (NO x NO)
+  for (int v = 0; v < 4; ++v)
+    for (int i = 0; i < NO; ++i)
+      for (int j = 0; j < NO; ++j) {
+        double s = 0.0;
+        for (int l = 0; l < NO; ++l) s += P.Mp(i, l) * P.orth_S[v](l, j);
+        t.push_back(s);
+      }
   for (int i = 0; i < NO; ++i)
     for (int j = 0; j < NO; ++j) t.push_back(P.Mpinv(i, j));
   return t;
