@@ -16,10 +16,14 @@
 // by bricks that touch the boundary; constrained (boundary-normal) rows / inputs are masked.
 //
 // One CTA owns a brick of BX x BY x BZ cells. HBM traffic is one read of x and one write of y
-// (16 B/DoF in fp64); the one-cell halos of neighbouring bricks are re-read from L2.
+// (16 B/DoF in fp64); the one-cell halos of neighbouring bricks are re-read from L2. Inputs are
+// staged by TMA (cp.async.bulk.tensor) into double-buffered shared memory, see the persistent kernel.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "smg_internal.cuh"
 
@@ -126,92 +130,186 @@ __device__ __forceinline__ void dg_sipg(const T (&in)[(NC + 2) * (K + 1)], T (&o
 // ---------------------------------------------------------------------------------------------
 // brick geometry
 // ---------------------------------------------------------------------------------------------
-template <int K, int BX, int BY, int BZ>
+template <typename T, int K, int BX, int BY, int BZ>
 struct Brick {
   static constexpr int H = K + 1;
+  static constexpr int VEC = 16 / static_cast<int>(sizeof(T));  // elements per 16 B (TMA granule)
+  static constexpr int rup(int v) { return (v + VEC - 1) / VEC * VEC; }
   static constexpr int B(int a) { return a == 0 ? BX : (a == 1 ? BY : BZ); }
   static constexpr int N(int a) { return B(a) * H; }
   static constexpr int O1(int c) { return c == 0 ? 1 : 0; }
   static constexpr int O2(int c) { return c == 2 ? 1 : 2; }
   static constexpr int LC(int c) { return N(c) + H + 1; }       // c range [-H, N_c]
-  static constexpr int PC(int c) { return odd(LC(c)); }         // padded c extent
+  static constexpr int PC(int c) { return odd(LC(c)); }         // padded c extent of intermediates
   static constexpr int LO1H(int c) { return N(O1(c)) + 2 * H; }  // o1 range [-H, N + H)
   static constexpr int LO2H(int c) { return N(O2(c)) + 2 * H; }
-  static constexpr int sizeU(int c) { return LO2H(c) * LO1H(c) * PC(c); }
+  // staged input box of component c, TMA box order (x fastest, x pitch UX):
+  //   c=0: [z=o2][y=o1][x=c]   c=1: [z=o2][y=c][x=o1]   c=2: [z=c][y=o2][x=o1]
+  static constexpr int UX(int c) { return c == 0 ? rup(LC(0)) : rup(LO1H(c)); }
+  static constexpr int UY(int c) { return c == 0 ? LO1H(0) : (c == 1 ? LC(1) : LO2H(2)); }
+  static constexpr int UZ(int c) { return c == 2 ? LC(2) : LO2H(c); }
+  static constexpr int sizeU(int c) { return UX(c) * UY(c) * UZ(c); }
   static constexpr int sizeA1(int c) { return N(O2(c)) * LO1H(c) * PC(c); }
   static constexpr int sizeST(int c) { return N(O2(c)) * N(O1(c)) * PC(c); }
   static constexpr int mx3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
-  static constexpr int U = mx3(sizeU(0), sizeU(1), sizeU(2));
+  static constexpr int U = rup(mx3(sizeU(0), sizeU(1), sizeU(2)));
   static constexpr int A1 = mx3(sizeA1(0), sizeA1(1), sizeA1(2));
   static constexpr int ST = mx3(sizeST(0), sizeST(1), sizeST(2));
-  static constexpr int PX = odd(N(0) + H);  // pressure box, low halo on every axis
-  static constexpr int PBOX = (N(2) + H) * (N(1) + H) * PX;
+  static constexpr int PXT = rup(N(0) + H);  // pressure box [-H, N) per axis, x pitch PXT
+  static constexpr int PBOX = (N(2) + H) * (N(1) + H) * PXT;
   static constexpr int YX = odd(N(0));
   static constexpr int YP = N(2) * N(1) * YX;
   static constexpr bool ALIAS = 2 * ST <= U;  // S and T overwrite the dead U buffer of the component
-  // layout: [U buffer 0][U buffer 1][A1 (also Q2)][B1][Q][P box][YP][S,T if no alias]
+  // layout: [U buffer 0][U buffer 1][P box][A1 (also Q2)][B1][Q][YP][S,T if no alias][mbarriers]
   static constexpr int OFF_U1 = U;
-  static constexpr int OFF_A1 = 2 * U;
+  static constexpr int OFF_P = 2 * U;
+  static constexpr int OFF_A1 = rup(OFF_P + PBOX);
   static constexpr int OFF_B1 = OFF_A1 + A1;
   static constexpr int OFF_Q = OFF_B1 + ST;
-  static constexpr int OFF_P = OFF_Q + ST;
-  static constexpr int OFF_YP = OFF_P + PBOX;
+  static constexpr int OFF_YP = OFF_Q + ST;
   static constexpr int OFF_ST = OFF_YP + YP;  // only used when !ALIAS
-  static constexpr int TOTAL = OFF_YP + YP + (ALIAS ? 0 : 2 * ST);
+  static constexpr int END = OFF_YP + YP + (ALIAS ? 0 : 2 * ST);
+  static constexpr size_t BYTES = (static_cast<size_t>(END) * sizeof(T) + 15) / 16 * 16 + 3 * 8;
   static constexpr int stride(int axis, int a0, int a1) { return axis == 0 ? 1 : (axis == 1 ? a0 : a0 * a1); }
+};
+
+struct Maps {
+  CUtensorMap u0, u1, u2, p;  // rank-1 rows of u_x; 3D boxes of u_y, u_z (constrained planes OOB), p
 };
 
 struct Geo {
   int m, n;
   int c0[3];  // brick cell origin
   int g0[3];  // brick node origin
-  const void* x;
-  void* y;
-  const void* b;
 };
 
 // ---------------------------------------------------------------------------------------------
-// asynchronous staging (cp.async with zero fill)
+// mbarrier / TMA primitives
 // ---------------------------------------------------------------------------------------------
-// U box of component C: [-H, N_c] x [-H, N_o1+H) x [-H, N_o2+H), walked in global axis order
-// (x fastest, coalesced), stored c-fastest with an odd (bank-conflict-free) c pitch.
-template <typename T, int K, int BX, int BY, int BZ, int NT, int C>
-__device__ __forceinline__ void issue_u(T* sU, const T* __restrict__ x, const Geo& G) {
-  using BR = Brick<K, BX, BY, BZ>;
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const CUtensorMap* map, int x, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------------------------
+// staging: TMA (default) or cp.async element copies (fallback when a pitch is not 16-B aligned,
+// i.e. fp32 on level 0 with even k). Both write the same TMA box layout.
+// ---------------------------------------------------------------------------------------------
+template <typename T, int K, int BX, int BY, int BZ, int NT, int C, bool TMA>
+__device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restrict__ x, const Maps& M, const Geo& G) {
+  using BR = Brick<T, K, BX, BY, BZ>;
   constexpr int H = K + 1;
-  constexpr int O1 = BR::O1(C), O2 = BR::O2(C);
-  constexpr int LC = BR::LC(C), PC = BR::PC(C), LO1H = BR::LO1H(C), LO2H = BR::LO2H(C);
-  constexpr int E0 = C == 0 ? LC : (O1 == 0 ? LO1H : LO2H);
-  constexpr int E1 = C == 1 ? LC : (O1 == 1 ? LO1H : LO2H);
-  constexpr int E2 = C == 2 ? LC : (O1 == 2 ? LO1H : LO2H);
+  constexpr int UX = BR::UX(C), UY = BR::UY(C), UZ = BR::UZ(C);
   const int n = G.n;
-  int gd[3] = {n, n, n};
-  gd[C] = n + 1;
-  const T* xc = x + C * (static_cast<int64_t>(n + 1) * n * n);
-  for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
-    const int l[3] = {i % E0 - H, (i / E0) % E1 - H, i / (E0 * E1) - H};
-    const int g[3] = {G.g0[0] + l[0], G.g0[1] + l[1], G.g0[2] + l[2]};
-    bool ok = g[0] >= 0 && g[1] >= 0 && g[2] >= 0 && g[0] < gd[0] && g[1] < gd[1] && g[2] < gd[2];
-    ok = ok && g[C] != 0 && g[C] != n;  // constrained boundary-normal entries read as 0
-    const T* src = ok ? xc + (static_cast<int64_t>(g[2]) * gd[1] + g[1]) * gd[0] + g[0] : xc;
-    cp_async_elem(sU + ((l[O2] + H) * LO1H + (l[O1] + H)) * PC + (l[C] + H), src, ok);
+  const int tid = threadIdx.x;
+  if constexpr (TMA) {
+    if constexpr (C == 0) {
+      // one rank-1 TMA per x-row inside the domain (rows have the odd pitch n+1); warp 0 issues,
+      // rows outside the domain are zero-filled directly
+      if (tid < 32) {
+        const int y0 = G.g0[1] - H, z0 = G.g0[2] - H;
+        const int ny = max(0, min(n, y0 + UY) - max(0, y0)), nz = max(0, min(n, z0 + UZ) - max(0, z0));
+        if (tid == 0) mbar_expect(bar, static_cast<unsigned>(ny * nz * UX * sizeof(T)));
+        __syncwarp();
+        for (int r = tid; r < UY * UZ; r += 32) {
+          const int y = y0 + r % UY, z = z0 + r / UY;
+          T* dst = sU + r * UX;
+          if (y >= 0 && y < n && z >= 0 && z < n) {
+            tma_load_1d(dst, &M.u0, (z * n + y) * (n + 1) + G.g0[0] - H, bar);
+          } else {
+#pragma unroll
+            for (int i = 0; i < UX; ++i) dst[i] = T(0);
+          }
+        }
+      }
+    } else {
+      if (tid == 0) {
+        mbar_expect(bar, static_cast<unsigned>(BR::sizeU(C) * sizeof(T)));
+        // u_y / u_z maps start one row / plane in, so the constrained planes 0 and n fall outside
+        if (C == 1) tma_load_3d(sU, &M.u1, G.g0[0] - H, G.g0[1] - H - 1, G.g0[2] - H, bar);
+        else tma_load_3d(sU, &M.u2, G.g0[0] - H, G.g0[1] - H, G.g0[2] - H - 1, bar);
+      }
+    }
+  } else {
+    int gd[3] = {n, n, n};
+    gd[C] = n + 1;
+    const T* xc = x + C * (static_cast<int64_t>(n + 1) * n * n);
+    for (int i = tid; i < UX * UY * UZ; i += NT) {
+      const int l[3] = {i % UX - H, (i / UX) % UY - H, i / (UX * UY) - H};
+      const int g[3] = {G.g0[0] + l[0], G.g0[1] + l[1], G.g0[2] + l[2]};
+      bool ok = g[0] >= 0 && g[1] >= 0 && g[2] >= 0 && g[0] < gd[0] && g[1] < gd[1] && g[2] < gd[2];
+      ok = ok && g[C] != 0 && g[C] != n;
+      const T* src = ok ? xc + (static_cast<int64_t>(g[2]) * gd[1] + g[1]) * gd[0] + g[0] : xc;
+      cp_async_elem(sU + i, src, ok);
+    }
   }
 }
 
-// pressure box [-H, N_a) on every axis, x fastest with an odd row pitch
-template <typename T, int K, int BX, int BY, int BZ, int NT>
-__device__ __forceinline__ void issue_p(T* sP, const T* __restrict__ x, const Geo& G) {
-  using BR = Brick<K, BX, BY, BZ>;
+template <typename T, int K, int BX, int BY, int BZ, int NT, bool TMA>
+__device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const T* __restrict__ x, const Maps& M, const Geo& G) {
+  using BR = Brick<T, K, BX, BY, BZ>;
   constexpr int H = K + 1;
-  constexpr int E0 = BR::N(0) + H, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
-  const int n = G.n;
-  const T* xp = x + 3 * (static_cast<int64_t>(n + 1) * n * n);
-  for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
-    const int lx = i % E0, ly = (i / E0) % E1, lz = i / (E0 * E1);
-    const int gx = G.g0[0] + lx - H, gy = G.g0[1] + ly - H, gz = G.g0[2] + lz - H;
-    const bool ok = gx >= 0 && gy >= 0 && gz >= 0 && gx < n && gy < n && gz < n;
-    const T* src = ok ? xp + (static_cast<int64_t>(gz) * n + gy) * n + gx : xp;
-    cp_async_elem(sP + (lz * E1 + ly) * BR::PX + lx, src, ok);
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_expect(bar, static_cast<unsigned>(BR::PBOX * sizeof(T)));
+      tma_load_3d(sP, &M.p, G.g0[0] - H, G.g0[1] - H, G.g0[2] - H, bar);
+    }
+  } else {
+    constexpr int E0 = BR::PXT, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
+    const int n = G.n;
+    const T* xp = x + 3 * (static_cast<int64_t>(n + 1) * n * n);
+    for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
+      const int lx = i % E0, ly = (i / E0) % E1, lz = i / (E0 * E1);
+      const int gx = G.g0[0] + lx - H, gy = G.g0[1] + ly - H, gz = G.g0[2] + lz - H;
+      const bool ok = gx >= 0 && gy >= 0 && gz >= 0 && gx < n && gy < n && gz < n;
+      const T* src = ok ? xp + (static_cast<int64_t>(gz) * n + gy) * n + gx : xp;
+      cp_async_elem(sP + i, src, ok);
+    }
+  }
+}
+
+// rank-1 row copies of u_x ignore the row structure: zero the columns outside [1, n-1] (halo beyond
+// the domain and the constrained boundary-normal nodes x = 0, x = n) in bricks touching the x ends
+template <typename T, int K, int BX, int BY, int BZ, int NT>
+__device__ __forceinline__ void fix_u0_columns(T* sU, const Geo& G) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  constexpr int UX = BR::UX(0), ROWS = BR::UY(0) * BR::UZ(0);
+  const int x0 = G.g0[0] - H;
+  if (x0 > 0 && x0 + UX <= G.n) return;
+  for (int i = threadIdx.x; i < ROWS * UX; i += NT) {
+    const int gx = x0 + i % UX;
+    if (gx <= 0 || gx >= G.n) sU[i] = T(0);
   }
 }
 
@@ -219,17 +317,18 @@ __device__ __forceinline__ void issue_p(T* sP, const T* __restrict__ x, const Ge
 // one velocity component (U already staged in sU); if C == 2 and Gn != nullptr, the next brick's
 // pressure box is issued as soon as this brick's P box is dead.
 // ---------------------------------------------------------------------------------------------
-template <typename T, int K, int BX, int BY, int BZ, int NT, int C, bool RESID>
-__device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const Geo* Gn) {
-  using BR = Brick<K, BX, BY, BZ>;
+template <typename T, int K, int BX, int BY, int BZ, int NT, int C, bool RESID, bool TMA>
+__device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const Geo* Gn, const T* __restrict__ x,
+                                          T* __restrict__ y, const T* __restrict__ b, const Maps& M, uint64_t* barP) {
+  using BR = Brick<T, K, BX, BY, BZ>;
   constexpr int H = K + 1;
   constexpr int O1 = BR::O1(C), O2 = BR::O2(C);
   constexpr int NCc = BR::B(C), NO1 = BR::B(O1), NO2 = BR::B(O2);
   constexpr int Nc = BR::N(C), No1 = BR::N(O1), No2 = BR::N(O2);
   constexpr int LC = BR::LC(C), PC = BR::PC(C), LO1H = BR::LO1H(C);
+  constexpr int UX = BR::UX(C), UY = BR::UY(C);
   const int tid = threadIdx.x;
   const int n = G.n, m = G.m;
-  T* __restrict__ y = static_cast<T*>(G.y);
   const int64_t sizeV = static_cast<int64_t>(n + 1) * n * n;
   int64_t gd[3] = {n, n, n};
   gd[C] = n + 1;
@@ -247,11 +346,13 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
   {
     T* sQ2 = sA1;
     constexpr int E1P = BR::N(1) + H;
-    constexpr int PSC = BR::stride(C, BR::PX, E1P), PSO1 = BR::stride(O1, BR::PX, E1P),
-                  PSO2 = BR::stride(O2, BR::PX, E1P);
+    constexpr int PSC = BR::stride(C, BR::PXT, E1P), PSO1 = BR::stride(O1, BR::PXT, E1P),
+                  PSO2 = BR::stride(O2, BR::PXT, E1P);
     constexpr int NPEN = (Nc + H) * No1;
     for (int p = tid; p < NPEN; p += NT) {
-      const int ci = p % (Nc + H), oi = p / (Nc + H);  // ci is the 0-based index of c in [-H, N_c)
+      // consecutive threads walk the P-box x axis (c for C=0, o1 otherwise): conflict-free
+      const int ci = C == 0 ? p % (Nc + H) : p / No1;
+      const int oi = C == 0 ? p / (Nc + H) : p % No1;
       const T* src = sP + ci * PSC + (oi + H) * PSO1 + H * PSO2;
       T in[No2];
 #pragma unroll
@@ -261,9 +362,10 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
 #pragma unroll
       for (int j = 0; j < No2; ++j) sQ2[(j * No1 + oi) * PC + ci] = out[j];
     }
+    fence_proxy_async();
     __syncthreads();
-    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, NT>(sP, static_cast<const T*>(G.x), *Gn);
-    if (C == 2) cp_async_commit();
+    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, NT, TMA>(sP, barP, x, M, *Gn);
+    if (!TMA && C == 2) cp_async_commit();
     // Q = M_o1 Q2 (pencils along o1)
     constexpr int NPEN2 = (Nc + H) * No2;
     for (int p = tid; p < NPEN2; p += NT) {
@@ -286,10 +388,15 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
     const int elast = (m - 1 - cell_o2 < NO2) ? m - 1 - cell_o2 : -1;
     constexpr int NPEN = LC * LO1H;
     for (int p = tid; p < NPEN; p += NT) {
-      const int ci = p % LC, oi = p / LC;  // 0-based indices in the halo box
+      // consecutive threads walk the staged box's x axis: c for C=0, o1 for C=1,2
+      const int ci = C == 0 ? p % LC : p / LO1H;
+      const int oi = C == 0 ? p / LC : p % LO1H;
+      // element (c=ci, o1=oi, o2=j) of the staged box
+      const int ub = C == 0 ? oi * UX + ci : (C == 1 ? ci * UX + oi : ci * UY * UX + oi);
+      constexpr int US = C == 0 ? UX * UY : (C == 1 ? UX * UY : UX);  // stride along o2
       T in[(NO2 + 2) * H];
 #pragma unroll
-      for (int j = 0; j < (NO2 + 2) * H; ++j) in[j] = sU[(j * LO1H + oi) * PC + ci];
+      for (int j = 0; j < (NO2 + 2) * H; ++j) in[j] = sU[ub + j * US];
       T a1[No2];
       dg_mass<T, K, NO2, 1>(in, a1);
 #pragma unroll
@@ -338,7 +445,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
     using R = Ref<K>;
     constexpr int P = K + 2;
     const T h2 = h * h;
-    const T* __restrict__ bc = RESID ? static_cast<const T*>(G.b) + C * sizeV : nullptr;
+    const T* __restrict__ bc = RESID ? b + C * sizeV : nullptr;
     T* __restrict__ yc = y + C * sizeV;
     constexpr int NPEN = No1 * No2;
     constexpr int YSC = BR::stride(C, BR::YX, BR::N(1)), YSO1 = BR::stride(O1, BR::YX, BR::N(1)),
@@ -401,6 +508,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       }
     }
   }
+  fence_proxy_async();  // generic reads of this U buffer happen-before the next TMA into it
   __syncthreads();
 }
 
@@ -413,56 +521,87 @@ __device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, i
 }
 
 // Persistent kernel: each CTA walks bricks blockIdx.x, blockIdx.x + gridDim.x, ... The three
-// component boxes of a brick alternate between two U buffers so that the cp.async staging of the
-// next component (and of the next brick's first component and pressure box) overlaps compute.
-template <typename T, int K, int BX, int BY, int BZ, int NT, bool RESID>
+// component boxes of a brick alternate between two U buffers (each with its own mbarrier) so that
+// the TMA staging of the next component -- and of the next brick's first component and pressure
+// box -- overlaps compute.
+template <typename T, int K, int BX, int BY, int BZ, int NT, bool RESID, bool TMA>
 __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                                             const T* __restrict__ b, int m, T h) {
-  using BR = Brick<K, BX, BY, BZ>;
+                                                             const T* __restrict__ b, int m, T h,
+                                                             const __grid_constant__ Maps maps) {
+  using BR = Brick<T, K, BX, BY, BZ>;
   constexpr int H = K + 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (BR::BYTES - 3 * 8));  // [buf0, buf1, P]
   const int nbx = (m + BX - 1) / BX, nby = (m + BY - 1) / BY, nbz = (m + BZ - 1) / BZ;
   const int nbricks = nbx * nby * nbz;
   Geo G, Gn;
   G.m = Gn.m = m;
   G.n = Gn.n = m * H;
-  G.x = Gn.x = x;
-  G.y = Gn.y = y;
-  G.b = Gn.b = b;
   const int n = G.n;
   const int64_t offP = 3 * static_cast<int64_t>(n + 1) * n * n;
   T* sP = sm + BR::OFF_P;
   T* sYP = sm + BR::OFF_YP;
   int brick = blockIdx.x;
   if (brick >= nbricks) return;
+  if (TMA && threadIdx.x == 0) {
+    mbar_init(&bars[0]);
+    mbar_init(&bars[1]);
+    mbar_init(&bars[2]);
+  }
+  fence_proxy_async();
+  __syncthreads();
   brick_geo(G, brick, nbx, nby, BX, BY, BZ, H);
-  issue_p<T, K, BX, BY, BZ, NT>(sP, x, G);
-  issue_u<T, K, BX, BY, BZ, NT, 0>(sm, x, G);
-  cp_async_commit();
+  issue_p<T, K, BX, BY, BZ, NT, TMA>(sP, &bars[2], x, maps, G);
+  issue_u<T, K, BX, BY, BZ, NT, 0, TMA>(sm, &bars[0], x, maps, G);
+  if (!TMA) cp_async_commit();
   int u0 = 0;
+  unsigned ph[2] = {0, 0}, phP = 0;  // mbarrier phase of buffer 0 / 1 / P
   for (; brick < nbricks; brick += gridDim.x) {
-    T* bufA = sm + (u0 ? BR::OFF_U1 : 0);  // components 0 and 2 of this brick
-    T* bufB = sm + (u0 ? 0 : BR::OFF_U1);  // component 1, then component 0 of the next brick
+    const int ia = u0, ib = u0 ^ 1;
+    T* bufA = sm + (ia ? BR::OFF_U1 : 0);  // components 0 and 2 of this brick
+    T* bufB = sm + (ib ? BR::OFF_U1 : 0);  // component 1, then component 0 of the next brick
     const int next = brick + gridDim.x;
     const bool has_next = next < nbricks;
     if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H);
-    issue_u<T, K, BX, BY, BZ, NT, 1>(bufB, x, G);
-    cp_async_commit();
+    issue_u<T, K, BX, BY, BZ, NT, 1, TMA>(bufB, &bars[ib], x, maps, G);
     for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
-    cp_async_wait<1>();  // P box and U_0 of this brick
+    if (TMA) {
+      mbar_wait(&bars[2], phP);
+      phP ^= 1;
+      mbar_wait(&bars[ia], ph[ia]);
+      ph[ia] ^= 1;
+    } else {
+      cp_async_commit();
+      cp_async_wait<1>();  // P box and U_0 of this brick
+    }
     __syncthreads();
-    component<T, K, BX, BY, BZ, NT, 0, RESID>(sm, bufA, G, h, nullptr);
-    issue_u<T, K, BX, BY, BZ, NT, 2>(bufA, x, G);
-    cp_async_commit();
-    cp_async_wait<1>();  // U_1
+    if (TMA) {
+      fix_u0_columns<T, K, BX, BY, BZ, NT>(bufA, G);
+      __syncthreads();
+    }
+    component<T, K, BX, BY, BZ, NT, 0, RESID, TMA>(sm, bufA, G, h, nullptr, x, y, b, maps, &bars[2]);
+    issue_u<T, K, BX, BY, BZ, NT, 2, TMA>(bufA, &bars[ia], x, maps, G);
+    if (TMA) {
+      mbar_wait(&bars[ib], ph[ib]);
+      ph[ib] ^= 1;
+    } else {
+      cp_async_commit();
+      cp_async_wait<1>();  // U_1
+    }
     __syncthreads();
-    component<T, K, BX, BY, BZ, NT, 1, RESID>(sm, bufB, G, h, nullptr);
-    if (has_next) issue_u<T, K, BX, BY, BZ, NT, 0>(bufB, x, Gn);
-    cp_async_commit();
-    cp_async_wait<1>();  // U_2
+    component<T, K, BX, BY, BZ, NT, 1, RESID, TMA>(sm, bufB, G, h, nullptr, x, y, b, maps, &bars[2]);
+    if (has_next) issue_u<T, K, BX, BY, BZ, NT, 0, TMA>(bufB, &bars[ib], x, maps, Gn);
+    if (TMA) {
+      mbar_wait(&bars[ia], ph[ia]);
+      ph[ia] ^= 1;
+    } else {
+      cp_async_commit();
+      cp_async_wait<1>();  // U_2
+    }
     __syncthreads();
-    component<T, K, BX, BY, BZ, NT, 2, RESID>(sm, bufA, G, h, has_next ? &Gn : nullptr);
+    component<T, K, BX, BY, BZ, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
+                                                   &bars[2]);
     // write the pressure rows of this brick
     {
       constexpr int N0 = BR::N(0), N1 = BR::N(1), N2 = BR::N(2);
@@ -479,29 +618,105 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
     G = Gn;
     u0 ^= 1;
   }
-  cp_async_wait<0>();
+  if (!TMA) cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------------------------
+// host: tensor maps
+// ---------------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SMG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw cuda_error("cuTensorMapEncodeTiled not available");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <typename T>
+void encode(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+            const uint32_t* box) {
+  const uint32_t es[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                 rank, const_cast<void*>(base), dims, strides_bytes, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+// TMA needs 16-B aligned row pitches / base offsets: n * sizeof(T) % 16 == 0
+template <typename T>
+bool tma_ok(int n) {
+  return (static_cast<int64_t>(n) * sizeof(T)) % 16 == 0;
+}
+
+template <typename T, int K, int BX, int BY, int BZ>
+Maps make_maps(const T* x, int n) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  Maps M;
+  std::memset(&M, 0, sizeof(M));
+  const uint64_t es = sizeof(T);
+  const uint64_t nn = static_cast<uint64_t>(n);
+  const uint64_t sizeV = (nn + 1) * nn * nn;
+  {  // u_x as one long row
+    const uint64_t d[1] = {sizeV};
+    const uint32_t box[1] = {static_cast<uint32_t>(BR::UX(0))};
+    encode<T>(&M.u0, x, 1, d, nullptr, box);
+  }
+  {  // u_y: dims (x n, y n+1, z n); base one row in -> y' = y - 1 in [0, n-1)
+    const uint64_t d[3] = {nn, nn - 1, nn};
+    const uint64_t s[2] = {nn * es, nn * (nn + 1) * es};
+    const uint32_t box[3] = {static_cast<uint32_t>(BR::UX(1)), static_cast<uint32_t>(BR::UY(1)),
+                             static_cast<uint32_t>(BR::UZ(1))};
+    encode<T>(&M.u1, x + sizeV + nn, 3, d, s, box);
+  }
+  {  // u_z: dims (x n, y n, z n+1); base one plane in -> z' = z - 1 in [0, n-1)
+    const uint64_t d[3] = {nn, nn, nn - 1};
+    const uint64_t s[2] = {nn * es, nn * nn * es};
+    const uint32_t box[3] = {static_cast<uint32_t>(BR::UX(2)), static_cast<uint32_t>(BR::UY(2)),
+                             static_cast<uint32_t>(BR::UZ(2))};
+    encode<T>(&M.u2, x + 2 * sizeV + nn * nn, 3, d, s, box);
+  }
+  {  // p
+    const uint64_t d[3] = {nn, nn, nn};
+    const uint64_t s[2] = {nn * es, nn * nn * es};
+    const uint32_t box[3] = {static_cast<uint32_t>(BR::PXT), static_cast<uint32_t>(BR::N(1) + H),
+                             static_cast<uint32_t>(BR::N(2) + H)};
+    encode<T>(&M.p, x + 3 * sizeV, 3, d, s, box);
+  }
+  return M;
 }
 
 template <typename T, int K, int BX, int BY, int BZ, int NT>
 void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
-  using BR = Brick<K, BX, BY, BZ>;
+  using BR = Brick<T, K, BX, BY, BZ>;
   const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
-  const int m = dl.lay.m;
+  const int m = dl.lay.m, n = dl.lay.n;
   const T h = static_cast<T>(1.0 / m);
   const int nbricks = ((m + BX - 1) / BX) * ((m + BY - 1) / BY) * ((m + BZ - 1) / BZ);
   static int num_sms = 0;
   if (num_sms == 0) SMG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ctx.device));
   const dim3 grid(std::min(nbricks, num_sms));
-  const size_t smem = sizeof(T) * BR::TOTAL;
+  const size_t smem = BR::BYTES;
+  const bool tma = tma_ok<T>(n) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  Maps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  if (tma) maps = make_maps<T, K, BX, BY, BZ>(static_cast<const T*>(x), n);
+  auto go = [&](auto kern) {
+    SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, NT, smem, ctx.stream>>>(static_cast<const T*>(x), static_cast<T*>(y), static_cast<const T*>(b), m, h,
+                                         maps);
+  };
   if (b) {
-    auto kern = stokes_vmult_kernel<T, K, BX, BY, BZ, NT, true>;
-    SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, NT, smem, ctx.stream>>>(static_cast<const T*>(x), static_cast<T*>(y), static_cast<const T*>(b), m,
-                                         h);
+    if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, true, true>);
+    else go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, true, false>);
   } else {
-    auto kern = stokes_vmult_kernel<T, K, BX, BY, BZ, NT, false>;
-    SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, NT, smem, ctx.stream>>>(static_cast<const T*>(x), static_cast<T*>(y), nullptr, m, h);
+    if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, false, true>);
+    else go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, false, false>);
   }
   SMG_CUDA(cudaGetLastError());
   ++ctx.launches;
