@@ -647,10 +647,19 @@ void encode(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, 
   if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
 }
 
-// TMA needs 16-B aligned row pitches / base offsets: n * sizeof(T) % 16 == 0
-template <typename T>
+// TMA needs 16-B aligned row pitches / base offsets (n * sizeof(T) % 16 == 0); boxes are kept no
+// larger than the tensor (small coarse levels take the cp.async path).
+template <typename T, int K, int BX, int BY, int BZ>
 bool tma_ok(int n) {
-  return (static_cast<int64_t>(n) * sizeof(T)) % 16 == 0;
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  if ((static_cast<int64_t>(n) * sizeof(T)) % 16 != 0) return false;
+  const int lim = n - 1;  // smallest extent among the u_y / u_z maps
+  const int ext[] = {BR::UX(1), BR::UY(1), BR::UZ(1), BR::UX(2), BR::UY(2), BR::UZ(2), BR::PXT, BR::N(1) + H,
+                     BR::N(2) + H};
+  for (int e : ext)
+    if (e > lim) return false;
+  return true;
 }
 
 template <typename T, int K, int BX, int BY, int BZ>
@@ -664,8 +673,9 @@ Maps make_maps(const T* x, int n) {
   const uint64_t sizeV = (nn + 1) * nn * nn;
   {  // u_x as one long row
     const uint64_t d[1] = {sizeV};
+    const uint64_t s[1] = {sizeV * es};  // unused for rank 1
     const uint32_t box[1] = {static_cast<uint32_t>(BR::UX(0))};
-    encode<T>(&M.u0, x, 1, d, nullptr, box);
+    encode<T>(&M.u0, x, 1, d, s, box);
   }
   {  // u_y: dims (x n, y n+1, z n); base one row in -> y' = y - 1 in [0, n-1)
     const uint64_t d[3] = {nn, nn - 1, nn};
@@ -702,7 +712,7 @@ void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
   if (num_sms == 0) SMG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ctx.device));
   const dim3 grid(std::min(nbricks, num_sms));
   const size_t smem = BR::BYTES;
-  const bool tma = tma_ok<T>(n) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  const bool tma = tma_ok<T, K, BX, BY, BZ>(n) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
   Maps maps;
   std::memset(&maps, 0, sizeof(maps));
   if (tma) maps = make_maps<T, K, BX, BY, BZ>(static_cast<const T*>(x), n);
