@@ -386,6 +386,8 @@ int smg_create(const smg_config* cfg, smg_context** out) {
     SMG_CUDA(cudaMalloc(&c->dot_partials, (smg::kDotBlocks + 8) * sizeof(double)));
     c->allocations.push_back(c->dot_partials);
     SMG_CUDA(cudaMallocHost(&c->dot_host, 64));
+    SMG_CUDA(cudaMalloc(&c->tmap_dev, static_cast<size_t>(smg::kTmapSlots) * smg::kTmapSlotBytes));
+    c->allocations.push_back(c->tmap_dev);
     smg::setup_coarse(*c);
     return SMG_OK;
   });

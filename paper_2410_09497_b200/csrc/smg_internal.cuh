@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -62,6 +63,14 @@ struct DevLevel {
   void* pweights = nullptr; // pressure node weights (k+1)
 };
 
+struct TmapKey {
+  const void* ptr;
+  int level, esize;
+  bool operator<(const TmapKey& o) const {
+    return ptr != o.ptr ? ptr < o.ptr : (level != o.level ? level < o.level : esize < o.esize);
+  }
+};
+
 struct Context {
   smg_config cfg{};
   int device = 0;
@@ -82,10 +91,16 @@ struct Context {
   std::vector<void*> allocations;
   // per-level work vectors for the smoother / V-cycle (allocated lazily): [prec][level]
   std::vector<void*> work_r[2], work_x[2], work_b[2];
+  // TMA descriptors of input vectors (vmult.cu)
+  void* tmap_dev = nullptr;
+  std::map<TmapKey, int> tmap_slots;
+  int tmap_next = 0;
   ~Context();
 };
 
 constexpr int kDotBlocks = 1184;  // 8 x 148 SMs
+constexpr int kTmapSlots = 64;         // cached TMA descriptor sets (global memory)
+constexpr int kTmapSlotBytes = 512;    // 4 CUtensorMap (128 B each)
 
 size_t elem_size(int precision);
 

@@ -527,7 +527,7 @@ __device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, i
 template <typename T, int K, int BX, int BY, int BZ, int NT, bool RESID, bool TMA>
 __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
                                                              const T* __restrict__ b, int m, T h,
-                                                             const __grid_constant__ Maps maps) {
+                                                             const Maps* __restrict__ mapsp) {
   using BR = Brick<T, K, BX, BY, BZ>;
   constexpr int H = K + 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -542,6 +542,7 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
   const int64_t offP = 3 * static_cast<int64_t>(n + 1) * n * n;
   T* sP = sm + BR::OFF_P;
   T* sYP = sm + BR::OFF_YP;
+  const Maps& maps = *mapsp;  // tensor maps live in global memory (64-B aligned slots)
   int brick = blockIdx.x;
   if (brick >= nbricks) return;
   if (TMA && threadIdx.x == 0) {
@@ -713,13 +714,30 @@ void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
   const dim3 grid(std::min(nbricks, num_sms));
   const size_t smem = BR::BYTES;
   const bool tma = tma_ok<T, K, BX, BY, BZ>(n) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
-  Maps maps;
-  std::memset(&maps, 0, sizeof(maps));
-  if (tma) maps = make_maps<T, K, BX, BY, BZ>(static_cast<const T*>(x), n);
+  const Maps* dmaps = nullptr;
+  if (tma) {
+    // tensor maps are cached per (input vector, level, precision) in 64-B aligned global slots,
+    // written stream-ordered before the launch
+    const TmapKey key{x, level, static_cast<int>(sizeof(T))};
+    auto it = ctx.tmap_slots.find(key);
+    if (it == ctx.tmap_slots.end()) {
+      const int slot = ctx.tmap_next++ % kTmapSlots;
+      for (auto e = ctx.tmap_slots.begin(); e != ctx.tmap_slots.end();)
+        e = (e->second == slot) ? ctx.tmap_slots.erase(e) : std::next(e);
+      Maps mh = make_maps<T, K, BX, BY, BZ>(static_cast<const T*>(x), n);
+      char* dst = static_cast<char*>(ctx.tmap_dev) + static_cast<size_t>(slot) * kTmapSlotBytes;
+      SMG_CUDA(cudaMemcpyAsync(dst, &mh, sizeof(Maps), cudaMemcpyHostToDevice, ctx.stream));
+      SMG_CUDA(cudaStreamSynchronize(ctx.stream));  // mh is a stack temporary
+      it = ctx.tmap_slots.emplace(key, slot).first;
+    }
+    dmaps = reinterpret_cast<const Maps*>(static_cast<char*>(ctx.tmap_dev) +
+                                          static_cast<size_t>(it->second) * kTmapSlotBytes);
+  }
+  static_assert(sizeof(Maps) <= kTmapSlotBytes, "tensor-map slot too small");
   auto go = [&](auto kern) {
     SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     kern<<<grid, NT, smem, ctx.stream>>>(static_cast<const T*>(x), static_cast<T*>(y), static_cast<const T*>(b), m, h,
-                                         maps);
+                                         dmaps);
   };
   if (b) {
     if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, true, true>);
