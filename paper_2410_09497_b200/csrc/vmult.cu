@@ -549,6 +549,7 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
     mbar_init(&bars[0]);
     mbar_init(&bars[1]);
     mbar_init(&bars[2]);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   fence_proxy_async();
   __syncthreads();
