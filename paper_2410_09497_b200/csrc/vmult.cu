@@ -145,25 +145,30 @@ struct Brick {
   static constexpr int LO2H(int c) { return N(O2(c)) + 2 * H; }
   // staged input box of component c, TMA box order (x fastest, x pitch UX):
   //   c=0: [z=o2][y=o1][x=c]   c=1: [z=o2][y=c][x=o1]   c=2: [z=c][y=o2][x=o1]
-  static constexpr int UX(int c) { return c == 0 ? rup(LC(0)) : rup(LO1H(c)); }
+  // TMA requires the x start of a box to be 16-B aligned and >= 0, so every row is loaded from the
+  // 16-B aligned position at or below the needed start; UX carries VEC-1 elements of slack and the
+  // consumers add the per-brick (per-row for c=0) shift.
+  static constexpr int XEXT(int c) { return c == 0 ? LC(0) : LO1H(c); }
+  static constexpr int UX(int c) { return rup(XEXT(c) + VEC - 1); }
   static constexpr int UY(int c) { return c == 0 ? LO1H(0) : (c == 1 ? LC(1) : LO2H(2)); }
   static constexpr int UZ(int c) { return c == 2 ? LC(2) : LO2H(c); }
-  static constexpr int sizeU(int c) { return UX(c) * UY(c) * UZ(c); }
+  static constexpr int sizeU(int c) { return UX(c) * UY(c) * UZ(c); }  // bytes loaded by one TMA box
   static constexpr int sizeA1(int c) { return N(O2(c)) * LO1H(c) * PC(c); }
   static constexpr int sizeST(int c) { return N(O2(c)) * N(O1(c)) * PC(c); }
   static constexpr int mx3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
-  static constexpr int U = rup(mx3(sizeU(0), sizeU(1), sizeU(2)));
+  static constexpr int U = rup(mx3(sizeU(0), sizeU(1), sizeU(2)) + VEC);  // + clamp slack
   static constexpr int A1 = mx3(sizeA1(0), sizeA1(1), sizeA1(2));
   static constexpr int ST = mx3(sizeST(0), sizeST(1), sizeST(2));
-  static constexpr int PXT = rup(N(0) + H);  // pressure box [-H, N) per axis, x pitch PXT
+  static constexpr int PXT = rup(N(0) + H + VEC - 1);  // pressure box [-H, N) per axis, x pitch PXT
   static constexpr int PBOX = (N(2) + H) * (N(1) + H) * PXT;
+  static constexpr int PBUF = rup(PBOX + VEC);
   static constexpr int YX = odd(N(0));
   static constexpr int YP = N(2) * N(1) * YX;
   static constexpr bool ALIAS = 2 * ST <= U;  // S and T overwrite the dead U buffer of the component
   // layout: [U buffer 0][U buffer 1][P box][A1 (also Q2)][B1][Q][YP][S,T if no alias][mbarriers]
   static constexpr int OFF_U1 = U;
   static constexpr int OFF_P = 2 * U;
-  static constexpr int OFF_A1 = rup(OFF_P + PBOX);
+  static constexpr int OFF_A1 = OFF_P + PBUF;
   static constexpr int OFF_B1 = OFF_A1 + A1;
   static constexpr int OFF_Q = OFF_B1 + ST;
   static constexpr int OFF_YP = OFF_Q + ST;
@@ -221,6 +226,23 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ int floor_to(int v, int q) { return (v >= 0 ? v / q : -((-v + q - 1) / q)) * q; }
+
+// smem origin offsets of the staged rows (element of x = g0x - H relative to the row start)
+template <typename T>
+__device__ __forceinline__ int brick_shift(const Geo& G, int H) {
+  constexpr int VEC = 16 / static_cast<int>(sizeof(T));
+  const int x0 = G.g0[0] - H;
+  return x0 - floor_to(x0, VEC);
+}
+// u_x rows: the 1D start (z n + y)(n+1) + x0 has the same residue mod VEC for every z (n % VEC == 0)
+template <typename T>
+__device__ __forceinline__ int row_shift0(const Geo& G, int H, int y) {
+  constexpr int VEC = 16 / static_cast<int>(sizeof(T));
+  const int v = (y * (G.n + 1) + G.g0[0] - H) % VEC;
+  return v < 0 ? v + VEC : v;
+}
+
 // ---------------------------------------------------------------------------------------------
 // staging: TMA (default) or cp.async element copies (fallback when a pitch is not 16-B aligned,
 // i.e. fp32 on level 0 with even k). Both write the same TMA box layout.
@@ -245,7 +267,9 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restric
           const int y = y0 + r % UY, z = z0 + r / UY;
           T* dst = sU + r * UX;
           if (y >= 0 && y < n && z >= 0 && z < n) {
-            tma_load_1d(dst, &M.u0, (z * n + y) * (n + 1) + G.g0[0] - H, bar);
+            const int start = (z * n + y) * (n + 1) + G.g0[0] - H;
+            const int sal = floor_to(start, BR::VEC), ss = max(sal, 0);
+            tma_load_1d(dst + (ss - sal), &M.u0, ss, bar);
           } else {
 #pragma unroll
             for (int i = 0; i < UX; ++i) dst[i] = T(0);
@@ -256,21 +280,24 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restric
       if (tid == 0) {
         mbar_expect(bar, static_cast<unsigned>(BR::sizeU(C) * sizeof(T)));
         // u_y / u_z maps start one row / plane in, so the constrained planes 0 and n fall outside
-        if (C == 1) tma_load_3d(sU, &M.u1, G.g0[0] - H, G.g0[1] - H - 1, G.g0[2] - H, bar);
-        else tma_load_3d(sU, &M.u2, G.g0[0] - H, G.g0[1] - H, G.g0[2] - H - 1, bar);
+        const int xal = floor_to(G.g0[0] - H, BR::VEC), xs = max(xal, 0);
+        if (C == 1) tma_load_3d(sU + (xs - xal), &M.u1, xs, G.g0[1] - H - 1, G.g0[2] - H, bar);
+        else tma_load_3d(sU + (xs - xal), &M.u2, xs, G.g0[1] - H, G.g0[2] - H - 1, bar);
       }
     }
   } else {
     int gd[3] = {n, n, n};
     gd[C] = n + 1;
     const T* xc = x + C * (static_cast<int64_t>(n + 1) * n * n);
-    for (int i = tid; i < UX * UY * UZ; i += NT) {
-      const int l[3] = {i % UX - H, (i / UX) % UY - H, i / (UX * UY) - H};
+    constexpr int XE = BR::XEXT(C);
+    for (int i = tid; i < XE * UY * UZ; i += NT) {
+      const int l[3] = {i % XE - H, (i / XE) % UY - H, i / (XE * UY) - H};
       const int g[3] = {G.g0[0] + l[0], G.g0[1] + l[1], G.g0[2] + l[2]};
       bool ok = g[0] >= 0 && g[1] >= 0 && g[2] >= 0 && g[0] < gd[0] && g[1] < gd[1] && g[2] < gd[2];
       ok = ok && g[C] != 0 && g[C] != n;
       const T* src = ok ? xc + (static_cast<int64_t>(g[2]) * gd[1] + g[1]) * gd[0] + g[0] : xc;
-      cp_async_elem(sU + i, src, ok);
+      const int sh = C == 0 ? row_shift0<T>(G, H, g[1]) : brick_shift<T>(G, H);
+      cp_async_elem(sU + (i / XE) * UX + sh + (l[0] + H), src, ok);
     }
   }
 }
@@ -282,35 +309,49 @@ __device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const T* __restric
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
       mbar_expect(bar, static_cast<unsigned>(BR::PBOX * sizeof(T)));
-      tma_load_3d(sP, &M.p, G.g0[0] - H, G.g0[1] - H, G.g0[2] - H, bar);
+      const int xal = floor_to(G.g0[0] - H, BR::VEC), xs = max(xal, 0);
+      tma_load_3d(sP + (xs - xal), &M.p, xs, G.g0[1] - H, G.g0[2] - H, bar);
     }
   } else {
-    constexpr int E0 = BR::PXT, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
+    constexpr int E0 = BR::N(0) + H, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
     const int n = G.n;
+    const int sh = brick_shift<T>(G, H);
     const T* xp = x + 3 * (static_cast<int64_t>(n + 1) * n * n);
     for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
       const int lx = i % E0, ly = (i / E0) % E1, lz = i / (E0 * E1);
       const int gx = G.g0[0] + lx - H, gy = G.g0[1] + ly - H, gz = G.g0[2] + lz - H;
       const bool ok = gx >= 0 && gy >= 0 && gz >= 0 && gx < n && gy < n && gz < n;
       const T* src = ok ? xp + (static_cast<int64_t>(gz) * n + gy) * n + gx : xp;
-      cp_async_elem(sP + i, src, ok);
+      cp_async_elem(sP + (lz * E1 + ly) * BR::PXT + sh + lx, src, ok);
     }
   }
 }
 
-// rank-1 row copies of u_x ignore the row structure: zero the columns outside [1, n-1] (halo beyond
-// the domain and the constrained boundary-normal nodes x = 0, x = n) in bricks touching the x ends
+// Boundary fix-ups after a TMA box landed (bricks touching the x ends only):
+//  - u_x rows are rank-1 copies that ignore the row structure: zero the columns outside [1, n-1]
+//    (halo beyond the domain and the constrained boundary-normal nodes x = 0, x = n);
+//  - u_y, u_z, p boxes clamped at x = 0 leave the x < 0 halo columns unwritten: zero them.
 template <typename T, int K, int BX, int BY, int BZ, int NT>
-__device__ __forceinline__ void fix_u0_columns(T* sU, const Geo& G) {
+__device__ __forceinline__ void fix_columns(T* sU0, T* sU1, T* sU2, T* sP, const Geo& G) {
   using BR = Brick<T, K, BX, BY, BZ>;
   constexpr int H = K + 1;
-  constexpr int UX = BR::UX(0), ROWS = BR::UY(0) * BR::UZ(0);
   const int x0 = G.g0[0] - H;
-  if (x0 > 0 && x0 + UX <= G.n) return;
-  for (int i = threadIdx.x; i < ROWS * UX; i += NT) {
-    const int gx = x0 + i % UX;
-    if (gx <= 0 || gx >= G.n) sU[i] = T(0);
+  if (x0 >= 0 && x0 + BR::XEXT(0) <= G.n) return;
+  if (sU0) {
+    constexpr int XE = BR::XEXT(0), UY = BR::UY(0), ROWS = BR::UY(0) * BR::UZ(0);
+    for (int i = threadIdx.x; i < ROWS * XE; i += NT) {
+      const int r = i / XE, gx = x0 + i % XE;
+      if (gx <= 0 || gx >= G.n) sU0[r * BR::UX(0) + row_shift0<T>(G, H, G.g0[1] - H + r % UY) + i % XE] = T(0);
+    }
   }
+  if (x0 >= 0) return;
+  const int sh = brick_shift<T>(G, H);
+  auto zero_low = [&](T* buf, int rows, int pitch) {
+    for (int i = threadIdx.x; i < rows * H; i += NT) buf[(i / H) * pitch + sh + i % H] = T(0);
+  };
+  if (sU1) zero_low(sU1, BR::UY(1) * BR::UZ(1), BR::UX(1));
+  if (sU2) zero_low(sU2, BR::UY(2) * BR::UZ(2), BR::UX(2));
+  if (sP) zero_low(sP, (BR::N(1) + H) * (BR::N(2) + H), BR::PXT);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -353,7 +394,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       // consecutive threads walk the P-box x axis (c for C=0, o1 otherwise): conflict-free
       const int ci = C == 0 ? p % (Nc + H) : p / No1;
       const int oi = C == 0 ? p / (Nc + H) : p % No1;
-      const T* src = sP + ci * PSC + (oi + H) * PSO1 + H * PSO2;
+      const T* src = sP + brick_shift<T>(G, H) + ci * PSC + (oi + H) * PSO1 + H * PSO2;
       T in[No2];
 #pragma unroll
       for (int j = 0; j < No2; ++j) in[j] = src[j * PSO2];
@@ -392,7 +433,8 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       const int ci = C == 0 ? p % LC : p / LO1H;
       const int oi = C == 0 ? p / LC : p % LO1H;
       // element (c=ci, o1=oi, o2=j) of the staged box
-      const int ub = C == 0 ? oi * UX + ci : (C == 1 ? ci * UX + oi : ci * UY * UX + oi);
+      const int ub = C == 0 ? oi * UX + ci + row_shift0<T>(G, H, G.g0[1] - H + oi)
+                            : (C == 1 ? ci * UX + oi : ci * UY * UX + oi) + brick_shift<T>(G, H);
       constexpr int US = C == 0 ? UX * UY : (C == 1 ? UX * UY : UX);  // stride along o2
       T in[(NO2 + 2) * H];
 #pragma unroll
@@ -579,7 +621,7 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
     }
     __syncthreads();
     if (TMA) {
-      fix_u0_columns<T, K, BX, BY, BZ, NT>(bufA, G);
+      fix_columns<T, K, BX, BY, BZ, NT>(bufA, nullptr, nullptr, sP, G);
       __syncthreads();
     }
     component<T, K, BX, BY, BZ, NT, 0, RESID, TMA>(sm, bufA, G, h, nullptr, x, y, b, maps, &bars[2]);
@@ -592,6 +634,10 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
       cp_async_wait<1>();  // U_1
     }
     __syncthreads();
+    if (TMA) {
+      fix_columns<T, K, BX, BY, BZ, NT>(nullptr, bufB, nullptr, nullptr, G);
+      __syncthreads();
+    }
     component<T, K, BX, BY, BZ, NT, 1, RESID, TMA>(sm, bufB, G, h, nullptr, x, y, b, maps, &bars[2]);
     if (has_next) issue_u<T, K, BX, BY, BZ, NT, 0, TMA>(bufB, &bars[ib], x, maps, Gn);
     if (TMA) {
@@ -602,6 +648,10 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
       cp_async_wait<1>();  // U_2
     }
     __syncthreads();
+    if (TMA) {
+      fix_columns<T, K, BX, BY, BZ, NT>(nullptr, nullptr, bufA, nullptr, G);
+      __syncthreads();
+    }
     component<T, K, BX, BY, BZ, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
                                                    &bars[2]);
     // write the pressure rows of this brick
