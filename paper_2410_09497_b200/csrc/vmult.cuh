@@ -1,0 +1,11 @@
+// Per-degree entry points of the Stokes vmult kernel (one translation unit per degree so the heavy
+// template instantiations compile in parallel).
+#pragma once
+#include "smg_internal.cuh"
+
+namespace smg {
+template <int K>
+void vmult_launch_k(Context& ctx, int level, int prec, void* y, const void* x, const void* b);
+template <int K>
+void vmult_upload_k(const double* t, const float* f);
+}  // namespace smg

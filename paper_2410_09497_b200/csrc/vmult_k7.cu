@@ -1,0 +1,6 @@
+// K1/K2 instantiation for degree 7 (see vmult_kernel.cuh).
+#include "vmult_kernel.cuh"
+
+namespace smg {
+SMG_INSTANTIATE_VMULT(7)
+}  // namespace smg

@@ -1,0 +1,836 @@
+#pragma once
+// K1/K2: matrix-free Stokes operator y = A x and residual r = b - A x on sm_100a.
+//
+// Reference: apply_stokes evaluated by Alg. 1. On the uniform
+// Cartesian unit cube the cell/face loops of Alg. 1 equal a Kronecker sum of banded 1D operators
+// (re-verified by the GPU-vs-Alg.1-oracle parity tests to 1e-13). Per velocity
+// component c with orthogonal axes o1, o2 (all 1D blocks at reference size h = 1, see
+// setup1d.hpp reference_cell_tables; level scaling applied once at the output):
+//   pass 1 (along o2):  A1 = M_o2 u_c,            B1 = L_o2 u_c
+//   pass 2 (along o1):  S  = M_o1 A1,             T  = L_o1 A1 + M_o1 B1
+//   pass 3 (along c) :  y_c = h (L_c S + M_c T) + h^2 D_c^T Q,   y_p += h^2 D_c S
+// with Q = M_o1 M_o2 p. Every pass is "one thread per pencil": a thread loads a 1D line of the
+// brick from shared memory into registers, applies the banded cell-block operator with fully
+// unrolled loops whose coefficients are compile-time offsets into __constant__ memory (so they are
+// DFMA constant-bank operands, no loads), and writes the result line back. Index arithmetic is per
+// pencil, never per element. Domain-boundary Nitsche rows are a CTA-uniform correction applied only
+// by bricks that touch the boundary; constrained (boundary-normal) rows / inputs are masked.
+//
+// One CTA owns a brick of BX x BY x BZ cells. HBM traffic is one read of x and one write of y
+// (16 B/DoF in fp64); the one-cell halos of neighbouring bricks are re-read from L2. Inputs are
+// staged by TMA (cp.async.bulk.tensor) into double-buffered shared memory, see the persistent kernel.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "smg_internal.cuh"
+#include "vmult.cuh"
+
+namespace smg {
+
+// each translation unit (one per degree, vmult_k<K>.cu) holds its own copy of the tables
+static __constant__ double c_ref_d[kRefTotal];
+static __constant__ float c_ref_f[kRefTotal];
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T cref(int i);
+template <>
+__device__ __forceinline__ double cref<double>(int i) { return c_ref_d[i]; }
+template <>
+__device__ __forceinline__ float cref<float>(int i) { return c_ref_f[i]; }
+
+template <int K>
+struct Ref {
+  static constexpr int H = K + 1, P = K + 2;
+  static constexpr int MO = ref_base(K);
+  static constexpr int LO0 = MO + H * H;
+  static constexpr int LOM = LO0 + H * H;
+  static constexpr int LOP = LOM + H * H;
+  static constexpr int DLF = LOP + H * H;
+  static constexpr int DLL = DLF + H * H;
+  static constexpr int MP = DLL + H * H;
+  static constexpr int LP = MP + P * P;
+  static constexpr int D = LP + P * P;
+};
+
+constexpr int odd(int v) { return v | 1; }
+
+// Asynchronous global->shared copy of one element with zero fill (cp.async, LDGSTS): when `ok` is
+// false nothing is read and the destination is zeroed -- this implements the halo outside the
+// domain and the constrained boundary-normal entries without any masking pass.
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* dst, const T* src, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int n = ok ? static_cast<int>(sizeof(T)) : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(src), "n"(sizeof(T)), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// ---------------------------------------------------------------------------------------------
+// register-pencil banded operators
+// ---------------------------------------------------------------------------------------------
+// DG mass (block diagonal): out[e*H+a] = sum_b MO[a][b] in[(e+OFF)*H+b]
+template <typename T, int K, int NC, int OFF, int LIN>
+__device__ __forceinline__ void dg_mass(const T (&in)[LIN], T (&out)[NC * (K + 1)]) {
+  constexpr int H = K + 1;
+#pragma unroll
+  for (int e = 0; e < NC; ++e)
+#pragma unroll
+    for (int a = 0; a < H; ++a) {
+      T s = T(0);
+#pragma unroll
+      for (int b = 0; b < H; ++b) s += cref<T>(Ref<K>::MO + a * H + b) * in[(e + OFF) * H + b];
+      out[e * H + a] = s;
+    }
+}
+
+// DG SIPG Laplacian (block tridiagonal; the off-diagonal blocks are "cross shaped" for the
+// Gauss-Lobatto nodal basis: LOM[a][b] != 0 only if a == 0 or b == K, LOP[a][b] only if a == K or
+// b == 0). in holds one halo cell on each side: cell e is in[(e+1)*H ...]. Output cells whose
+// global index is 0 / m-1 get the Nitsche correction (efirst / elast local cell, -1 if none).
+template <typename T, int K, int NC, bool BND>
+__device__ __forceinline__ void dg_sipg(const T (&in)[(NC + 2) * (K + 1)], T (&out)[NC * (K + 1)], int efirst,
+                                        int elast) {
+  constexpr int H = K + 1;
+  using R = Ref<K>;
+#pragma unroll
+  for (int e = 0; e < NC; ++e)
+#pragma unroll
+    for (int a = 0; a < H; ++a) {
+      T s = T(0);
+#pragma unroll
+      for (int b = 0; b < H; ++b) s += cref<T>(R::LO0 + a * H + b) * in[(e + 1) * H + b];
+#pragma unroll
+      for (int b = 0; b < H; ++b)
+        if (a == 0 || b == K) s += cref<T>(R::LOM + a * H + b) * in[e * H + b];
+#pragma unroll
+      for (int b = 0; b < H; ++b)
+        if (a == K || b == 0) s += cref<T>(R::LOP + a * H + b) * in[(e + 2) * H + b];
+      if (BND) {
+        if (e == efirst) {
+#pragma unroll
+          for (int b = 0; b < H; ++b) s += cref<T>(R::DLF + a * H + b) * in[(e + 1) * H + b];
+        }
+        if (e == elast) {
+#pragma unroll
+          for (int b = 0; b < H; ++b) s += cref<T>(R::DLL + a * H + b) * in[(e + 1) * H + b];
+        }
+      }
+      out[e * H + a] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// brick geometry
+// ---------------------------------------------------------------------------------------------
+template <typename T, int K, int BX, int BY, int BZ>
+struct Brick {
+  static constexpr int H = K + 1;
+  static constexpr int VEC = 16 / static_cast<int>(sizeof(T));  // elements per 16 B (TMA granule)
+  static constexpr int rup(int v) { return (v + VEC - 1) / VEC * VEC; }
+  static constexpr int B(int a) { return a == 0 ? BX : (a == 1 ? BY : BZ); }
+  static constexpr int N(int a) { return B(a) * H; }
+  static constexpr int O1(int c) { return c == 0 ? 1 : 0; }
+  static constexpr int O2(int c) { return c == 2 ? 1 : 2; }
+  static constexpr int LC(int c) { return N(c) + H + 1; }       // c range [-H, N_c]
+  static constexpr int PC(int c) { return odd(LC(c)); }         // padded c extent of intermediates
+  static constexpr int LO1H(int c) { return N(O1(c)) + 2 * H; }  // o1 range [-H, N + H)
+  static constexpr int LO2H(int c) { return N(O2(c)) + 2 * H; }
+  // staged input box of component c, TMA box order (x fastest, x pitch UX):
+  //   c=0: [z=o2][y=o1][x=c]   c=1: [z=o2][y=c][x=o1]   c=2: [z=c][y=o2][x=o1]
+  // TMA requires the x start of a box to be 16-B aligned and >= 0, so every row is loaded from the
+  // 16-B aligned position at or below the needed start; UX carries VEC-1 elements of slack and the
+  // consumers add the per-brick (per-row for c=0) shift.
+  static constexpr int XEXT(int c) { return c == 0 ? LC(0) : LO1H(c); }
+  static constexpr int UX(int c) { return rup(XEXT(c) + VEC - 1); }
+  static constexpr int UY(int c) { return c == 0 ? LO1H(0) : (c == 1 ? LC(1) : LO2H(2)); }
+  static constexpr int UZ(int c) { return c == 2 ? LC(2) : LO2H(c); }
+  static constexpr int sizeU(int c) { return UX(c) * UY(c) * UZ(c); }  // bytes loaded by one TMA box
+  static constexpr int sizeA1(int c) { return N(O2(c)) * LO1H(c) * PC(c); }
+  static constexpr int sizeST(int c) { return N(O2(c)) * N(O1(c)) * PC(c); }
+  static constexpr int mx3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
+  static constexpr int U = rup(mx3(sizeU(0), sizeU(1), sizeU(2)) + VEC);  // + clamp slack
+  static constexpr int A1 = mx3(sizeA1(0), sizeA1(1), sizeA1(2));
+  static constexpr int ST = mx3(sizeST(0), sizeST(1), sizeST(2));
+  static constexpr int PXT = rup(N(0) + H + VEC - 1);  // pressure box [-H, N) per axis, x pitch PXT
+  static constexpr int PBOX = (N(2) + H) * (N(1) + H) * PXT;
+  static constexpr int PBUF = rup(PBOX + VEC);
+  static constexpr int YX = odd(N(0));
+  static constexpr int YP = N(2) * N(1) * YX;
+  static constexpr bool ALIAS = 2 * ST <= U;  // S and T overwrite the dead U buffer of the component
+  // layout: [U buffer 0][U buffer 1][P box][A1 (also Q2)][B1][Q][YP][S,T if no alias][mbarriers]
+  static constexpr int OFF_U1 = U;
+  static constexpr int OFF_P = 2 * U;
+  static constexpr int OFF_A1 = OFF_P + PBUF;
+  static constexpr int OFF_B1 = OFF_A1 + A1;
+  static constexpr int OFF_Q = OFF_B1 + ST;
+  static constexpr int OFF_YP = OFF_Q + ST;
+  static constexpr int OFF_ST = OFF_YP + YP;  // only used when !ALIAS
+  static constexpr int END = OFF_YP + YP + (ALIAS ? 0 : 2 * ST);
+  static constexpr size_t BYTES = (static_cast<size_t>(END) * sizeof(T) + 15) / 16 * 16 + 3 * 8;
+  static constexpr int stride(int axis, int a0, int a1) { return axis == 0 ? 1 : (axis == 1 ? a0 : a0 * a1); }
+};
+
+struct Maps {
+  CUtensorMap u0, u1, u2, p;  // rank-1 rows of u_x; 3D boxes of u_y, u_z (constrained planes OOB), p
+};
+
+struct Geo {
+  int m, n;
+  int c0[3];  // brick cell origin
+  int g0[3];  // brick node origin
+};
+
+// ---------------------------------------------------------------------------------------------
+// mbarrier / TMA primitives
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const CUtensorMap* map, int x, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int floor_to(int v, int q) { return (v >= 0 ? v / q : -((-v + q - 1) / q)) * q; }
+
+// smem origin offsets of the staged rows (element of x = g0x - H relative to the row start)
+template <typename T>
+__device__ __forceinline__ int brick_shift(const Geo& G, int H) {
+  constexpr int VEC = 16 / static_cast<int>(sizeof(T));
+  const int x0 = G.g0[0] - H;
+  return x0 - floor_to(x0, VEC);
+}
+// u_x rows: the 1D start (z n + y)(n+1) + x0 has the same residue mod VEC for every z (n % VEC == 0)
+template <typename T>
+__device__ __forceinline__ int row_shift0(const Geo& G, int H, int y) {
+  constexpr int VEC = 16 / static_cast<int>(sizeof(T));
+  const int v = (y * (G.n + 1) + G.g0[0] - H) % VEC;
+  return v < 0 ? v + VEC : v;
+}
+
+// ---------------------------------------------------------------------------------------------
+// staging: TMA (default) or cp.async element copies (fallback when a pitch is not 16-B aligned,
+// i.e. fp32 on level 0 with even k). Both write the same TMA box layout.
+// ---------------------------------------------------------------------------------------------
+template <typename T, int K, int BX, int BY, int BZ, int NT, int C, bool TMA>
+__device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restrict__ x, const Maps& M, const Geo& G) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  constexpr int UX = BR::UX(C), UY = BR::UY(C), UZ = BR::UZ(C);
+  const int n = G.n;
+  const int tid = threadIdx.x;
+  if constexpr (TMA) {
+    if constexpr (C == 0) {
+      // one rank-1 TMA per x-row inside the domain (rows have the odd pitch n+1); warp 0 issues,
+      // rows outside the domain are zero-filled directly
+      if (tid < 32) {
+        const int y0 = G.g0[1] - H, z0 = G.g0[2] - H;
+        const int ny = max(0, min(n, y0 + UY) - max(0, y0)), nz = max(0, min(n, z0 + UZ) - max(0, z0));
+        if (tid == 0) mbar_expect(bar, static_cast<unsigned>(ny * nz * UX * sizeof(T)));
+        __syncwarp();
+        for (int r = tid; r < UY * UZ; r += 32) {
+          const int y = y0 + r % UY, z = z0 + r / UY;
+          T* dst = sU + r * UX;
+          if (y >= 0 && y < n && z >= 0 && z < n) {
+            const int start = (z * n + y) * (n + 1) + G.g0[0] - H;
+            const int sal = floor_to(start, BR::VEC), ss = max(sal, 0);
+            tma_load_1d(dst + (ss - sal), &M.u0, ss, bar);
+          } else {
+#pragma unroll
+            for (int i = 0; i < UX; ++i) dst[i] = T(0);
+          }
+        }
+      }
+    } else {
+      if (tid == 0) {
+        mbar_expect(bar, static_cast<unsigned>(BR::sizeU(C) * sizeof(T)));
+        // u_y / u_z maps start one row / plane in, so the constrained planes 0 and n fall outside
+        const int xal = floor_to(G.g0[0] - H, BR::VEC), xs = max(xal, 0);
+        if (C == 1) tma_load_3d(sU + (xs - xal), &M.u1, xs, G.g0[1] - H - 1, G.g0[2] - H, bar);
+        else tma_load_3d(sU + (xs - xal), &M.u2, xs, G.g0[1] - H, G.g0[2] - H - 1, bar);
+      }
+    }
+  } else {
+    int gd[3] = {n, n, n};
+    gd[C] = n + 1;
+    const T* xc = x + C * (static_cast<int64_t>(n + 1) * n * n);
+    constexpr int XE = BR::XEXT(C);
+    for (int i = tid; i < XE * UY * UZ; i += NT) {
+      const int l[3] = {i % XE - H, (i / XE) % UY - H, i / (XE * UY) - H};
+      const int g[3] = {G.g0[0] + l[0], G.g0[1] + l[1], G.g0[2] + l[2]};
+      bool ok = g[0] >= 0 && g[1] >= 0 && g[2] >= 0 && g[0] < gd[0] && g[1] < gd[1] && g[2] < gd[2];
+      ok = ok && g[C] != 0 && g[C] != n;
+      const T* src = ok ? xc + (static_cast<int64_t>(g[2]) * gd[1] + g[1]) * gd[0] + g[0] : xc;
+      const int sh = C == 0 ? row_shift0<T>(G, H, g[1]) : brick_shift<T>(G, H);
+      cp_async_elem(sU + (i / XE) * UX + sh + (l[0] + H), src, ok);
+    }
+  }
+}
+
+template <typename T, int K, int BX, int BY, int BZ, int NT, bool TMA>
+__device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const T* __restrict__ x, const Maps& M, const Geo& G) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_expect(bar, static_cast<unsigned>(BR::PBOX * sizeof(T)));
+      const int xal = floor_to(G.g0[0] - H, BR::VEC), xs = max(xal, 0);
+      tma_load_3d(sP + (xs - xal), &M.p, xs, G.g0[1] - H, G.g0[2] - H, bar);
+    }
+  } else {
+    constexpr int E0 = BR::N(0) + H, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
+    const int n = G.n;
+    const int sh = brick_shift<T>(G, H);
+    const T* xp = x + 3 * (static_cast<int64_t>(n + 1) * n * n);
+    for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
+      const int lx = i % E0, ly = (i / E0) % E1, lz = i / (E0 * E1);
+      const int gx = G.g0[0] + lx - H, gy = G.g0[1] + ly - H, gz = G.g0[2] + lz - H;
+      const bool ok = gx >= 0 && gy >= 0 && gz >= 0 && gx < n && gy < n && gz < n;
+      const T* src = ok ? xp + (static_cast<int64_t>(gz) * n + gy) * n + gx : xp;
+      cp_async_elem(sP + (lz * E1 + ly) * BR::PXT + sh + lx, src, ok);
+    }
+  }
+}
+
+// Boundary fix-ups after a TMA box landed (bricks touching the x ends only):
+//  - u_x rows are rank-1 copies that ignore the row structure: zero the columns outside [1, n-1]
+//    (halo beyond the domain and the constrained boundary-normal nodes x = 0, x = n);
+//  - u_y, u_z, p boxes clamped at x = 0 leave the x < 0 halo columns unwritten: zero them.
+template <typename T, int K, int BX, int BY, int BZ, int NT>
+__device__ __forceinline__ void fix_columns(T* sU0, T* sU1, T* sU2, T* sP, const Geo& G) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  const int x0 = G.g0[0] - H;
+  if (x0 >= 0 && x0 + BR::XEXT(0) <= G.n) return;
+  if (sU0) {
+    constexpr int XE = BR::XEXT(0), UY = BR::UY(0), ROWS = BR::UY(0) * BR::UZ(0);
+    for (int i = threadIdx.x; i < ROWS * XE; i += NT) {
+      const int r = i / XE, gx = x0 + i % XE;
+      if (gx <= 0 || gx >= G.n) sU0[r * BR::UX(0) + row_shift0<T>(G, H, G.g0[1] - H + r % UY) + i % XE] = T(0);
+    }
+  }
+  if (x0 >= 0) return;
+  const int sh = brick_shift<T>(G, H);
+  auto zero_low = [&](T* buf, int rows, int pitch) {
+    for (int i = threadIdx.x; i < rows * H; i += NT) buf[(i / H) * pitch + sh + i % H] = T(0);
+  };
+  if (sU1) zero_low(sU1, BR::UY(1) * BR::UZ(1), BR::UX(1));
+  if (sU2) zero_low(sU2, BR::UY(2) * BR::UZ(2), BR::UX(2));
+  if (sP) zero_low(sP, (BR::N(1) + H) * (BR::N(2) + H), BR::PXT);
+}
+
+// ---------------------------------------------------------------------------------------------
+// one velocity component (U already staged in sU); if C == 2 and Gn != nullptr, the next brick's
+// pressure box is issued as soon as this brick's P box is dead.
+// ---------------------------------------------------------------------------------------------
+template <typename T, int K, int BX, int BY, int BZ, int NT, int C, bool RESID, bool TMA>
+__device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const Geo* Gn, const T* __restrict__ x,
+                                          T* __restrict__ y, const T* __restrict__ b, const Maps& M, uint64_t* barP) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  constexpr int O1 = BR::O1(C), O2 = BR::O2(C);
+  constexpr int NCc = BR::B(C), NO1 = BR::B(O1), NO2 = BR::B(O2);
+  constexpr int Nc = BR::N(C), No1 = BR::N(O1), No2 = BR::N(O2);
+  constexpr int LC = BR::LC(C), PC = BR::PC(C), LO1H = BR::LO1H(C);
+  constexpr int UX = BR::UX(C), UY = BR::UY(C);
+  const int tid = threadIdx.x;
+  const int n = G.n, m = G.m;
+  const int64_t sizeV = static_cast<int64_t>(n + 1) * n * n;
+  int64_t gd[3] = {n, n, n};
+  gd[C] = n + 1;
+  const int64_t st[3] = {1, gd[0], gd[0] * gd[1]};
+
+  T* sA1 = sm + BR::OFF_A1;
+  T* sB1 = sm + BR::OFF_B1;
+  T* sQ = sm + BR::OFF_Q;
+  T* sP = sm + BR::OFF_P;
+  T* sYP = sm + BR::OFF_YP;
+  T* sS = BR::ALIAS ? sU : sm + BR::OFF_ST;
+  T* sT = sS + BR::ST;
+
+  // ---- Q2 = M_o2 p over c in [-H, N_c), o1 owned, o2 owned  (pencils along o2, from the P box) ----
+  {
+    T* sQ2 = sA1;
+    constexpr int E1P = BR::N(1) + H;
+    constexpr int PSC = BR::stride(C, BR::PXT, E1P), PSO1 = BR::stride(O1, BR::PXT, E1P),
+                  PSO2 = BR::stride(O2, BR::PXT, E1P);
+    constexpr int NPEN = (Nc + H) * No1;
+    for (int p = tid; p < NPEN; p += NT) {
+      // consecutive threads walk the P-box x axis (c for C=0, o1 otherwise): conflict-free
+      const int ci = C == 0 ? p % (Nc + H) : p / No1;
+      const int oi = C == 0 ? p / (Nc + H) : p % No1;
+      const T* src = sP + brick_shift<T>(G, H) + ci * PSC + (oi + H) * PSO1 + H * PSO2;
+      T in[No2];
+#pragma unroll
+      for (int j = 0; j < No2; ++j) in[j] = src[j * PSO2];
+      T out[No2];
+      dg_mass<T, K, NO2, 0>(in, out);
+#pragma unroll
+      for (int j = 0; j < No2; ++j) sQ2[(j * No1 + oi) * PC + ci] = out[j];
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, NT, TMA>(sP, barP, x, M, *Gn);
+    if (!TMA && C == 2) cp_async_commit();
+    // Q = M_o1 Q2 (pencils along o1)
+    constexpr int NPEN2 = (Nc + H) * No2;
+    for (int p = tid; p < NPEN2; p += NT) {
+      const int ci = p % (Nc + H), oj = p / (Nc + H);
+      T in[No1];
+#pragma unroll
+      for (int j = 0; j < No1; ++j) in[j] = sQ2[(oj * No1 + j) * PC + ci];
+      T out[No1];
+      dg_mass<T, K, NO1, 0>(in, out);
+#pragma unroll
+      for (int j = 0; j < No1; ++j) sQ[(oj * No1 + j) * PC + ci] = out[j];
+    }
+    __syncthreads();
+  }
+  // ---- pass 1 (along o2): A1 = M_o2 U  (c full, o1 with halo, o2 owned);  B1 = L_o2 U (o1 owned) ----
+  {
+    const int cell_o2 = G.c0[O2];
+    const bool bnd = (cell_o2 == 0) || (cell_o2 + NO2 >= m);
+    const int efirst = (cell_o2 == 0) ? 0 : -1;
+    const int elast = (m - 1 - cell_o2 < NO2) ? m - 1 - cell_o2 : -1;
+    constexpr int NPEN = LC * LO1H;
+    for (int p = tid; p < NPEN; p += NT) {
+      // consecutive threads walk the staged box's x axis: c for C=0, o1 for C=1,2
+      const int ci = C == 0 ? p % LC : p / LO1H;
+      const int oi = C == 0 ? p / LC : p % LO1H;
+      // element (c=ci, o1=oi, o2=j) of the staged box
+      const int ub = C == 0 ? oi * UX + ci + row_shift0<T>(G, H, G.g0[1] - H + oi)
+                            : (C == 1 ? ci * UX + oi : ci * UY * UX + oi) + brick_shift<T>(G, H);
+      constexpr int US = C == 0 ? UX * UY : (C == 1 ? UX * UY : UX);  // stride along o2
+      T in[(NO2 + 2) * H];
+#pragma unroll
+      for (int j = 0; j < (NO2 + 2) * H; ++j) in[j] = sU[ub + j * US];
+      T a1[No2];
+      dg_mass<T, K, NO2, 1>(in, a1);
+#pragma unroll
+      for (int j = 0; j < No2; ++j) sA1[(j * LO1H + oi) * PC + ci] = a1[j];
+      if (oi >= H && oi < H + No1) {
+        T b1[No2];
+        if (bnd) dg_sipg<T, K, NO2, true>(in, b1, efirst, elast);
+        else dg_sipg<T, K, NO2, false>(in, b1, -1, -1);
+#pragma unroll
+        for (int j = 0; j < No2; ++j) sB1[(j * No1 + (oi - H)) * PC + ci] = b1[j];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- pass 2 (along o1): S = M_o1 A1, T = L_o1 A1 + M_o1 B1  (c full, o1/o2 owned) ----
+  {
+    const int cell_o1 = G.c0[O1];
+    const bool bnd = (cell_o1 == 0) || (cell_o1 + NO1 >= m);
+    const int efirst = (cell_o1 == 0) ? 0 : -1;
+    const int elast = (m - 1 - cell_o1 < NO1) ? m - 1 - cell_o1 : -1;
+    constexpr int NPEN = LC * No2;
+    for (int p = tid; p < NPEN; p += NT) {
+      const int ci = p % LC, oj = p / LC;
+      T in[(NO1 + 2) * H];
+#pragma unroll
+      for (int j = 0; j < (NO1 + 2) * H; ++j) in[j] = sA1[(oj * LO1H + j) * PC + ci];
+      T s[No1], t[No1];
+      dg_mass<T, K, NO1, 1>(in, s);
+      if (bnd) dg_sipg<T, K, NO1, true>(in, t, efirst, elast);
+      else dg_sipg<T, K, NO1, false>(in, t, -1, -1);
+      T bb[No1];
+#pragma unroll
+      for (int j = 0; j < No1; ++j) bb[j] = sB1[(oj * No1 + j) * PC + ci];
+      T mb[No1];
+      dg_mass<T, K, NO1, 0>(bb, mb);
+#pragma unroll
+      for (int j = 0; j < No1; ++j) {
+        sS[(oj * No1 + j) * PC + ci] = s[j];
+        sT[(oj * No1 + j) * PC + ci] = t[j] + mb[j];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- pass 3 (along c): y_c = h (L_c S + M_c T) + h^2 D^T Q ;  y_p += h^2 D S ----
+  {
+    using R = Ref<K>;
+    constexpr int P = K + 2;
+    const T h2 = h * h;
+    const T* __restrict__ bc = RESID ? b + C * sizeV : nullptr;
+    T* __restrict__ yc = y + C * sizeV;
+    constexpr int NPEN = No1 * No2;
+    constexpr int YSC = BR::stride(C, BR::YX, BR::N(1)), YSO1 = BR::stride(O1, BR::YX, BR::N(1)),
+                  YSO2 = BR::stride(O2, BR::YX, BR::N(1));
+    for (int p = tid; p < NPEN; p += NT) {
+      const int oi = p % No1, oj = p / No1;
+      T s[LC], t[LC], q[LC - 1];
+      const int base = (oj * No1 + oi) * PC;
+#pragma unroll
+      for (int j = 0; j < LC; ++j) {
+        s[j] = sS[base + j];
+        t[j] = sT[base + j];
+      }
+#pragma unroll
+      for (int j = 0; j < LC - 1; ++j) q[j] = sQ[base + j];
+      int g[3];
+      g[O1] = G.g0[O1] + oi;
+      g[O2] = G.g0[O2] + oj;
+      const bool inside = g[O1] < n && g[O2] < n;
+      T* yp = sYP + oi * YSO1 + oj * YSO2;
+#pragma unroll
+      for (int e = 0; e < NCc; ++e) {
+#pragma unroll
+        for (int a = 0; a < H; ++a) {
+          const int j = e * H + a + H;  // pencil index of the output node
+          T v = T(0), w = T(0);
+#pragma unroll
+          for (int bq = 0; bq < P; ++bq) {
+            v += cref<T>(R::LP + a * P + bq) * s[j - a + bq] + cref<T>(R::MP + a * P + bq) * t[j - a + bq];
+            if (a == 0)
+              v += cref<T>(R::LP + (K + 1) * P + bq) * s[j - H + bq] + cref<T>(R::MP + (K + 1) * P + bq) * t[j - H + bq];
+          }
+#pragma unroll
+          for (int i = 0; i < H; ++i) {
+            w += cref<T>(R::D + i * P + a) * q[j - a + i];
+            if (a == 0) w += cref<T>(R::D + i * P + H) * q[j - H + i];
+          }
+          g[C] = G.g0[C] + e * H + a;
+          if (inside && g[C] < n) {
+            const int64_t gi = g[0] * st[0] + g[1] * st[1] + g[2] * st[2];
+            T r = h * v + h2 * w;
+            if (g[C] == 0) r = T(0);  // constrained boundary-normal row
+            else if (RESID) r = bc[gi] - r;
+            yc[gi] = r;
+          }
+        }
+        // pressure rows of cell e: y_p += h^2 D S
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+          T z = T(0);
+#pragma unroll
+          for (int bq = 0; bq < P; ++bq) z += cref<T>(R::D + i * P + bq) * s[e * H + H + bq];
+          yp[(e * H + i) * YSC] += h2 * z;
+        }
+      }
+      // the constrained plane g_c = n belongs to the brick holding the last cell along c
+      if (inside && G.c0[C] + NCc >= m) {
+        g[C] = n;
+        yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
+      }
+    }
+  }
+  fence_proxy_async();  // generic reads of this U buffer happen-before the next TMA into it
+  __syncthreads();
+}
+
+__device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, int bx, int by, int bz, int H) {
+  const int ix = brick % nbx, iy = (brick / nbx) % nby, iz = brick / (nbx * nby);
+  G.c0[0] = ix * bx;
+  G.c0[1] = iy * by;
+  G.c0[2] = iz * bz;
+  for (int a = 0; a < 3; ++a) G.g0[a] = G.c0[a] * H;
+}
+
+// Persistent kernel: each CTA walks bricks blockIdx.x, blockIdx.x + gridDim.x, ... The three
+// component boxes of a brick alternate between two U buffers (each with its own mbarrier) so that
+// the TMA staging of the next component -- and of the next brick's first component and pressure
+// box -- overlaps compute.
+template <typename T, int K, int BX, int BY, int BZ, int NT, bool RESID, bool TMA>
+__global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
+                                                             const T* __restrict__ b, int m, T h,
+                                                             const Maps* __restrict__ mapsp) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (BR::BYTES - 3 * 8));  // [buf0, buf1, P]
+  const int nbx = (m + BX - 1) / BX, nby = (m + BY - 1) / BY, nbz = (m + BZ - 1) / BZ;
+  const int nbricks = nbx * nby * nbz;
+  Geo G, Gn;
+  G.m = Gn.m = m;
+  G.n = Gn.n = m * H;
+  const int n = G.n;
+  const int64_t offP = 3 * static_cast<int64_t>(n + 1) * n * n;
+  T* sP = sm + BR::OFF_P;
+  T* sYP = sm + BR::OFF_YP;
+  const Maps& maps = *mapsp;  // tensor maps live in global memory (64-B aligned slots)
+  int brick = blockIdx.x;
+  if (brick >= nbricks) return;
+  if (TMA && threadIdx.x == 0) {
+    mbar_init(&bars[0]);
+    mbar_init(&bars[1]);
+    mbar_init(&bars[2]);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_proxy_async();
+  __syncthreads();
+  brick_geo(G, brick, nbx, nby, BX, BY, BZ, H);
+  issue_p<T, K, BX, BY, BZ, NT, TMA>(sP, &bars[2], x, maps, G);
+  issue_u<T, K, BX, BY, BZ, NT, 0, TMA>(sm, &bars[0], x, maps, G);
+  if (!TMA) cp_async_commit();
+  int u0 = 0;
+  unsigned ph[2] = {0, 0}, phP = 0;  // mbarrier phase of buffer 0 / 1 / P
+  for (; brick < nbricks; brick += gridDim.x) {
+    const int ia = u0, ib = u0 ^ 1;
+    T* bufA = sm + (ia ? BR::OFF_U1 : 0);  // components 0 and 2 of this brick
+    T* bufB = sm + (ib ? BR::OFF_U1 : 0);  // component 1, then component 0 of the next brick
+    const int next = brick + gridDim.x;
+    const bool has_next = next < nbricks;
+    if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H);
+    issue_u<T, K, BX, BY, BZ, NT, 1, TMA>(bufB, &bars[ib], x, maps, G);
+    for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
+    if (TMA) {
+      mbar_wait(&bars[2], phP);
+      phP ^= 1;
+      mbar_wait(&bars[ia], ph[ia]);
+      ph[ia] ^= 1;
+    } else {
+      cp_async_commit();
+      cp_async_wait<1>();  // P box and U_0 of this brick
+    }
+    __syncthreads();
+    if (TMA) {
+      fix_columns<T, K, BX, BY, BZ, NT>(bufA, nullptr, nullptr, sP, G);
+      __syncthreads();
+    }
+    component<T, K, BX, BY, BZ, NT, 0, RESID, TMA>(sm, bufA, G, h, nullptr, x, y, b, maps, &bars[2]);
+    issue_u<T, K, BX, BY, BZ, NT, 2, TMA>(bufA, &bars[ia], x, maps, G);
+    if (TMA) {
+      mbar_wait(&bars[ib], ph[ib]);
+      ph[ib] ^= 1;
+    } else {
+      cp_async_commit();
+      cp_async_wait<1>();  // U_1
+    }
+    __syncthreads();
+    if (TMA) {
+      fix_columns<T, K, BX, BY, BZ, NT>(nullptr, bufB, nullptr, nullptr, G);
+      __syncthreads();
+    }
+    component<T, K, BX, BY, BZ, NT, 1, RESID, TMA>(sm, bufB, G, h, nullptr, x, y, b, maps, &bars[2]);
+    if (has_next) issue_u<T, K, BX, BY, BZ, NT, 0, TMA>(bufB, &bars[ib], x, maps, Gn);
+    if (TMA) {
+      mbar_wait(&bars[ia], ph[ia]);
+      ph[ia] ^= 1;
+    } else {
+      cp_async_commit();
+      cp_async_wait<1>();  // U_2
+    }
+    __syncthreads();
+    if (TMA) {
+      fix_columns<T, K, BX, BY, BZ, NT>(nullptr, nullptr, bufA, nullptr, G);
+      __syncthreads();
+    }
+    component<T, K, BX, BY, BZ, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
+                                                   &bars[2]);
+    // write the pressure rows of this brick
+    {
+      constexpr int N0 = BR::N(0), N1 = BR::N(1), N2 = BR::N(2);
+      for (int i = threadIdx.x; i < N0 * N1 * N2; i += NT) {
+        const int lx = i % N0, ly = (i / N0) % N1, lz = i / (N0 * N1);
+        const int gx = G.g0[0] + lx, gy = G.g0[1] + ly, gz = G.g0[2] + lz;
+        if (gx >= n || gy >= n || gz >= n) continue;
+        const int64_t gi = offP + (static_cast<int64_t>(gz) * n + gy) * n + gx;
+        const T v = sYP[(lz * N1 + ly) * BR::YX + lx];
+        y[gi] = RESID ? b[gi] - v : v;
+      }
+    }
+    __syncthreads();  // y_p accumulator is re-zeroed by the next brick
+    G = Gn;
+    u0 ^= 1;
+  }
+  if (!TMA) cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------------------------
+// host: tensor maps
+// ---------------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SMG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw cuda_error("cuTensorMapEncodeTiled not available");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <typename T>
+void encode(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+            const uint32_t* box) {
+  const uint32_t es[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                 rank, const_cast<void*>(base), dims, strides_bytes, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+// TMA needs 16-B aligned row pitches / base offsets (n * sizeof(T) % 16 == 0); boxes are kept no
+// larger than the tensor (small coarse levels take the cp.async path).
+template <typename T, int K, int BX, int BY, int BZ>
+bool tma_ok(int n) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  if ((static_cast<int64_t>(n) * sizeof(T)) % 16 != 0) return false;
+  const int lim = n - 1;  // smallest extent among the u_y / u_z maps
+  const int ext[] = {BR::UX(1), BR::UY(1), BR::UZ(1), BR::UX(2), BR::UY(2), BR::UZ(2), BR::PXT, BR::N(1) + H,
+                     BR::N(2) + H};
+  for (int e : ext)
+    if (e > lim) return false;
+  return true;
+}
+
+template <typename T, int K, int BX, int BY, int BZ>
+Maps make_maps(const T* x, int n) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int H = K + 1;
+  Maps M;
+  std::memset(&M, 0, sizeof(M));
+  const uint64_t es = sizeof(T);
+  const uint64_t nn = static_cast<uint64_t>(n);
+  const uint64_t sizeV = (nn + 1) * nn * nn;
+  {  // u_x as one long row
+    const uint64_t d[1] = {sizeV};
+    const uint64_t s[1] = {sizeV * es};  // unused for rank 1
+    const uint32_t box[1] = {static_cast<uint32_t>(BR::UX(0))};
+    encode<T>(&M.u0, x, 1, d, s, box);
+  }
+  {  // u_y: dims (x n, y n+1, z n); base one row in -> y' = y - 1 in [0, n-1)
+    const uint64_t d[3] = {nn, nn - 1, nn};
+    const uint64_t s[2] = {nn * es, nn * (nn + 1) * es};
+    const uint32_t box[3] = {static_cast<uint32_t>(BR::UX(1)), static_cast<uint32_t>(BR::UY(1)),
+                             static_cast<uint32_t>(BR::UZ(1))};
+    encode<T>(&M.u1, x + sizeV + nn, 3, d, s, box);
+  }
+  {  // u_z: dims (x n, y n, z n+1); base one plane in -> z' = z - 1 in [0, n-1)
+    const uint64_t d[3] = {nn, nn, nn - 1};
+    const uint64_t s[2] = {nn * es, nn * nn * es};
+    const uint32_t box[3] = {static_cast<uint32_t>(BR::UX(2)), static_cast<uint32_t>(BR::UY(2)),
+                             static_cast<uint32_t>(BR::UZ(2))};
+    encode<T>(&M.u2, x + 2 * sizeV + nn * nn, 3, d, s, box);
+  }
+  {  // p
+    const uint64_t d[3] = {nn, nn, nn};
+    const uint64_t s[2] = {nn * es, nn * nn * es};
+    const uint32_t box[3] = {static_cast<uint32_t>(BR::PXT), static_cast<uint32_t>(BR::N(1) + H),
+                             static_cast<uint32_t>(BR::N(2) + H)};
+    encode<T>(&M.p, x + 3 * sizeV, 3, d, s, box);
+  }
+  return M;
+}
+
+template <typename T, int K, int BX, int BY, int BZ, int NT>
+void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
+  const int m = dl.lay.m, n = dl.lay.n;
+  const T h = static_cast<T>(1.0 / m);
+  const int nbricks = ((m + BX - 1) / BX) * ((m + BY - 1) / BY) * ((m + BZ - 1) / BZ);
+  static int num_sms = 0;
+  if (num_sms == 0) SMG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ctx.device));
+  const dim3 grid(std::min(nbricks, num_sms));
+  const size_t smem = BR::BYTES;
+  const bool tma = tma_ok<T, K, BX, BY, BZ>(n) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  const Maps* dmaps = nullptr;
+  if (tma) {
+    // tensor maps are cached per (input vector, level, precision) in 64-B aligned global slots,
+    // written stream-ordered before the launch
+    const TmapKey key{x, level, static_cast<int>(sizeof(T))};
+    auto it = ctx.tmap_slots.find(key);
+    if (it == ctx.tmap_slots.end()) {
+      const int slot = ctx.tmap_next++ % kTmapSlots;
+      for (auto e = ctx.tmap_slots.begin(); e != ctx.tmap_slots.end();)
+        e = (e->second == slot) ? ctx.tmap_slots.erase(e) : std::next(e);
+      Maps mh = make_maps<T, K, BX, BY, BZ>(static_cast<const T*>(x), n);
+      char* dst = static_cast<char*>(ctx.tmap_dev) + static_cast<size_t>(slot) * kTmapSlotBytes;
+      SMG_CUDA(cudaMemcpyAsync(dst, &mh, sizeof(Maps), cudaMemcpyHostToDevice, ctx.stream));
+      SMG_CUDA(cudaStreamSynchronize(ctx.stream));  // mh is a stack temporary
+      it = ctx.tmap_slots.emplace(key, slot).first;
+    }
+    dmaps = reinterpret_cast<const Maps*>(static_cast<char*>(ctx.tmap_dev) +
+                                          static_cast<size_t>(it->second) * kTmapSlotBytes);
+  }
+  static_assert(sizeof(Maps) <= kTmapSlotBytes, "tensor-map slot too small");
+  auto go = [&](auto kern) {
+    SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, NT, smem, ctx.stream>>>(static_cast<const T*>(x), static_cast<T*>(y), static_cast<const T*>(b), m, h,
+                                         dmaps);
+  };
+  if (b) {
+    if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, true, true>);
+    else go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, true, false>);
+  } else {
+    if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, false, true>);
+    else go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, false, false>);
+  }
+  SMG_CUDA(cudaGetLastError());
+  ++ctx.launches;
+}
+
+}  // namespace
+
+// Brick shape (cells) per degree: fp64 SMEM ~80-200 KB, one persistent CTA per SM.
+template <int K> struct BrickShape;
+template <> struct BrickShape<1> { static constexpr int X = 8, Y = 4, Z = 4; };
+template <> struct BrickShape<2> { static constexpr int X = 4, Y = 4, Z = 4; };
+template <> struct BrickShape<3> { static constexpr int X = 4, Y = 2, Z = 2; };
+template <> struct BrickShape<4> { static constexpr int X = 2, Y = 2, Z = 2; };
+template <> struct BrickShape<5> { static constexpr int X = 2, Y = 2, Z = 1; };
+template <> struct BrickShape<6> { static constexpr int X = 2, Y = 1, Z = 1; };
+template <> struct BrickShape<7> { static constexpr int X = 2, Y = 1, Z = 1; };
+
+template <int K>
+void vmult_launch_k(Context& ctx, int level, int prec, void* y, const void* x, const void* b) {
+  using S = BrickShape<K>;
+  if (prec == SMG_F64) launch_t<double, K, S::X, S::Y, S::Z, 256>(ctx, level, y, x, b);
+  else launch_t<float, K, S::X, S::Y, S::Z, 256>(ctx, level, y, x, b);
+}
+
+template <int K>
+void vmult_upload_k(const double* t, const float* f) {
+  SMG_CUDA(cudaMemcpyToSymbol(c_ref_d, t, sizeof(double) * kRefTotal));
+  SMG_CUDA(cudaMemcpyToSymbol(c_ref_f, f, sizeof(float) * kRefTotal));
+}
+
+#define SMG_INSTANTIATE_VMULT(K)                                                                  \
+  template void vmult_launch_k<K>(Context&, int, int, void*, const void*, const void*);           \
+  template void vmult_upload_k<K>(const double*, const float*);
+
+}  // namespace smg

@@ -35,7 +35,10 @@ def dev(x, dtype=torch.float64):
     return torch.from_numpy(np.ascontiguousarray(x)).to(device="cuda", dtype=dtype)
 
 
-@pytest.mark.parametrize("k,level", [(1, 0), (1, 1), (1, 2), (2, 0), (2, 1), (2, 2), (3, 1), (3, 2), (4, 1)])
+# levels >= 2-3 take the TMA staging path with interior bricks; small levels the cp.async path
+@pytest.mark.parametrize("k,level", [(1, 0), (1, 1), (1, 2), (1, 3), (1, 4), (2, 0), (2, 1), (2, 2), (2, 3), (2, 4),
+                                     (3, 1), (3, 2), (3, 3), (4, 1), (4, 2), (5, 1), (5, 2), (6, 1), (6, 2), (7, 1),
+                                     (7, 2)])
 def test_vmult_fp64_matches_oracle(k, level):
     ctx = smg.Context(k, level)
     x = rand_vec(k, level, 1, zero_constrained=False)  # constrained entries must be ignored
@@ -44,7 +47,7 @@ def test_vmult_fp64_matches_oracle(k, level):
     assert rel(y, y_ref) <= 1e-12
 
 
-@pytest.mark.parametrize("k,level", [(1, 2), (2, 2), (3, 1)])
+@pytest.mark.parametrize("k,level", [(1, 2), (1, 3), (2, 2), (2, 3), (3, 1), (3, 2), (4, 2), (5, 2), (7, 2)])
 def test_vmult_fp32_matches_oracle(k, level):
     ctx = smg.Context(k, level)
     x = rand_vec(k, level, 2)
@@ -53,7 +56,7 @@ def test_vmult_fp32_matches_oracle(k, level):
     assert rel(y, y_ref) <= 1e-5
 
 
-@pytest.mark.parametrize("k,level", [(1, 2), (2, 1)])
+@pytest.mark.parametrize("k,level", [(1, 2), (2, 1), (2, 3), (3, 2)])
 def test_residual(k, level):
     ctx = smg.Context(k, level)
     x, b = rand_vec(k, level, 3), rand_vec(k, level, 4)
