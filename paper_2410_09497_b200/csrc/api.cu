@@ -54,6 +54,7 @@ Dense global1d(const LevelTables& T, int op, bool par_rows, bool par_cols) {
 // Kronecker factors, then the leading block of the inverse of [[A, e],[e^T, 0]] with e the constant
 // pressure vector — equal to A^+ for symmetric A with ker A = span(e).
 void setup_coarse(Context& c) {
+  if (c.coarse_pinv[0]) return;  // built on first use (dense inverse of the level-0 system)
   const LevelTables& T = c.tables[0];
   const LevelLayout lay(c.cfg.degree, 0);
   const int n = lay.n;
@@ -166,6 +167,7 @@ void smooth(Context& c, int level, int prec, void* x, const void* b) {
 
 void vcycle(Context& c, int level, int prec, void* x, const void* b) {
   if (level == 0) {
+    setup_coarse(c);
     launch_coarse_apply(c, prec, x, b);
     return;
   }
@@ -388,7 +390,6 @@ int smg_create(const smg_config* cfg, smg_context** out) {
     SMG_CUDA(cudaMallocHost(&c->dot_host, 64));
     SMG_CUDA(cudaMalloc(&c->tmap_dev, static_cast<size_t>(smg::kTmapSlots) * smg::kTmapSlotBytes));
     c->allocations.push_back(c->tmap_dev);
-    smg::setup_coarse(*c);
     return SMG_OK;
   });
   if (rc != SMG_OK) {
@@ -497,6 +498,7 @@ int smg_coarse_solve(smg_context* h, int precision, void* x, const void* b) {
   return smg::guarded(h, [&] {
     Context& c = smg::ctx_of(h);
     smg::check_prec(precision);
+    smg::setup_coarse(c);
     smg::launch_coarse_apply(c, precision, x, b);
     return SMG_OK;
   });

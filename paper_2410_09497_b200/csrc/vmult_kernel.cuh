@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "smg_internal.cuh"
@@ -137,7 +138,10 @@ template <typename T, int K, int BX, int BY, int BZ>
 struct Brick {
   static constexpr int H = K + 1;
   static constexpr int VEC = 16 / static_cast<int>(sizeof(T));  // elements per 16 B (TMA granule)
+  static constexpr int ALN = 128 / static_cast<int>(sizeof(T));  // elements per 128 B (TMA smem alignment)
+  static constexpr int PADF = ALN;  // front pad of a TMA box buffer: room for the x < 0 halo of clamped boxes
   static constexpr int rup(int v) { return (v + VEC - 1) / VEC * VEC; }
+  static constexpr int rupa(int v) { return (v + ALN - 1) / ALN * ALN; }
   static constexpr int B(int a) { return a == 0 ? BX : (a == 1 ? BY : BZ); }
   static constexpr int N(int a) { return B(a) * H; }
   static constexpr int O1(int c) { return c == 0 ? 1 : 0; }
@@ -148,9 +152,10 @@ struct Brick {
   static constexpr int LO2H(int c) { return N(O2(c)) + 2 * H; }
   // staged input box of component c, TMA box order (x fastest, x pitch UX):
   //   c=0: [z=o2][y=o1][x=c]   c=1: [z=o2][y=c][x=o1]   c=2: [z=c][y=o2][x=o1]
-  // TMA requires the x start of a box to be 16-B aligned and >= 0, so every row is loaded from the
-  // 16-B aligned position at or below the needed start; UX carries VEC-1 elements of slack and the
-  // consumers add the per-brick (per-row for c=0) shift.
+  // TMA (measured on B200, tools/tma_test.cu) needs the x start of a box 16-B aligned and >= 0 and the
+  // shared-memory destination 128-B aligned. Every row is loaded from the 16-B aligned position at or
+  // below the needed start (clamped to 0); UX carries VEC-1 elements of slack and the consumers add
+  // the per-brick shift PADF + x0 - xs (per-row shift for the u_x rows, which are bulk copies).
   static constexpr int XEXT(int c) { return c == 0 ? LC(0) : LO1H(c); }
   static constexpr int UX(int c) { return rup(XEXT(c) + VEC - 1); }
   static constexpr int UY(int c) { return c == 0 ? LO1H(0) : (c == 1 ? LC(1) : LO2H(2)); }
@@ -159,18 +164,25 @@ struct Brick {
   static constexpr int sizeA1(int c) { return N(O2(c)) * LO1H(c) * PC(c); }
   static constexpr int sizeST(int c) { return N(O2(c)) * N(O1(c)) * PC(c); }
   static constexpr int mx3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
-  static constexpr int U = rup(mx3(sizeU(0), sizeU(1), sizeU(2)) + VEC);  // + clamp slack
+  static constexpr int U = rupa(PADF + mx3(sizeU(0), sizeU(1), sizeU(2)) + VEC);  // + clamp slack
   static constexpr int A1 = mx3(sizeA1(0), sizeA1(1), sizeA1(2));
   static constexpr int ST = mx3(sizeST(0), sizeST(1), sizeST(2));
   static constexpr int PXT = rup(N(0) + H + VEC - 1);  // pressure box [-H, N) per axis, x pitch PXT
   static constexpr int PBOX = (N(2) + H) * (N(1) + H) * PXT;
-  static constexpr int PBUF = rup(PBOX + VEC);
+  static constexpr int PBUF = rupa(PADF + PBOX + VEC);
   static constexpr int YX = odd(N(0));
   static constexpr int YP = N(2) * N(1) * YX;
   static constexpr bool ALIAS = 2 * ST <= U;  // S and T overwrite the dead U buffer of the component
   // layout: [U buffer 0][U buffer 1][P box][A1 (also Q2)][B1][Q][YP][S,T if no alias][mbarriers]
-  static constexpr int OFF_U1 = U;
-  static constexpr int OFF_P = 2 * U;
+  // two U buffers (staging of the next component overlaps compute) when they fit in 227 KB, else one
+  static constexpr size_t kSmemCap = 232448;
+  static constexpr size_t bytes_for(int nbuf) {
+    return (static_cast<size_t>(nbuf * U + PBUF + A1 + 2 * ST + YP + (ALIAS ? 0 : 2 * ST)) * sizeof(T) + 15) / 16 *
+               16 + 3 * 8;
+  }
+  static constexpr bool DB = bytes_for(2) <= kSmemCap;
+  static constexpr int OFF_U1 = DB ? U : 0;
+  static constexpr int OFF_P = (DB ? 2 : 1) * U;
   static constexpr int OFF_A1 = OFF_P + PBUF;
   static constexpr int OFF_B1 = OFF_A1 + A1;
   static constexpr int OFF_Q = OFF_B1 + ST;
@@ -178,11 +190,12 @@ struct Brick {
   static constexpr int OFF_ST = OFF_YP + YP;  // only used when !ALIAS
   static constexpr int END = OFF_YP + YP + (ALIAS ? 0 : 2 * ST);
   static constexpr size_t BYTES = (static_cast<size_t>(END) * sizeof(T) + 15) / 16 * 16 + 3 * 8;
+  static_assert(BYTES == bytes_for(DB ? 2 : 1), "smem layout");
   static constexpr int stride(int axis, int a0, int a1) { return axis == 0 ? 1 : (axis == 1 ? a0 : a0 * a1); }
 };
 
 struct Maps {
-  CUtensorMap u0, u1, u2, p;  // rank-1 rows of u_x; 3D boxes of u_y, u_z (constrained planes OOB), p
+  CUtensorMap u0, u1, u2, p;  // u0 unused (u_x rows are bulk copies); 3D boxes of u_y, u_z, p
 };
 
 struct Geo {
@@ -229,14 +242,25 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// non-tensor bulk copy global -> shared (16-B aligned addresses, size multiple of 16 B)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 __device__ __forceinline__ int floor_to(int v, int q) { return (v >= 0 ? v / q : -((-v + q - 1) / q)) * q; }
 
 // smem origin offsets of the staged rows (element of x = g0x - H relative to the row start)
+// smem position of element x0 in a staged 3D box row: PADF + x0 - xs, xs = max(floor16B(x0), 0);
+// negative x0 (boxes clamped at the domain start) lands in the front pad / the previous row's unused tail
 template <typename T>
 __device__ __forceinline__ int brick_shift(const Geo& G, int H) {
   constexpr int VEC = 16 / static_cast<int>(sizeof(T));
+  constexpr int PADF = 128 / static_cast<int>(sizeof(T));
   const int x0 = G.g0[0] - H;
-  return x0 - floor_to(x0, VEC);
+  return PADF + x0 - max(floor_to(x0, VEC), 0);
 }
 // u_x rows: the 1D start (z n + y)(n+1) + x0 has the same residue mod VEC for every z (n % VEC == 0)
 template <typename T>
@@ -259,33 +283,37 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restric
   const int tid = threadIdx.x;
   if constexpr (TMA) {
     if constexpr (C == 0) {
-      // one rank-1 TMA per x-row inside the domain (rows have the odd pitch n+1); warp 0 issues,
-      // rows outside the domain are zero-filled directly
+      // one bulk copy per x-row inside the domain (rows have the odd pitch n+1, so no tensor map);
+      // warp 0 issues, rows outside the domain are zero-filled directly. A row may read past the
+      // end of u_x into u_y (same allocation); those columns are zeroed by fix_columns.
       if (tid < 32) {
         const int y0 = G.g0[1] - H, z0 = G.g0[2] - H;
-        const int ny = max(0, min(n, y0 + UY) - max(0, y0)), nz = max(0, min(n, z0 + UZ) - max(0, z0));
-        if (tid == 0) mbar_expect(bar, static_cast<unsigned>(ny * nz * UX * sizeof(T)));
-        __syncwarp();
+        unsigned bytes = 0;
         for (int r = tid; r < UY * UZ; r += 32) {
           const int y = y0 + r % UY, z = z0 + r / UY;
           T* dst = sU + r * UX;
           if (y >= 0 && y < n && z >= 0 && z < n) {
-            const int start = (z * n + y) * (n + 1) + G.g0[0] - H;
-            const int sal = floor_to(start, BR::VEC), ss = max(sal, 0);
-            tma_load_1d(dst + (ss - sal), &M.u0, ss, bar);
+            const int64_t start = (static_cast<int64_t>(z) * n + y) * (n + 1) + G.g0[0] - H;
+            const int64_t sal = start >= 0 ? start / BR::VEC * BR::VEC : -((-start + BR::VEC - 1) / BR::VEC) * BR::VEC;
+            const int64_t ss = sal > 0 ? sal : 0;
+            const unsigned nb = static_cast<unsigned>((UX - (ss - sal)) * sizeof(T));
+            bulk_load(dst + (ss - sal), x + ss, nb, bar);
+            bytes += nb;
           } else {
 #pragma unroll
             for (int i = 0; i < UX; ++i) dst[i] = T(0);
           }
         }
+        bytes = __reduce_add_sync(0xffffffffu, bytes);
+        if (tid == 0) mbar_expect(bar, bytes);  // arrive + expect_tx after the copies: tx may go negative first
       }
     } else {
       if (tid == 0) {
         mbar_expect(bar, static_cast<unsigned>(BR::sizeU(C) * sizeof(T)));
         // u_y / u_z maps start one row / plane in, so the constrained planes 0 and n fall outside
-        const int xal = floor_to(G.g0[0] - H, BR::VEC), xs = max(xal, 0);
-        if (C == 1) tma_load_3d(sU + (xs - xal), &M.u1, xs, G.g0[1] - H - 1, G.g0[2] - H, bar);
-        else tma_load_3d(sU + (xs - xal), &M.u2, xs, G.g0[1] - H, G.g0[2] - H - 1, bar);
+        const int xs = max(floor_to(G.g0[0] - H, BR::VEC), 0);
+        if (C == 1) tma_load_3d(sU + BR::PADF, &M.u1, xs, G.g0[1] - H - 1, G.g0[2] - H, bar);
+        else tma_load_3d(sU + BR::PADF, &M.u2, xs, G.g0[1] - H, G.g0[2] - H - 1, bar);
       }
     }
   } else {
@@ -312,8 +340,8 @@ __device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const T* __restric
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
       mbar_expect(bar, static_cast<unsigned>(BR::PBOX * sizeof(T)));
-      const int xal = floor_to(G.g0[0] - H, BR::VEC), xs = max(xal, 0);
-      tma_load_3d(sP + (xs - xal), &M.p, xs, G.g0[1] - H, G.g0[2] - H, bar);
+      const int xs = max(floor_to(G.g0[0] - H, BR::VEC), 0);
+      tma_load_3d(sP + BR::PADF, &M.p, xs, G.g0[1] - H, G.g0[2] - H, bar);
     }
   } else {
     constexpr int E0 = BR::N(0) + H, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
@@ -339,7 +367,7 @@ __device__ __forceinline__ void fix_columns(T* sU0, T* sU1, T* sU2, T* sP, const
   using BR = Brick<T, K, BX, BY, BZ>;
   constexpr int H = K + 1;
   const int x0 = G.g0[0] - H;
-  if (x0 >= 0 && x0 + BR::XEXT(0) <= G.n) return;
+  if (x0 > 0 && x0 + BR::XEXT(0) <= G.n) return;
   if (sU0) {
     constexpr int XE = BR::XEXT(0), UY = BR::UY(0), ROWS = BR::UY(0) * BR::UZ(0);
     for (int i = threadIdx.x; i < ROWS * XE; i += NT) {
@@ -557,6 +585,23 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
   __syncthreads();
 }
 
+// write the pressure rows of this brick from the smem accumulator
+template <typename T, int K, int BX, int BY, int BZ, int NT, bool RESID>
+__device__ __forceinline__ void write_pressure(const T* sYP, const Geo& G, T* __restrict__ y, const T* __restrict__ b,
+                                               int64_t offP) {
+  using BR = Brick<T, K, BX, BY, BZ>;
+  constexpr int N0 = BR::N(0), N1 = BR::N(1), N2 = BR::N(2);
+  const int n = G.n;
+  for (int i = threadIdx.x; i < N0 * N1 * N2; i += NT) {
+    const int lx = i % N0, ly = (i / N0) % N1, lz = i / (N0 * N1);
+    const int gx = G.g0[0] + lx, gy = G.g0[1] + ly, gz = G.g0[2] + lz;
+    if (gx >= n || gy >= n || gz >= n) continue;
+    const int64_t gi = offP + (static_cast<int64_t>(gz) * n + gy) * n + gx;
+    const T v = sYP[(lz * N1 + ly) * BR::YX + lx];
+    y[gi] = RESID ? b[gi] - v : v;
+  }
+}
+
 __device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, int bx, int by, int bz, int H) {
   const int ix = brick % nbx, iy = (brick / nbx) % nby, iz = brick / (nbx * nby);
   G.c0[0] = ix * bx;
@@ -604,6 +649,55 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
   if (!TMA) cp_async_commit();
   int u0 = 0;
   unsigned ph[2] = {0, 0}, phP = 0;  // mbarrier phase of buffer 0 / 1 / P
+  if constexpr (!BR::DB) {
+    // single U buffer (large degrees): stage, compute, stage the next component
+    auto wait_u = [&](bool withP) {
+      if (TMA) {
+        if (withP) {
+          mbar_wait(&bars[2], phP);
+          phP ^= 1;
+        }
+        mbar_wait(&bars[0], ph[0]);
+        ph[0] ^= 1;
+      } else {
+        cp_async_commit();
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+    };
+    for (; brick < nbricks; brick += gridDim.x) {
+      const int next = brick + gridDim.x;
+      const bool has_next = next < nbricks;
+      if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H);
+      for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
+      wait_u(true);
+      if (TMA) {
+        fix_columns<T, K, BX, BY, BZ, NT>(sm, nullptr, nullptr, sP, G);
+        __syncthreads();
+      }
+      component<T, K, BX, BY, BZ, NT, 0, RESID, TMA>(sm, sm, G, h, nullptr, x, y, b, maps, &bars[2]);
+      issue_u<T, K, BX, BY, BZ, NT, 1, TMA>(sm, &bars[0], x, maps, G);
+      wait_u(false);
+      if (TMA) {
+        fix_columns<T, K, BX, BY, BZ, NT>(nullptr, sm, nullptr, nullptr, G);
+        __syncthreads();
+      }
+      component<T, K, BX, BY, BZ, NT, 1, RESID, TMA>(sm, sm, G, h, nullptr, x, y, b, maps, &bars[2]);
+      issue_u<T, K, BX, BY, BZ, NT, 2, TMA>(sm, &bars[0], x, maps, G);
+      wait_u(false);
+      if (TMA) {
+        fix_columns<T, K, BX, BY, BZ, NT>(nullptr, nullptr, sm, nullptr, G);
+        __syncthreads();
+      }
+      component<T, K, BX, BY, BZ, NT, 2, RESID, TMA>(sm, sm, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
+                                                     &bars[2]);
+      write_pressure<T, K, BX, BY, BZ, NT, RESID>(sYP, G, y, b, offP);
+      __syncthreads();
+      if (has_next) issue_u<T, K, BX, BY, BZ, NT, 0, TMA>(sm, &bars[0], x, maps, Gn);
+      G = Gn;
+    }
+    if (!TMA) cp_async_wait<0>();
+  } else {
   for (; brick < nbricks; brick += gridDim.x) {
     const int ia = u0, ib = u0 ^ 1;
     T* bufA = sm + (ia ? BR::OFF_U1 : 0);  // components 0 and 2 of this brick
@@ -657,23 +751,13 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
     }
     component<T, K, BX, BY, BZ, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
                                                    &bars[2]);
-    // write the pressure rows of this brick
-    {
-      constexpr int N0 = BR::N(0), N1 = BR::N(1), N2 = BR::N(2);
-      for (int i = threadIdx.x; i < N0 * N1 * N2; i += NT) {
-        const int lx = i % N0, ly = (i / N0) % N1, lz = i / (N0 * N1);
-        const int gx = G.g0[0] + lx, gy = G.g0[1] + ly, gz = G.g0[2] + lz;
-        if (gx >= n || gy >= n || gz >= n) continue;
-        const int64_t gi = offP + (static_cast<int64_t>(gz) * n + gy) * n + gx;
-        const T v = sYP[(lz * N1 + ly) * BR::YX + lx];
-        y[gi] = RESID ? b[gi] - v : v;
-      }
-    }
+    write_pressure<T, K, BX, BY, BZ, NT, RESID>(sYP, G, y, b, offP);
     __syncthreads();  // y_p accumulator is re-zeroed by the next brick
     G = Gn;
     u0 ^= 1;
   }
   if (!TMA) cp_async_wait<0>();
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -726,12 +810,7 @@ Maps make_maps(const T* x, int n) {
   const uint64_t es = sizeof(T);
   const uint64_t nn = static_cast<uint64_t>(n);
   const uint64_t sizeV = (nn + 1) * nn * nn;
-  {  // u_x as one long row
-    const uint64_t d[1] = {sizeV};
-    const uint64_t s[1] = {sizeV * es};  // unused for rank 1
-    const uint32_t box[1] = {static_cast<uint32_t>(BR::UX(0))};
-    encode<T>(&M.u0, x, 1, d, s, box);
-  }
+  // u_x rows have the odd pitch n+1 (not a legal TMA stride): staged by non-tensor bulk copies
   {  // u_y: dims (x n, y n+1, z n); base one row in -> y' = y - 1 in [0, n-1)
     const uint64_t d[3] = {nn, nn - 1, nn};
     const uint64_t s[2] = {nn * es, nn * (nn + 1) * es};
@@ -767,7 +846,8 @@ void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
   if (num_sms == 0) SMG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ctx.device));
   const dim3 grid(std::min(nbricks, num_sms));
   const size_t smem = BR::BYTES;
-  const bool tma = tma_ok<T, K, BX, BY, BZ>(n) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  static const bool no_tma = std::getenv("SMG_NO_TMA") != nullptr;  // diagnostics: force the cp.async path
+  const bool tma = !no_tma && tma_ok<T, K, BX, BY, BZ>(n) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
   const Maps* dmaps = nullptr;
   if (tma) {
     // tensor maps are cached per (input vector, level, precision) in 64-B aligned global slots,
@@ -807,20 +887,26 @@ void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
 }  // namespace
 
 // Brick shape (cells) per degree: fp64 SMEM ~80-200 KB, one persistent CTA per SM.
-template <int K> struct BrickShape;
-template <> struct BrickShape<1> { static constexpr int X = 8, Y = 4, Z = 4; };
-template <> struct BrickShape<2> { static constexpr int X = 4, Y = 4, Z = 4; };
-template <> struct BrickShape<3> { static constexpr int X = 4, Y = 2, Z = 2; };
-template <> struct BrickShape<4> { static constexpr int X = 2, Y = 2, Z = 2; };
-template <> struct BrickShape<5> { static constexpr int X = 2, Y = 2, Z = 1; };
-template <> struct BrickShape<6> { static constexpr int X = 2, Y = 1, Z = 1; };
-template <> struct BrickShape<7> { static constexpr int X = 2, Y = 1, Z = 1; };
+template <typename T, int K> struct BrickShape;
+template <typename T> struct BrickShape<T, 1> { static constexpr int X = 8, Y = 4, Z = 4; };
+template <typename T> struct BrickShape<T, 2> { static constexpr int X = 4, Y = 4, Z = 4; };
+template <typename T> struct BrickShape<T, 3> { static constexpr int X = 4, Y = 2, Z = 2; };
+template <typename T> struct BrickShape<T, 4> { static constexpr int X = 2, Y = 2, Z = 2; };
+template <> struct BrickShape<double, 5> { static constexpr int X = 2, Y = 1, Z = 1; };
+template <> struct BrickShape<float, 5> { static constexpr int X = 2, Y = 2, Z = 1; };
+template <> struct BrickShape<double, 6> { static constexpr int X = 1, Y = 1, Z = 1; };
+template <> struct BrickShape<float, 6> { static constexpr int X = 2, Y = 1, Z = 1; };
+template <> struct BrickShape<double, 7> { static constexpr int X = 1, Y = 1, Z = 1; };  // single U buffer
+template <> struct BrickShape<float, 7> { static constexpr int X = 2, Y = 1, Z = 1; };
 
 template <int K>
 void vmult_launch_k(Context& ctx, int level, int prec, void* y, const void* x, const void* b) {
-  using S = BrickShape<K>;
-  if (prec == SMG_F64) launch_t<double, K, S::X, S::Y, S::Z, 256>(ctx, level, y, x, b);
-  else launch_t<float, K, S::X, S::Y, S::Z, 256>(ctx, level, y, x, b);
+  using SD = BrickShape<double, K>;
+  using SF = BrickShape<float, K>;
+  static_assert(Brick<double, K, SD::X, SD::Y, SD::Z>::BYTES <= 232448, "fp64 brick exceeds 227 KB");
+  static_assert(Brick<float, K, SF::X, SF::Y, SF::Z>::BYTES <= 232448, "fp32 brick exceeds 227 KB");
+  if (prec == SMG_F64) launch_t<double, K, SD::X, SD::Y, SD::Z, 256>(ctx, level, y, x, b);
+  else launch_t<float, K, SF::X, SF::Y, SF::Z, 256>(ctx, level, y, x, b);
 }
 
 template <int K>
