@@ -302,7 +302,7 @@ def main():
                    "l2": "inputs larger than L2 (x, y 227 MB each vs 126 MB L2); no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_per_launch, "kernel": "stokes_vmult_kernel<double,2,4,4,4>"},
+                     "algorithmic_bytes_per_launch": bytes_per_launch, "kernel": "stokes_vmult_kernel<double,2,4,4,2,OCC=2,NT=384>"},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
         "fp32_vmult": {"value": N * world / (ms32 * 1e-3), "unit": "DoF/s", "ms": ms32},
         "smoother_fp32": {"value": N * world / (ms_smooth * 1e-3), "unit": "DoF/s", "ms_per_step": ms_smooth,

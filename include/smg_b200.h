@@ -95,7 +95,15 @@ int smg_dot(smg_context* ctx, int level, int precision, const void* a, const voi
 int smg_axpy(smg_context* ctx, int level, int precision, double alpha, const void* x, void* y);
 int smg_convert(smg_context* ctx, int level, int dst_precision, void* dst, int src_precision, const void* src);
 
-/* ---- host-buffer entry points in the BlockVector layout (reference-facing e2e path) ---- */
+/* ---- host BlockVector <-> device level vector (BlockVector<dim,T> block_vector.hpp:15-18 with the
+ *      DoFLayout of SPEC.md:173-176: velocity component blocks lexicographic x-fastest including the
+ *      constrained boundary-normal DoFs; pressure CELL-LOCAL lexicographic, i.e. cells x-fastest and
+ *      (k+1)^3 nodes per cell x-fastest). Host arrays are caller-owned; synchronous. ---- */
+int smg_vec_upload(smg_context* ctx, int level, int precision, void* dst, const void* const vel[3], const void* p);
+int smg_vec_download(smg_context* ctx, int level, int precision, void* const vel[3], void* p, const void* src);
+
+/* ---- host-buffer operator apply in the BlockVector layout (the reference-facing vmult: what
+ *      StokesOperator::vmult(BlockVector&, const BlockVector&) becomes; copies included) ---- */
 int smg_vmult_host(smg_context* ctx, int level, int precision, void* const y_vel[3], void* y_p,
                    const void* const x_vel[3], const void* x_p);
 

@@ -24,7 +24,7 @@ EXPORTED = [
     "smg_config_default", "smg_create", "smg_destroy", "smg_set_stream", "smg_last_error", "smg_launch_count",
     "smg_level_sizes", "smg_vec_alloc", "smg_vec_free", "smg_vmult", "smg_residual", "smg_smooth",
     "smg_prolongate_add", "smg_restrict", "smg_coarse_solve", "smg_vcycle", "smg_solve", "smg_dot", "smg_axpy",
-    "smg_convert", "smg_vmult_host",
+    "smg_convert", "smg_vmult_host", "smg_vec_upload", "smg_vec_download",
 ]
 
 
@@ -79,6 +79,8 @@ def lib():
         L.smg_axpy.argtypes = [P, I, I, D, P, P]
         L.smg_convert.argtypes = [P, I, I, P, I, P]
         L.smg_vmult_host.argtypes = [P, I, I, P, P, P, P]
+        L.smg_vec_upload.argtypes = [P, I, I, P, P, P]
+        L.smg_vec_download.argtypes = [P, I, I, P, P, P]
         _LIB = L
     return _LIB
 
@@ -250,8 +252,9 @@ class Context:
         return out.value
 
     def vmult_host(self, level, x_blocks, precision=F64, out=None):
-        """Reference-facing path: host arrays in the BlockVector layout (3 velocity + pressure) in,
-        host arrays out; host<->device copies included (block_vector.hpp:17-18)."""
+        """Reference-facing path: host arrays in the BlockVector layout (3 velocity blocks + the pressure
+        block in cell-local order; see to_blockvector) in, host arrays out; host<->device
+        copies included (block_vector.hpp:17-18)."""
         dt = np.float64 if precision == F64 else np.float32
         s = self.sizes(level)
         xs = [np.ascontiguousarray(a, dtype=dt) for a in x_blocks]
@@ -268,6 +271,61 @@ class Context:
         self._check(lib().smg_vmult_host(self._h, level, precision, yv, ctypes.c_void_p(ys[3].ctypes.data), xv,
                                          ctypes.c_void_p(xs[3].ctypes.data)))
         return ys
+
+
+    def upload(self, level, blocks, out=None, dtype=None):
+        """BlockVector host blocks (pressure cell-local) -> device level vector (stored layout)."""
+        torch = self._torch
+        dtype = dtype or (torch.float64 if np.asarray(blocks[0]).dtype == np.float64 else torch.float32)
+        prec = F64 if dtype == torch.float64 else F32
+        dt = np.float64 if prec == F64 else np.float32
+        s = self.sizes(level)
+        xs = [np.ascontiguousarray(a, dtype=dt) for a in blocks]
+        if any(xs[i].size != s[i] for i in range(4)):
+            raise ValueError("block sizes do not match the level layout")
+        v = out if out is not None else self.new_vector(level, dtype)
+        vel = (ctypes.c_void_p * 3)(*[a.ctypes.data for a in xs[:3]])
+        self._sync_stream()
+        self._check(lib().smg_vec_upload(self._h, level, prec, _ptr(v), vel, ctypes.c_void_p(xs[3].ctypes.data)))
+        return v
+
+    def download(self, level, v):
+        """device level vector -> BlockVector host blocks (pressure cell-local)."""
+        prec = self._prec(v)
+        dt = np.float64 if prec == F64 else np.float32
+        s = self.sizes(level)
+        ys = [np.empty(s[i], dtype=dt) for i in range(4)]
+        vel = (ctypes.c_void_p * 3)(*[a.ctypes.data for a in ys[:3]])
+        self._sync_stream()
+        self._check(lib().smg_vec_download(self._h, level, prec, vel, ctypes.c_void_p(ys[3].ctypes.data), _ptr(v)))
+        return ys
+
+
+def pressure_cell_local_index(degree, level):
+    """perm such that p_cell_local = p_global_lex[perm] (SPEC.md:174 cell-local pressure numbering)."""
+    H = degree + 1
+    m = 2 << level
+    n = m * H
+    c = np.arange(m)
+    a = np.arange(H)
+    # cell-local index order: cz, cy, cx, az, ay, ax (slowest to fastest)
+    gz = (c[:, None, None, None, None, None] * H + a[None, None, None, :, None, None])
+    gy = (c[None, :, None, None, None, None] * H + a[None, None, None, None, :, None])
+    gx = (c[None, None, :, None, None, None] * H + a[None, None, None, None, None, :])
+    return ((gz * n + gy) * n + gx).reshape(-1)
+
+
+def to_blockvector(v, degree, level):
+    """stored level vector (numpy) -> BlockVector blocks [u_x, u_y, u_z, p_cell_local]."""
+    b = split_blocks(np.asarray(v), degree, level)
+    return [b[0].copy(), b[1].copy(), b[2].copy(), b[3][pressure_cell_local_index(degree, level)]]
+
+
+def from_blockvector(blocks, degree, level):
+    """BlockVector blocks (pressure cell-local) -> stored level vector (numpy)."""
+    p = np.empty_like(np.asarray(blocks[3]))
+    p[pressure_cell_local_index(degree, level)] = blocks[3]
+    return np.concatenate([np.asarray(blocks[0]), np.asarray(blocks[1]), np.asarray(blocks[2]), p])
 
 
 def split_blocks(v, degree, level):

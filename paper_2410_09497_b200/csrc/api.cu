@@ -279,6 +279,35 @@ int fgmres(Context& c, int level, double* x, const double* b, double tol, int ma
   return converged ? SMG_OK : SMG_ENOTCONV;
 }
 
+// BlockVector (host, reference DoFLayout: pressure cell-local) <-> device level vector
+// (stored layout, pressure global lexicographic). Velocity blocks are copied as they are; the
+// pressure goes through a staging buffer and the permutation kernel. Stream-ordered, asynchronous
+// with respect to the host for pinned buffers.
+char* pressure_stage(Context& c, int prec) {
+  if (!c.pstage[prec]) c.pstage[prec] = alloc_vec(c, c.cfg.max_level, prec);
+  return static_cast<char*>(c.pstage[prec]);
+}
+
+void upload_blocks(Context& c, int level, int prec, char* dst, const void* const vel[3], const void* p) {
+  const LevelLayout& lay = c.dev[0][level].lay;
+  const size_t es = elem_size(prec);
+  for (int b = 0; b < 3; ++b)
+    SMG_CUDA(cudaMemcpyAsync(dst + lay.off[b] * es, vel[b], lay.size[b] * es, cudaMemcpyHostToDevice, c.stream));
+  char* st = pressure_stage(c, prec);
+  SMG_CUDA(cudaMemcpyAsync(st, p, lay.size[3] * es, cudaMemcpyHostToDevice, c.stream));
+  launch_pressure_permute(c, level, prec, dst + lay.off[3] * es, st, false);
+}
+
+void download_blocks(Context& c, int level, int prec, void* const vel[3], void* p, const char* src) {
+  const LevelLayout& lay = c.dev[0][level].lay;
+  const size_t es = elem_size(prec);
+  for (int b = 0; b < 3; ++b)
+    SMG_CUDA(cudaMemcpyAsync(vel[b], src + lay.off[b] * es, lay.size[b] * es, cudaMemcpyDeviceToHost, c.stream));
+  char* st = pressure_stage(c, prec);
+  launch_pressure_permute(c, level, prec, st, src + lay.off[3] * es, true);
+  SMG_CUDA(cudaMemcpyAsync(p, st, lay.size[3] * es, cudaMemcpyDeviceToHost, c.stream));
+}
+
 template <class F>
 int guarded(smg_context* h, F&& f) {
   Context* c = reinterpret_cast<Context*>(h);
@@ -558,25 +587,44 @@ int smg_convert(smg_context* h, int level, int dp, void* dst, int sp, const void
   });
 }
 
+int smg_vec_upload(smg_context* h, int level, int precision, void* dst, const void* const vel[3], const void* p) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!dst || !vel || !vel[0] || !vel[1] || !vel[2] || !p) throw std::invalid_argument("vec_upload: null pointer");
+    smg::upload_blocks(c, level, precision, static_cast<char*>(dst), vel, p);
+    SMG_CUDA(cudaStreamSynchronize(c.stream));
+    return SMG_OK;
+  });
+}
+
+int smg_vec_download(smg_context* h, int level, int precision, void* const vel[3], void* p, const void* src) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!src || !vel || !vel[0] || !vel[1] || !vel[2] || !p) throw std::invalid_argument("vec_download: null pointer");
+    smg::download_blocks(c, level, precision, vel, p, static_cast<const char*>(src));
+    SMG_CUDA(cudaStreamSynchronize(c.stream));
+    return SMG_OK;
+  });
+}
+
 int smg_vmult_host(smg_context* h, int level, int precision, void* const y_vel[3], void* y_p,
                    const void* const x_vel[3], const void* x_p) {
   return smg::guarded(h, [&] {
     Context& c = smg::ctx_of(h);
     smg::check_level(c, level);
     smg::check_prec(precision);
-    const smg::LevelLayout& lay = c.dev[0][level].lay;
-    const size_t es = smg::elem_size(precision);
-    // device staging buffers: reuse the level's work vectors of this precision
+    if (!x_vel || !y_vel || !x_p || !y_p) throw std::invalid_argument("vmult_host: null pointer");
+    // device staging buffers: the level's work vectors of this precision
     smg::ensure_work(c, precision);
     char* dx = static_cast<char*>(c.work_x[precision][level]);
     char* dy = static_cast<char*>(c.work_b[precision][level]);
-    for (int b = 0; b < 3; ++b)
-      SMG_CUDA(cudaMemcpyAsync(dx + lay.off[b] * es, x_vel[b], lay.size[b] * es, cudaMemcpyHostToDevice, c.stream));
-    SMG_CUDA(cudaMemcpyAsync(dx + lay.off[3] * es, x_p, lay.size[3] * es, cudaMemcpyHostToDevice, c.stream));
+    smg::upload_blocks(c, level, precision, dx, x_vel, x_p);
     smg::launch_vmult(c, level, precision, dy, dx, nullptr);
-    for (int b = 0; b < 3; ++b)
-      SMG_CUDA(cudaMemcpyAsync(y_vel[b], dy + lay.off[b] * es, lay.size[b] * es, cudaMemcpyDeviceToHost, c.stream));
-    SMG_CUDA(cudaMemcpyAsync(y_p, dy + lay.off[3] * es, lay.size[3] * es, cudaMemcpyDeviceToHost, c.stream));
+    smg::download_blocks(c, level, precision, y_vel, y_p, dy);
     SMG_CUDA(cudaStreamSynchronize(c.stream));
     return SMG_OK;
   });

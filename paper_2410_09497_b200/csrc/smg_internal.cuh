@@ -91,6 +91,7 @@ struct Context {
   std::vector<void*> allocations;
   // per-level work vectors for the smoother / V-cycle (allocated lazily): [prec][level]
   std::vector<void*> work_r[2], work_x[2], work_b[2];
+  void* pstage[2] = {nullptr, nullptr};  // pressure staging for the BlockVector host path (finest level size)
   // TMA descriptors of input vectors (vmult.cu)
   void* tmap_dev = nullptr;
   std::map<TmapKey, int> tmap_slots;
@@ -119,5 +120,7 @@ void launch_convert(Context& c, int64_t n, int dst_prec, void* dst, int src_prec
 void launch_zero(Context& c, int64_t n, int prec, void* x);
 void launch_scale(Context& c, int64_t n, int prec, double alpha, void* x);
 void launch_sub_pressure_mean(Context& c, int level, int prec, void* x);  // mass-weighted mean removal
+// pressure block global lexicographic <-> cell-local (BlockVector / DoFLayout order)
+void launch_pressure_permute(Context& c, int level, int prec, void* dst, const void* src, bool to_cell_local);
 
 }  // namespace smg

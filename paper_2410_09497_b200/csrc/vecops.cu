@@ -100,6 +100,23 @@ __global__ void sub_scalar_kernel(int64_t n, T* __restrict__ p, const double* __
     p[i] -= mean;
 }
 
+// pressure block: global lexicographic (device layout) <-> cell-local lexicographic (the reference's
+// DoFLayout: cells x-fastest, (k+1)^3 nodes per cell x-fastest). One thread per DoF,
+// indexed by the global lexicographic position (coalesced on that side).
+template <typename T, bool TO_CELL>
+__global__ void pressure_permute_kernel(T* __restrict__ dst, const T* __restrict__ src, int m, int H) {
+  const int n = m * H;
+  const int64_t total = static_cast<int64_t>(n) * n * n;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int gx = static_cast<int>(i % n), gy = static_cast<int>((i / n) % n), gz = static_cast<int>(i / (int64_t(n) * n));
+    const int64_t cell = (static_cast<int64_t>(gz / H) * m + gy / H) * m + gx / H;
+    const int64_t c = cell * H * H * H + ((gz % H) * H + gy % H) * H + gx % H;
+    if (TO_CELL) dst[c] = src[i];
+    else dst[i] = src[c];
+  }
+}
+
 int grid_for(int64_t n) {
   const int64_t g = (n + kThreads - 1) / kThreads;
   return static_cast<int>(g < kDotBlocks ? (g < 1 ? 1 : g) : kDotBlocks);
@@ -176,6 +193,28 @@ void launch_convert(Context& c, int64_t n, int dst_prec, void* dst, int src_prec
   else
     convert_kernel<double, float><<<g, kThreads, 0, c.stream>>>(n, static_cast<double*>(dst),
                                                                  static_cast<const float*>(src));
+  ++c.launches;
+  SMG_CUDA(cudaGetLastError());
+}
+
+void launch_pressure_permute(Context& c, int level, int prec, void* dst, const void* src, bool to_cell_local) {
+  const LevelLayout& lay = c.dev[0][level].lay;
+  const int g = grid_for(lay.size[3]), H = c.cfg.degree + 1;
+  if (prec == SMG_F64) {
+    if (to_cell_local)
+      pressure_permute_kernel<double, true><<<g, kThreads, 0, c.stream>>>(static_cast<double*>(dst),
+                                                                          static_cast<const double*>(src), lay.m, H);
+    else
+      pressure_permute_kernel<double, false><<<g, kThreads, 0, c.stream>>>(static_cast<double*>(dst),
+                                                                           static_cast<const double*>(src), lay.m, H);
+  } else {
+    if (to_cell_local)
+      pressure_permute_kernel<float, true><<<g, kThreads, 0, c.stream>>>(static_cast<float*>(dst),
+                                                                         static_cast<const float*>(src), lay.m, H);
+    else
+      pressure_permute_kernel<float, false><<<g, kThreads, 0, c.stream>>>(static_cast<float*>(dst),
+                                                                          static_cast<const float*>(src), lay.m, H);
+  }
   ++c.launches;
   SMG_CUDA(cudaGetLastError());
 }

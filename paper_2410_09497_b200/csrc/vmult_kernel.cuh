@@ -80,61 +80,10 @@ __device__ __forceinline__ void cp_async_wait() {
 // ---------------------------------------------------------------------------------------------
 // register-pencil banded operators
 // ---------------------------------------------------------------------------------------------
-// DG mass (block diagonal): out[e*H+a] = sum_b MO[a][b] in[(e+OFF)*H+b]
-template <typename T, int K, int NC, int OFF, int LIN>
-__device__ __forceinline__ void dg_mass(const T (&in)[LIN], T (&out)[NC * (K + 1)]) {
-  constexpr int H = K + 1;
-#pragma unroll
-  for (int e = 0; e < NC; ++e)
-#pragma unroll
-    for (int a = 0; a < H; ++a) {
-      T s = T(0);
-#pragma unroll
-      for (int b = 0; b < H; ++b) s += cref<T>(Ref<K>::MO + a * H + b) * in[(e + OFF) * H + b];
-      out[e * H + a] = s;
-    }
-}
-
-// DG SIPG Laplacian (block tridiagonal; the off-diagonal blocks are "cross shaped" for the
-// Gauss-Lobatto nodal basis: LOM[a][b] != 0 only if a == 0 or b == K, LOP[a][b] only if a == K or
-// b == 0). in holds one halo cell on each side: cell e is in[(e+1)*H ...]. Output cells whose
-// global index is 0 / m-1 get the Nitsche correction (efirst / elast local cell, -1 if none).
-template <typename T, int K, int NC, bool BND>
-__device__ __forceinline__ void dg_sipg(const T (&in)[(NC + 2) * (K + 1)], T (&out)[NC * (K + 1)], int efirst,
-                                        int elast) {
-  constexpr int H = K + 1;
-  using R = Ref<K>;
-#pragma unroll
-  for (int e = 0; e < NC; ++e)
-#pragma unroll
-    for (int a = 0; a < H; ++a) {
-      T s = T(0);
-#pragma unroll
-      for (int b = 0; b < H; ++b) s += cref<T>(R::LO0 + a * H + b) * in[(e + 1) * H + b];
-#pragma unroll
-      for (int b = 0; b < H; ++b)
-        if (a == 0 || b == K) s += cref<T>(R::LOM + a * H + b) * in[e * H + b];
-#pragma unroll
-      for (int b = 0; b < H; ++b)
-        if (a == K || b == 0) s += cref<T>(R::LOP + a * H + b) * in[(e + 2) * H + b];
-      if (BND) {
-        if (e == efirst) {
-#pragma unroll
-          for (int b = 0; b < H; ++b) s += cref<T>(R::DLF + a * H + b) * in[(e + 1) * H + b];
-        }
-        if (e == elast) {
-#pragma unroll
-          for (int b = 0; b < H; ++b) s += cref<T>(R::DLL + a * H + b) * in[(e + 1) * H + b];
-        }
-      }
-      out[e * H + a] = s;
-    }
-}
-
 // ---------------------------------------------------------------------------------------------
 // brick geometry
 // ---------------------------------------------------------------------------------------------
-template <typename T, int K, int BX, int BY, int BZ>
+template <typename T, int K, int BX, int BY, int BZ, int OCC>
 struct Brick {
   static constexpr int H = K + 1;
   static constexpr int VEC = 16 / static_cast<int>(sizeof(T));  // elements per 16 B (TMA granule)
@@ -174,8 +123,9 @@ struct Brick {
   static constexpr int YP = N(2) * N(1) * YX;
   static constexpr bool ALIAS = 2 * ST <= U;  // S and T overwrite the dead U buffer of the component
   // layout: [U buffer 0][U buffer 1][P box][A1 (also Q2)][B1][Q][YP][S,T if no alias][mbarriers]
-  // two U buffers (staging of the next component overlaps compute) when they fit in 227 KB, else one
-  static constexpr size_t kSmemCap = 232448;
+  // two U buffers (staging of the next component overlaps compute) when they fit in the per-CTA share
+  // of the 228 KB SM (OCC resident CTAs, 1 KB reserved per CTA), else one
+  static constexpr size_t kSmemCap = OCC == 1 ? 232448 : 233472 / OCC - 1024;
   static constexpr size_t bytes_for(int nbuf) {
     return (static_cast<size_t>(nbuf * U + PBUF + A1 + 2 * ST + YP + (ALIAS ? 0 : 2 * ST)) * sizeof(T) + 15) / 16 *
                16 + 3 * 8;
@@ -274,9 +224,9 @@ __device__ __forceinline__ int row_shift0(const Geo& G, int H, int y) {
 // staging: TMA (default) or cp.async element copies (fallback when a pitch is not 16-B aligned,
 // i.e. fp32 on level 0 with even k). Both write the same TMA box layout.
 // ---------------------------------------------------------------------------------------------
-template <typename T, int K, int BX, int BY, int BZ, int NT, int C, bool TMA>
+template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, int C, bool TMA>
 __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restrict__ x, const Maps& M, const Geo& G) {
-  using BR = Brick<T, K, BX, BY, BZ>;
+  using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   constexpr int UX = BR::UX(C), UY = BR::UY(C), UZ = BR::UZ(C);
   const int n = G.n;
@@ -333,9 +283,9 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restric
   }
 }
 
-template <typename T, int K, int BX, int BY, int BZ, int NT, bool TMA>
+template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, bool TMA>
 __device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const T* __restrict__ x, const Maps& M, const Geo& G) {
-  using BR = Brick<T, K, BX, BY, BZ>;
+  using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
@@ -362,9 +312,9 @@ __device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const T* __restric
 //  - u_x rows are rank-1 copies that ignore the row structure: zero the columns outside [1, n-1]
 //    (halo beyond the domain and the constrained boundary-normal nodes x = 0, x = n);
 //  - u_y, u_z, p boxes clamped at x = 0 leave the x < 0 halo columns unwritten: zero them.
-template <typename T, int K, int BX, int BY, int BZ, int NT>
+template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT>
 __device__ __forceinline__ void fix_columns(T* sU0, T* sU1, T* sU2, T* sP, const Geo& G) {
-  using BR = Brick<T, K, BX, BY, BZ>;
+  using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   const int x0 = G.g0[0] - H;
   if (x0 > 0 && x0 + BR::XEXT(0) <= G.n) return;
@@ -386,14 +336,64 @@ __device__ __forceinline__ void fix_columns(T* sU0, T* sU1, T* sU2, T* sP, const
 }
 
 // ---------------------------------------------------------------------------------------------
-// one velocity component (U already staged in sU); if C == 2 and Gn != nullptr, the next brick's
-// pressure box is issued as soon as this brick's P box is dead.
+// per-cell 1D kernels on register arrays (one work item = one cell of one 1D line)
 // ---------------------------------------------------------------------------------------------
-template <typename T, int K, int BX, int BY, int BZ, int NT, int C, bool RESID, bool TMA>
+// DG mass, one cell block: out[a] = sum_b MO[a][b] cu[b]
+template <typename T, int K>
+__device__ __forceinline__ void cell_mass(const T (&cu)[K + 1], T (&out)[K + 1]) {
+  constexpr int H = K + 1;
+#pragma unroll
+  for (int a = 0; a < H; ++a) {
+    T s = T(0);
+#pragma unroll
+    for (int b = 0; b < H; ++b) s += cref<T>(Ref<K>::MO + a * H + b) * cu[b];
+    out[a] = s;
+  }
+}
+// DG SIPG rows of one cell from its (previous, current, next) cell values. The off-diagonal blocks
+// are cross shaped for the Gauss-Lobatto basis (LOM[a][b] != 0 only if a == 0 or b == K, LOP only
+// if a == K or b == 0). first / last: the cell is the first / last of the global line (Nitsche end
+// rows DLF / DLL); neighbours outside the domain arrive zero-filled.
+template <typename T, int K>
+__device__ __forceinline__ void cell_sipg(const T (&pv)[K + 1], const T (&cu)[K + 1], const T (&nx)[K + 1], bool first,
+                                          bool last, T (&out)[K + 1]) {
+  constexpr int H = K + 1;
+  using R = Ref<K>;
+#pragma unroll
+  for (int a = 0; a < H; ++a) {
+    T s = T(0);
+#pragma unroll
+    for (int b = 0; b < H; ++b) s += cref<T>(R::LO0 + a * H + b) * cu[b];
+#pragma unroll
+    for (int b = 0; b < H; ++b)
+      if (a == 0 || b == K) s += cref<T>(R::LOM + a * H + b) * pv[b];
+#pragma unroll
+    for (int b = 0; b < H; ++b)
+      if (a == K || b == 0) s += cref<T>(R::LOP + a * H + b) * nx[b];
+    if (first) {
+#pragma unroll
+      for (int b = 0; b < H; ++b) s += cref<T>(R::DLF + a * H + b) * cu[b];
+    }
+    if (last) {
+#pragma unroll
+      for (int b = 0; b < H; ++b) s += cref<T>(R::DLL + a * H + b) * cu[b];
+    }
+    out[a] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// one velocity component (U already staged in sU); if C == 2 and Gn != nullptr, the next brick's
+// pressure box is issued as soon as this brick's P box is dead. Every pass is a loop over
+// (cell, line) work items -- NT threads get several times more items than there are 1D lines, so
+// the passes stay balanced and the dependency chains short (v5; v2-v4 used one thread per line).
+// ---------------------------------------------------------------------------------------------
+template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, int C, bool RESID, bool TMA>
 __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const Geo* Gn, const T* __restrict__ x,
                                           T* __restrict__ y, const T* __restrict__ b, const Maps& M, uint64_t* barP) {
-  using BR = Brick<T, K, BX, BY, BZ>;
-  constexpr int H = K + 1;
+  using BR = Brick<T, K, BX, BY, BZ, OCC>;
+  using R = Ref<K>;
+  constexpr int H = K + 1, P = K + 2;
   constexpr int O1 = BR::O1(C), O2 = BR::O2(C);
   constexpr int NCc = BR::B(C), NO1 = BR::B(O1), NO2 = BR::B(O2);
   constexpr int Nc = BR::N(C), No1 = BR::N(O1), No2 = BR::N(O2);
@@ -414,170 +414,205 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
   T* sS = BR::ALIAS ? sU : sm + BR::OFF_ST;
   T* sT = sS + BR::ST;
 
-  // ---- Q2 = M_o2 p over c in [-H, N_c), o1 owned, o2 owned  (pencils along o2, from the P box) ----
+  // ---- Q2 = M_o2 p over c in [-H, N_c), o1 owned, o2 owned (from the P box) ----
   {
     T* sQ2 = sA1;
     constexpr int E1P = BR::N(1) + H;
     constexpr int PSC = BR::stride(C, BR::PXT, E1P), PSO1 = BR::stride(O1, BR::PXT, E1P),
                   PSO2 = BR::stride(O2, BR::PXT, E1P);
-    constexpr int NPEN = (Nc + H) * No1;
-    for (int p = tid; p < NPEN; p += NT) {
-      // consecutive threads walk the P-box x axis (c for C=0, o1 otherwise): conflict-free
-      const int ci = C == 0 ? p % (Nc + H) : p / No1;
-      const int oi = C == 0 ? p / (Nc + H) : p % No1;
-      const T* src = sP + brick_shift<T>(G, H) + ci * PSC + (oi + H) * PSO1 + H * PSO2;
-      T in[No2];
+    constexpr int NL = (Nc + H) * No1;
+    const int psh = brick_shift<T>(G, H);
+    for (int it = tid; it < NL * NO2; it += NT) {
+      const int e2 = it / NL, r = it - e2 * NL;
+      // consecutive items walk the P-box x axis (c for C=0, o1 otherwise): conflict-free
+      const int ci = C == 0 ? r % (Nc + H) : r / No1;
+      const int oi = C == 0 ? r / (Nc + H) : r % No1;
+      const T* src = sP + psh + ci * PSC + (oi + H) * PSO1 + (e2 + 1) * H * PSO2;
+      T cu[H], out[H];
 #pragma unroll
-      for (int j = 0; j < No2; ++j) in[j] = src[j * PSO2];
-      T out[No2];
-      dg_mass<T, K, NO2, 0>(in, out);
+      for (int j = 0; j < H; ++j) cu[j] = src[j * PSO2];
+      cell_mass<T, K>(cu, out);
 #pragma unroll
-      for (int j = 0; j < No2; ++j) sQ2[(j * No1 + oi) * PC + ci] = out[j];
+      for (int a = 0; a < H; ++a) sQ2[((e2 * H + a) * No1 + oi) * PC + ci] = out[a];
     }
     fence_proxy_async();
     __syncthreads();
-    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, NT, TMA>(sP, barP, x, M, *Gn);
+    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, barP, x, M, *Gn);
     if (!TMA && C == 2) cp_async_commit();
-    // Q = M_o1 Q2 (pencils along o1)
-    constexpr int NPEN2 = (Nc + H) * No2;
-    for (int p = tid; p < NPEN2; p += NT) {
-      const int ci = p % (Nc + H), oj = p / (Nc + H);
-      T in[No1];
+    // Q = M_o1 Q2
+    constexpr int NL2 = (Nc + H) * No2;
+    for (int it = tid; it < NL2 * NO1; it += NT) {
+      const int e1 = it / NL2, r = it - e1 * NL2;
+      const int ci = r % (Nc + H), oj = r / (Nc + H);
+      T cu[H], out[H];
 #pragma unroll
-      for (int j = 0; j < No1; ++j) in[j] = sQ2[(oj * No1 + j) * PC + ci];
-      T out[No1];
-      dg_mass<T, K, NO1, 0>(in, out);
+      for (int j = 0; j < H; ++j) cu[j] = sQ2[(oj * No1 + e1 * H + j) * PC + ci];
+      cell_mass<T, K>(cu, out);
 #pragma unroll
-      for (int j = 0; j < No1; ++j) sQ[(oj * No1 + j) * PC + ci] = out[j];
+      for (int a = 0; a < H; ++a) sQ[(oj * No1 + e1 * H + a) * PC + ci] = out[a];
     }
     __syncthreads();
   }
-  // ---- pass 1 (along o2): A1 = M_o2 U  (c full, o1 with halo, o2 owned);  B1 = L_o2 U (o1 owned) ----
+  // ---- pass 1 (along o2): A1 = M_o2 U (c full, o1 with halo, o2 owned); B1 = L_o2 U (o1 owned) ----
   {
+    constexpr int US = C == 2 ? UX : UX * UY;  // staged-box stride along o2
+    const int bsh = brick_shift<T>(G, H);
+    // element (c = ci, o1 = oi, o2 = 0) of the staged box
+    auto ub = [&](int ci, int oi) {
+      return C == 0 ? oi * UX + ci + row_shift0<T>(G, H, G.g0[1] - H + oi)
+                    : (C == 1 ? ci * UX + oi : ci * UY * UX + oi) + bsh;
+    };
+    constexpr int NLA = LC * LO1H;
+    for (int it = tid; it < NLA * NO2; it += NT) {
+      const int e2 = it / NLA, r = it - e2 * NLA;
+      // consecutive items walk the staged box's x axis: c for C=0, o1 for C=1,2
+      const int ci = C == 0 ? r % LC : r / LO1H;
+      const int oi = C == 0 ? r / LC : r % LO1H;
+      const T* src = sU + ub(ci, oi) + (e2 + 1) * H * US;
+      T cu[H], out[H];
+#pragma unroll
+      for (int j = 0; j < H; ++j) cu[j] = src[j * US];
+      cell_mass<T, K>(cu, out);
+#pragma unroll
+      for (int a = 0; a < H; ++a) sA1[((e2 * H + a) * LO1H + oi) * PC + ci] = out[a];
+    }
     const int cell_o2 = G.c0[O2];
-    const bool bnd = (cell_o2 == 0) || (cell_o2 + NO2 >= m);
-    const int efirst = (cell_o2 == 0) ? 0 : -1;
-    const int elast = (m - 1 - cell_o2 < NO2) ? m - 1 - cell_o2 : -1;
-    constexpr int NPEN = LC * LO1H;
-    for (int p = tid; p < NPEN; p += NT) {
-      // consecutive threads walk the staged box's x axis: c for C=0, o1 for C=1,2
-      const int ci = C == 0 ? p % LC : p / LO1H;
-      const int oi = C == 0 ? p / LC : p % LO1H;
-      // element (c=ci, o1=oi, o2=j) of the staged box
-      const int ub = C == 0 ? oi * UX + ci + row_shift0<T>(G, H, G.g0[1] - H + oi)
-                            : (C == 1 ? ci * UX + oi : ci * UY * UX + oi) + brick_shift<T>(G, H);
-      constexpr int US = C == 0 ? UX * UY : (C == 1 ? UX * UY : UX);  // stride along o2
-      T in[(NO2 + 2) * H];
+    constexpr int NLB = LC * No1;
+    for (int it = tid; it < NLB * NO2; it += NT) {
+      const int e2 = it / NLB, r = it - e2 * NLB;
+      const int ci = C == 0 ? r % LC : r / No1;
+      const int o = C == 0 ? r / LC : r % No1;
+      const T* src = sU + ub(ci, o + H) + e2 * H * US;
+      T pv[H], cu[H], nx[H], out[H];
 #pragma unroll
-      for (int j = 0; j < (NO2 + 2) * H; ++j) in[j] = sU[ub + j * US];
-      T a1[No2];
-      dg_mass<T, K, NO2, 1>(in, a1);
-#pragma unroll
-      for (int j = 0; j < No2; ++j) sA1[(j * LO1H + oi) * PC + ci] = a1[j];
-      if (oi >= H && oi < H + No1) {
-        T b1[No2];
-        if (bnd) dg_sipg<T, K, NO2, true>(in, b1, efirst, elast);
-        else dg_sipg<T, K, NO2, false>(in, b1, -1, -1);
-#pragma unroll
-        for (int j = 0; j < No2; ++j) sB1[(j * No1 + (oi - H)) * PC + ci] = b1[j];
+      for (int j = 0; j < H; ++j) {
+        pv[j] = src[j * US];
+        cu[j] = src[(H + j) * US];
+        nx[j] = src[(2 * H + j) * US];
       }
+      cell_sipg<T, K>(pv, cu, nx, cell_o2 + e2 == 0, cell_o2 + e2 == m - 1, out);
+#pragma unroll
+      for (int a = 0; a < H; ++a) sB1[((e2 * H + a) * No1 + o) * PC + ci] = out[a];
     }
   }
   __syncthreads();
-  // ---- pass 2 (along o1): S = M_o1 A1, T = L_o1 A1 + M_o1 B1  (c full, o1/o2 owned) ----
+  // ---- pass 2 (along o1): S = M_o1 A1, T = L_o1 A1 + M_o1 B1 (c full, o1/o2 owned) ----
   {
     const int cell_o1 = G.c0[O1];
-    const bool bnd = (cell_o1 == 0) || (cell_o1 + NO1 >= m);
-    const int efirst = (cell_o1 == 0) ? 0 : -1;
-    const int elast = (m - 1 - cell_o1 < NO1) ? m - 1 - cell_o1 : -1;
-    constexpr int NPEN = LC * No2;
-    for (int p = tid; p < NPEN; p += NT) {
-      const int ci = p % LC, oj = p / LC;
-      T in[(NO1 + 2) * H];
+    constexpr int NL = LC * No2;
+    for (int it = tid; it < NL * NO1; it += NT) {
+      const int e1 = it / NL, r = it - e1 * NL;
+      const int ci = r % LC, oj = r / LC;
+      const T* a1 = sA1 + (oj * LO1H + e1 * H) * PC + ci;
+      const T* b1 = sB1 + (oj * No1 + e1 * H) * PC + ci;
+      T pv[H], cu[H], nx[H], bb[H];
 #pragma unroll
-      for (int j = 0; j < (NO1 + 2) * H; ++j) in[j] = sA1[(oj * LO1H + j) * PC + ci];
-      T s[No1], t[No1];
-      dg_mass<T, K, NO1, 1>(in, s);
-      if (bnd) dg_sipg<T, K, NO1, true>(in, t, efirst, elast);
-      else dg_sipg<T, K, NO1, false>(in, t, -1, -1);
-      T bb[No1];
+      for (int j = 0; j < H; ++j) {
+        pv[j] = a1[j * PC];
+        cu[j] = a1[(H + j) * PC];
+        nx[j] = a1[(2 * H + j) * PC];
+        bb[j] = b1[j * PC];
+      }
+      T sv[H], tv[H], mb[H];
+      cell_mass<T, K>(cu, sv);
+      cell_sipg<T, K>(pv, cu, nx, cell_o1 + e1 == 0, cell_o1 + e1 == m - 1, tv);
+      cell_mass<T, K>(bb, mb);
 #pragma unroll
-      for (int j = 0; j < No1; ++j) bb[j] = sB1[(oj * No1 + j) * PC + ci];
-      T mb[No1];
-      dg_mass<T, K, NO1, 0>(bb, mb);
-#pragma unroll
-      for (int j = 0; j < No1; ++j) {
-        sS[(oj * No1 + j) * PC + ci] = s[j];
-        sT[(oj * No1 + j) * PC + ci] = t[j] + mb[j];
+      for (int a = 0; a < H; ++a) {
+        sS[(oj * No1 + e1 * H + a) * PC + ci] = sv[a];
+        sT[(oj * No1 + e1 * H + a) * PC + ci] = tv[a] + mb[a];
       }
     }
   }
   __syncthreads();
   // ---- pass 3 (along c): y_c = h (L_c S + M_c T) + h^2 D^T Q ;  y_p += h^2 D S ----
+  // item (o1 line oi, o2 line oj, cell e) reads the window [eH, eH + 2H] of the c pencils
+  constexpr int NCP = odd(Nc);
+  T* sYC = sA1;  // C = 0: outputs staged in smem (A1 is dead) for a coalesced x-row write-out
   {
-    using R = Ref<K>;
-    constexpr int P = K + 2;
     const T h2 = h * h;
     const T* __restrict__ bc = RESID ? b + C * sizeV : nullptr;
     T* __restrict__ yc = y + C * sizeV;
-    constexpr int NPEN = No1 * No2;
     constexpr int YSC = BR::stride(C, BR::YX, BR::N(1)), YSO1 = BR::stride(O1, BR::YX, BR::N(1)),
                   YSO2 = BR::stride(O2, BR::YX, BR::N(1));
-    for (int p = tid; p < NPEN; p += NT) {
-      const int oi = p % No1, oj = p / No1;
-      T s[LC], t[LC], q[LC - 1];
-      const int base = (oj * No1 + oi) * PC;
+    constexpr int NL = No1 * No2;
+    for (int it = tid; it < NL * NCc; it += NT) {
+      const int e = it / NL, r = it - e * NL;
+      const int oi = r % No1, oj = r / No1;
+      const int base = (oj * No1 + oi) * PC + e * H;
+      T s[2 * H + 1], t[2 * H + 1], q[2 * H];
 #pragma unroll
-      for (int j = 0; j < LC; ++j) {
+      for (int j = 0; j < 2 * H + 1; ++j) {
         s[j] = sS[base + j];
         t[j] = sT[base + j];
       }
 #pragma unroll
-      for (int j = 0; j < LC - 1; ++j) q[j] = sQ[base + j];
+      for (int j = 0; j < 2 * H; ++j) q[j] = sQ[base + j];
       int g[3];
       g[O1] = G.g0[O1] + oi;
       g[O2] = G.g0[O2] + oj;
       const bool inside = g[O1] < n && g[O2] < n;
-      T* yp = sYP + oi * YSO1 + oj * YSO2;
 #pragma unroll
-      for (int e = 0; e < NCc; ++e) {
+      for (int a = 0; a < H; ++a) {
+        T v = T(0), w = T(0);
 #pragma unroll
-        for (int a = 0; a < H; ++a) {
-          const int j = e * H + a + H;  // pencil index of the output node
-          T v = T(0), w = T(0);
+        for (int bq = 0; bq < P; ++bq) {
+          v += cref<T>(R::LP + a * P + bq) * s[H + bq] + cref<T>(R::MP + a * P + bq) * t[H + bq];
+          if (a == 0) v += cref<T>(R::LP + (K + 1) * P + bq) * s[bq] + cref<T>(R::MP + (K + 1) * P + bq) * t[bq];
+        }
 #pragma unroll
-          for (int bq = 0; bq < P; ++bq) {
-            v += cref<T>(R::LP + a * P + bq) * s[j - a + bq] + cref<T>(R::MP + a * P + bq) * t[j - a + bq];
-            if (a == 0)
-              v += cref<T>(R::LP + (K + 1) * P + bq) * s[j - H + bq] + cref<T>(R::MP + (K + 1) * P + bq) * t[j - H + bq];
-          }
-#pragma unroll
-          for (int i = 0; i < H; ++i) {
-            w += cref<T>(R::D + i * P + a) * q[j - a + i];
-            if (a == 0) w += cref<T>(R::D + i * P + H) * q[j - H + i];
-          }
+        for (int i = 0; i < H; ++i) {
+          w += cref<T>(R::D + i * P + a) * q[H + i];
+          if (a == 0) w += cref<T>(R::D + i * P + H) * q[i];
+        }
+        const T val = h * v + h2 * w;
+        if (C == 0) {
+          sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
+        } else {
           g[C] = G.g0[C] + e * H + a;
           if (inside && g[C] < n) {
             const int64_t gi = g[0] * st[0] + g[1] * st[1] + g[2] * st[2];
-            T r = h * v + h2 * w;
-            if (g[C] == 0) r = T(0);  // constrained boundary-normal row
-            else if (RESID) r = bc[gi] - r;
-            yc[gi] = r;
+            T rr = val;
+            if (g[C] == 0) rr = T(0);  // constrained boundary-normal row
+            else if (RESID) rr = bc[gi] - rr;
+            yc[gi] = rr;
           }
         }
-        // pressure rows of cell e: y_p += h^2 D S
+      }
+      // pressure rows of cell e: y_p += h^2 D S
+      T* yp = sYP + oi * YSO1 + oj * YSO2;
 #pragma unroll
-        for (int i = 0; i < H; ++i) {
-          T z = T(0);
+      for (int i = 0; i < H; ++i) {
+        T z = T(0);
 #pragma unroll
-          for (int bq = 0; bq < P; ++bq) z += cref<T>(R::D + i * P + bq) * s[e * H + H + bq];
-          yp[(e * H + i) * YSC] += h2 * z;
-        }
+        for (int bq = 0; bq < P; ++bq) z += cref<T>(R::D + i * P + bq) * s[H + bq];
+        yp[(e * H + i) * YSC] += h2 * z;
       }
       // the constrained plane g_c = n belongs to the brick holding the last cell along c
-      if (inside && G.c0[C] + NCc >= m) {
+      if (C != 0 && e == NCc - 1 && inside && G.c0[C] + NCc >= m) {
         g[C] = n;
         yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
+      }
+    }
+    if (C == 0) {
+      __syncthreads();
+      // coalesced write-out of the u_x rows (x = c fastest), plus the constrained plane x = n
+      const bool last = G.c0[0] + NCc >= m;
+      constexpr int NW = (Nc + 1) * No1 * No2;
+      for (int i = tid; i < NW; i += NT) {
+        const int lx = i % (Nc + 1), r = i / (Nc + 1);
+        const int ly = r % No1, lz = r / No1;
+        const int gx = G.g0[0] + lx, gy = G.g0[1] + ly, gz = G.g0[2] + lz;
+        if (gy >= n || gz >= n || gx > n) continue;
+        if (lx == Nc && !(last && gx == n)) continue;
+        const int64_t gi = (static_cast<int64_t>(gz) * n + gy) * (n + 1) + gx;
+        T rr;
+        if (gx == 0 || gx == n) rr = T(0);
+        else {
+          rr = sYC[(lz * No1 + ly) * NCP + lx];
+          if (RESID) rr = bc[gi] - rr;
+        }
+        yc[gi] = rr;
       }
     }
   }
@@ -586,10 +621,10 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
 }
 
 // write the pressure rows of this brick from the smem accumulator
-template <typename T, int K, int BX, int BY, int BZ, int NT, bool RESID>
+template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, bool RESID>
 __device__ __forceinline__ void write_pressure(const T* sYP, const Geo& G, T* __restrict__ y, const T* __restrict__ b,
                                                int64_t offP) {
-  using BR = Brick<T, K, BX, BY, BZ>;
+  using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int N0 = BR::N(0), N1 = BR::N(1), N2 = BR::N(2);
   const int n = G.n;
   for (int i = threadIdx.x; i < N0 * N1 * N2; i += NT) {
@@ -614,11 +649,11 @@ __device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, i
 // component boxes of a brick alternate between two U buffers (each with its own mbarrier) so that
 // the TMA staging of the next component -- and of the next brick's first component and pressure
 // box -- overlaps compute.
-template <typename T, int K, int BX, int BY, int BZ, int NT, bool RESID, bool TMA>
-__global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
+template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, bool RESID, bool TMA>
+__global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
                                                              const T* __restrict__ b, int m, T h,
                                                              const Maps* __restrict__ mapsp) {
-  using BR = Brick<T, K, BX, BY, BZ>;
+  using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -644,8 +679,8 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
   fence_proxy_async();
   __syncthreads();
   brick_geo(G, brick, nbx, nby, BX, BY, BZ, H);
-  issue_p<T, K, BX, BY, BZ, NT, TMA>(sP, &bars[2], x, maps, G);
-  issue_u<T, K, BX, BY, BZ, NT, 0, TMA>(sm, &bars[0], x, maps, G);
+  issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, &bars[2], x, maps, G);
+  issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sm, &bars[0], x, maps, G);
   if (!TMA) cp_async_commit();
   int u0 = 0;
   unsigned ph[2] = {0, 0}, phP = 0;  // mbarrier phase of buffer 0 / 1 / P
@@ -672,28 +707,28 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
       for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
       wait_u(true);
       if (TMA) {
-        fix_columns<T, K, BX, BY, BZ, NT>(sm, nullptr, nullptr, sP, G);
+        fix_columns<T, K, BX, BY, BZ, OCC, NT>(sm, nullptr, nullptr, sP, G);
         __syncthreads();
       }
-      component<T, K, BX, BY, BZ, NT, 0, RESID, TMA>(sm, sm, G, h, nullptr, x, y, b, maps, &bars[2]);
-      issue_u<T, K, BX, BY, BZ, NT, 1, TMA>(sm, &bars[0], x, maps, G);
+      component<T, K, BX, BY, BZ, OCC, NT, 0, RESID, TMA>(sm, sm, G, h, nullptr, x, y, b, maps, &bars[2]);
+      issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA>(sm, &bars[0], x, maps, G);
       wait_u(false);
       if (TMA) {
-        fix_columns<T, K, BX, BY, BZ, NT>(nullptr, sm, nullptr, nullptr, G);
+        fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, sm, nullptr, nullptr, G);
         __syncthreads();
       }
-      component<T, K, BX, BY, BZ, NT, 1, RESID, TMA>(sm, sm, G, h, nullptr, x, y, b, maps, &bars[2]);
-      issue_u<T, K, BX, BY, BZ, NT, 2, TMA>(sm, &bars[0], x, maps, G);
+      component<T, K, BX, BY, BZ, OCC, NT, 1, RESID, TMA>(sm, sm, G, h, nullptr, x, y, b, maps, &bars[2]);
+      issue_u<T, K, BX, BY, BZ, OCC, NT, 2, TMA>(sm, &bars[0], x, maps, G);
       wait_u(false);
       if (TMA) {
-        fix_columns<T, K, BX, BY, BZ, NT>(nullptr, nullptr, sm, nullptr, G);
+        fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, nullptr, sm, nullptr, G);
         __syncthreads();
       }
-      component<T, K, BX, BY, BZ, NT, 2, RESID, TMA>(sm, sm, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
+      component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, sm, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
                                                      &bars[2]);
-      write_pressure<T, K, BX, BY, BZ, NT, RESID>(sYP, G, y, b, offP);
+      write_pressure<T, K, BX, BY, BZ, OCC, NT, RESID>(sYP, G, y, b, offP);
       __syncthreads();
-      if (has_next) issue_u<T, K, BX, BY, BZ, NT, 0, TMA>(sm, &bars[0], x, maps, Gn);
+      if (has_next) issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sm, &bars[0], x, maps, Gn);
       G = Gn;
     }
     if (!TMA) cp_async_wait<0>();
@@ -705,7 +740,7 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
     const int next = brick + gridDim.x;
     const bool has_next = next < nbricks;
     if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H);
-    issue_u<T, K, BX, BY, BZ, NT, 1, TMA>(bufB, &bars[ib], x, maps, G);
+    issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA>(bufB, &bars[ib], x, maps, G);
     for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
     if (TMA) {
       mbar_wait(&bars[2], phP);
@@ -718,11 +753,11 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
     }
     __syncthreads();
     if (TMA) {
-      fix_columns<T, K, BX, BY, BZ, NT>(bufA, nullptr, nullptr, sP, G);
+      fix_columns<T, K, BX, BY, BZ, OCC, NT>(bufA, nullptr, nullptr, sP, G);
       __syncthreads();
     }
-    component<T, K, BX, BY, BZ, NT, 0, RESID, TMA>(sm, bufA, G, h, nullptr, x, y, b, maps, &bars[2]);
-    issue_u<T, K, BX, BY, BZ, NT, 2, TMA>(bufA, &bars[ia], x, maps, G);
+    component<T, K, BX, BY, BZ, OCC, NT, 0, RESID, TMA>(sm, bufA, G, h, nullptr, x, y, b, maps, &bars[2]);
+    issue_u<T, K, BX, BY, BZ, OCC, NT, 2, TMA>(bufA, &bars[ia], x, maps, G);
     if (TMA) {
       mbar_wait(&bars[ib], ph[ib]);
       ph[ib] ^= 1;
@@ -732,11 +767,11 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
     }
     __syncthreads();
     if (TMA) {
-      fix_columns<T, K, BX, BY, BZ, NT>(nullptr, bufB, nullptr, nullptr, G);
+      fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, bufB, nullptr, nullptr, G);
       __syncthreads();
     }
-    component<T, K, BX, BY, BZ, NT, 1, RESID, TMA>(sm, bufB, G, h, nullptr, x, y, b, maps, &bars[2]);
-    if (has_next) issue_u<T, K, BX, BY, BZ, NT, 0, TMA>(bufB, &bars[ib], x, maps, Gn);
+    component<T, K, BX, BY, BZ, OCC, NT, 1, RESID, TMA>(sm, bufB, G, h, nullptr, x, y, b, maps, &bars[2]);
+    if (has_next) issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(bufB, &bars[ib], x, maps, Gn);
     if (TMA) {
       mbar_wait(&bars[ia], ph[ia]);
       ph[ia] ^= 1;
@@ -746,12 +781,12 @@ __global__ void __launch_bounds__(NT, 1) stokes_vmult_kernel(const T* __restrict
     }
     __syncthreads();
     if (TMA) {
-      fix_columns<T, K, BX, BY, BZ, NT>(nullptr, nullptr, bufA, nullptr, G);
+      fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, nullptr, bufA, nullptr, G);
       __syncthreads();
     }
-    component<T, K, BX, BY, BZ, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
+    component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
                                                    &bars[2]);
-    write_pressure<T, K, BX, BY, BZ, NT, RESID>(sYP, G, y, b, offP);
+    write_pressure<T, K, BX, BY, BZ, OCC, NT, RESID>(sYP, G, y, b, offP);
     __syncthreads();  // y_p accumulator is re-zeroed by the next brick
     G = Gn;
     u0 ^= 1;
@@ -788,9 +823,9 @@ void encode(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, 
 
 // TMA needs 16-B aligned row pitches / base offsets (n * sizeof(T) % 16 == 0); boxes are kept no
 // larger than the tensor (small coarse levels take the cp.async path).
-template <typename T, int K, int BX, int BY, int BZ>
+template <typename T, int K, int BX, int BY, int BZ, int OCC>
 bool tma_ok(int n) {
-  using BR = Brick<T, K, BX, BY, BZ>;
+  using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   if ((static_cast<int64_t>(n) * sizeof(T)) % 16 != 0) return false;
   const int lim = n - 1;  // smallest extent among the u_y / u_z maps
@@ -801,9 +836,9 @@ bool tma_ok(int n) {
   return true;
 }
 
-template <typename T, int K, int BX, int BY, int BZ>
+template <typename T, int K, int BX, int BY, int BZ, int OCC>
 Maps make_maps(const T* x, int n) {
-  using BR = Brick<T, K, BX, BY, BZ>;
+  using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   Maps M;
   std::memset(&M, 0, sizeof(M));
@@ -835,19 +870,19 @@ Maps make_maps(const T* x, int n) {
   return M;
 }
 
-template <typename T, int K, int BX, int BY, int BZ, int NT>
+template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT>
 void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
-  using BR = Brick<T, K, BX, BY, BZ>;
+  using BR = Brick<T, K, BX, BY, BZ, OCC>;
   const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
   const int m = dl.lay.m, n = dl.lay.n;
   const T h = static_cast<T>(1.0 / m);
   const int nbricks = ((m + BX - 1) / BX) * ((m + BY - 1) / BY) * ((m + BZ - 1) / BZ);
   static int num_sms = 0;
   if (num_sms == 0) SMG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ctx.device));
-  const dim3 grid(std::min(nbricks, num_sms));
+  const dim3 grid(std::min(nbricks, OCC * num_sms));
   const size_t smem = BR::BYTES;
   static const bool no_tma = std::getenv("SMG_NO_TMA") != nullptr;  // diagnostics: force the cp.async path
-  const bool tma = !no_tma && tma_ok<T, K, BX, BY, BZ>(n) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  const bool tma = !no_tma && tma_ok<T, K, BX, BY, BZ, OCC>(n) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
   const Maps* dmaps = nullptr;
   if (tma) {
     // tensor maps are cached per (input vector, level, precision) in 64-B aligned global slots,
@@ -858,7 +893,7 @@ void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
       const int slot = ctx.tmap_next++ % kTmapSlots;
       for (auto e = ctx.tmap_slots.begin(); e != ctx.tmap_slots.end();)
         e = (e->second == slot) ? ctx.tmap_slots.erase(e) : std::next(e);
-      Maps mh = make_maps<T, K, BX, BY, BZ>(static_cast<const T*>(x), n);
+      Maps mh = make_maps<T, K, BX, BY, BZ, OCC>(static_cast<const T*>(x), n);
       char* dst = static_cast<char*>(ctx.tmap_dev) + static_cast<size_t>(slot) * kTmapSlotBytes;
       SMG_CUDA(cudaMemcpyAsync(dst, &mh, sizeof(Maps), cudaMemcpyHostToDevice, ctx.stream));
       SMG_CUDA(cudaStreamSynchronize(ctx.stream));  // mh is a stack temporary
@@ -874,11 +909,11 @@ void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
                                          dmaps);
   };
   if (b) {
-    if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, true, true>);
-    else go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, true, false>);
+    if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, OCC, NT, true, true>);
+    else go(stokes_vmult_kernel<T, K, BX, BY, BZ, OCC, NT, true, false>);
   } else {
-    if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, false, true>);
-    else go(stokes_vmult_kernel<T, K, BX, BY, BZ, NT, false, false>);
+    if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, OCC, NT, false, true>);
+    else go(stokes_vmult_kernel<T, K, BX, BY, BZ, OCC, NT, false, false>);
   }
   SMG_CUDA(cudaGetLastError());
   ++ctx.launches;
@@ -888,25 +923,55 @@ void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
 
 // Brick shape (cells) per degree: fp64 SMEM ~80-200 KB, one persistent CTA per SM.
 template <typename T, int K> struct BrickShape;
-template <typename T> struct BrickShape<T, 1> { static constexpr int X = 8, Y = 4, Z = 4; };
-template <typename T> struct BrickShape<T, 2> { static constexpr int X = 4, Y = 4, Z = 4; };
-template <typename T> struct BrickShape<T, 3> { static constexpr int X = 4, Y = 2, Z = 2; };
-template <typename T> struct BrickShape<T, 4> { static constexpr int X = 2, Y = 2, Z = 2; };
-template <> struct BrickShape<double, 5> { static constexpr int X = 2, Y = 1, Z = 1; };
-template <> struct BrickShape<float, 5> { static constexpr int X = 2, Y = 2, Z = 1; };
-template <> struct BrickShape<double, 6> { static constexpr int X = 1, Y = 1, Z = 1; };
-template <> struct BrickShape<float, 6> { static constexpr int X = 2, Y = 1, Z = 1; };
-template <> struct BrickShape<double, 7> { static constexpr int X = 1, Y = 1, Z = 1; };  // single U buffer
-template <> struct BrickShape<float, 7> { static constexpr int X = 2, Y = 1, Z = 1; };
+// NT: threads per CTA; OCC: resident CTAs per SM (persistent grid of OCC x #SMs, __launch_bounds__(NT, OCC))
+template <typename T> struct BrickShape<T, 1> { static constexpr int X = 8, Y = 4, Z = 4, NT = 512, OCC = 1; };
+template <typename T> struct BrickShape<T, 2> { static constexpr int X = 4, Y = 4, Z = 2, NT = 384, OCC = 2; };
+template <typename T> struct BrickShape<T, 3> { static constexpr int X = 4, Y = 2, Z = 2, NT = 512, OCC = 1; };
+template <typename T> struct BrickShape<T, 4> { static constexpr int X = 2, Y = 2, Z = 2, NT = 384, OCC = 1; };
+template <> struct BrickShape<double, 5> { static constexpr int X = 2, Y = 1, Z = 1, NT = 256, OCC = 1; };
+template <> struct BrickShape<float, 5> { static constexpr int X = 2, Y = 2, Z = 1, NT = 256, OCC = 1; };
+template <> struct BrickShape<double, 6> { static constexpr int X = 1, Y = 1, Z = 1, NT = 256, OCC = 1; };
+template <> struct BrickShape<float, 6> { static constexpr int X = 2, Y = 1, Z = 1, NT = 256, OCC = 1; };
+template <> struct BrickShape<double, 7> { static constexpr int X = 1, Y = 1, Z = 1, NT = 256, OCC = 1; };
+template <> struct BrickShape<float, 7> { static constexpr int X = 2, Y = 1, Z = 1, NT = 256, OCC = 1; };
+
+template <typename T, int K, class S>
+void launch_shape(Context& ctx, int level, void* y, const void* x, const void* b) {
+  static_assert(Brick<T, K, S::X, S::Y, S::Z, S::OCC>::BYTES <= (S::OCC == 1 ? 232448 : 233472 / S::OCC - 1024),
+                "brick exceeds the shared memory of its occupancy");
+  launch_t<T, K, S::X, S::Y, S::Z, S::OCC, S::NT>(ctx, level, y, x, b);
+}
+
+#ifdef SMG_TUNE
+// tuning build only: alternative brick shapes selected by SMG_VMULT_VARIANT=1..N
+template <int X_, int Y_, int Z_, int NT_, int OCC_>
+struct Shape { static constexpr int X = X_, Y = Y_, Z = Z_, NT = NT_, OCC = OCC_; };
+template <typename T, int K>
+bool launch_variant(int v, Context& ctx, int level, void* y, const void* x, const void* b) {
+  switch (v) {
+    case 1: launch_shape<T, K, Shape<4, 4, 2, 256, 2>>(ctx, level, y, x, b); return true;
+    case 2: launch_shape<T, K, Shape<4, 2, 2, 256, 2>>(ctx, level, y, x, b); return true;
+    case 3: launch_shape<T, K, Shape<2, 2, 2, 128, 4>>(ctx, level, y, x, b); return true;
+    case 4: launch_shape<T, K, Shape<4, 4, 2, 384, 2>>(ctx, level, y, x, b); return true;
+    case 5: launch_shape<T, K, Shape<8, 2, 2, 256, 2>>(ctx, level, y, x, b); return true;
+    case 6: launch_shape<T, K, Shape<4, 2, 2, 128, 3>>(ctx, level, y, x, b); return true;
+    default: return false;
+  }
+}
+#endif
 
 template <int K>
 void vmult_launch_k(Context& ctx, int level, int prec, void* y, const void* x, const void* b) {
-  using SD = BrickShape<double, K>;
-  using SF = BrickShape<float, K>;
-  static_assert(Brick<double, K, SD::X, SD::Y, SD::Z>::BYTES <= 232448, "fp64 brick exceeds 227 KB");
-  static_assert(Brick<float, K, SF::X, SF::Y, SF::Z>::BYTES <= 232448, "fp32 brick exceeds 227 KB");
-  if (prec == SMG_F64) launch_t<double, K, SD::X, SD::Y, SD::Z, 256>(ctx, level, y, x, b);
-  else launch_t<float, K, SF::X, SF::Y, SF::Z, 256>(ctx, level, y, x, b);
+#ifdef SMG_TUNE
+  static const int variant = std::getenv("SMG_VMULT_VARIANT") ? std::atoi(std::getenv("SMG_VMULT_VARIANT")) : 0;
+  if (K == 2 && variant > 0) {
+    if (prec == SMG_F64 ? launch_variant<double, K>(variant, ctx, level, y, x, b)
+                        : launch_variant<float, K>(variant, ctx, level, y, x, b))
+      return;
+  }
+#endif
+  if (prec == SMG_F64) launch_shape<double, K, BrickShape<double, K>>(ctx, level, y, x, b);
+  else launch_shape<float, K, BrickShape<float, K>>(ctx, level, y, x, b);
 }
 
 template <int K>

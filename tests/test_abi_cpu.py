@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 import oracle
@@ -47,3 +48,24 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(Exception):
         smg.Context(2, 2)
+
+
+@pytest.mark.parametrize("k,level", [(1, 0), (2, 1)])
+def test_blockvector_pressure_numbering(k, level):
+    # pressure is numbered cell by cell (cells x-fastest), (k+1)^3 nodes per cell x-fastest
+    H, m = k + 1, 2 << level
+    n = m * H
+    perm = smg.pressure_cell_local_index(k, level)
+    assert sorted(perm.tolist()) == list(range(n ** 3))
+    i = 0
+    for cz in range(m):
+        for cy in range(m):
+            for cx in range(m):
+                for az in range(H):
+                    for ay in range(H):
+                        for ax in range(H):
+                            g = ((cz * H + az) * n + cy * H + ay) * n + cx * H + ax
+                            assert perm[i] == g
+                            i += 1
+    v = np.random.default_rng(0).uniform(size=smg.level_sizes(k, level)[4])
+    assert np.array_equal(smg.from_blockvector(smg.to_blockvector(v, k, level), k, level), v)

@@ -131,13 +131,27 @@ def test_solve_iteration_counts(k, level):
         assert res <= 2e-8
 
 
-def test_vmult_host_blockvector_path():
-    k, level = 2, 2
+@pytest.mark.parametrize("k,level", [(1, 2), (2, 2), (3, 1)])
+def test_vmult_host_blockvector_path(k, level):
+    # reference-facing path: BlockVector blocks with the cell-local pressure numbering
     ctx = smg.Context(k, level)
     x = rand_vec(k, level, 14)
-    blocks = smg.split_blocks(x, k, level)
-    ys = ctx.vmult_host(level, blocks)
-    assert rel(np.concatenate(ys), oracle.apply_stokes(k, level, x)) <= 1e-12
+    ys = ctx.vmult_host(level, smg.to_blockvector(x, k, level))
+    assert rel(smg.from_blockvector(ys, k, level), oracle.apply_stokes(k, level, x)) <= 1e-12
+    ys32 = ctx.vmult_host(level, [b.astype(np.float32) for b in smg.to_blockvector(x, k, level)], smg.F32)
+    assert rel(smg.from_blockvector(ys32, k, level).astype(np.float64), oracle.apply_stokes(k, level, x)) <= 1e-5
+
+
+def test_vec_upload_download_roundtrip():
+    k, level = 2, 2
+    ctx = smg.Context(k, level)
+    x = rand_vec(k, level, 15)
+    blocks = smg.to_blockvector(x, k, level)
+    v = ctx.upload(level, blocks)
+    assert np.array_equal(v.cpu().numpy(), x)  # device layout: pressure global lexicographic
+    back = ctx.download(level, v)
+    for a, b in zip(back, blocks):
+        assert np.array_equal(a, b)
 
 
 def test_large_level_properties_symmetry_linearity():
