@@ -90,6 +90,21 @@ int smg_vcycle(smg_context* ctx, int level, int precision, void* x, const void* 
 int smg_solve(smg_context* ctx, int level, void* x, const void* b, double rel_tol, int max_iter,
               int vcycle_precision, int* iters, double* history);
 
+/* ---- z-slab partition (multi-GPU, one context per GPU). A slab vector holds the cells
+ *      [max(z0-1,0), min(z1+1,m)) of the level: the owned cells [z0, z1) plus one ghost cell layer on
+ *      each interior side; every block keeps its global x/y extents and the z node planes of those
+ *      cells (u_z: the planes zlo(k+1) .. zhi(k+1) inclusive). The caller refreshes the ghost layers
+ *      (halo exchange) before each apply; the operator writes the rows of the owned cells only.
+ *      z1 - z0 must be a multiple of the kernel's brick depth (1, 2 or 4; use multiples of 4) unless
+ *      z1 == m. ---- */
+int smg_slab_sizes(int degree, int level, int z0, int z1, int64_t sizes[5]);
+int smg_vmult_slab(smg_context* ctx, int level, int precision, void* y, const void* x, int z0, int z1);
+int smg_residual_slab(smg_context* ctx, int level, int precision, void* r, const void* b, const void* x, int z0,
+                      int z1);
+/* dot over the owned rows of two slab vectors (fp64 accumulate); the caller all-reduces across ranks */
+int smg_dot_slab(smg_context* ctx, int level, int precision, const void* a, const void* b, int z0, int z1,
+                 double* out);
+
 /* ---- BLAS-1 on level vectors (block_vector.hpp:52-93); dots accumulate in fp64 ---- */
 int smg_dot(smg_context* ctx, int level, int precision, const void* a, const void* b, double* out);
 int smg_axpy(smg_context* ctx, int level, int precision, double alpha, const void* x, void* y);

@@ -24,7 +24,8 @@ EXPORTED = [
     "smg_config_default", "smg_create", "smg_destroy", "smg_set_stream", "smg_last_error", "smg_launch_count",
     "smg_level_sizes", "smg_vec_alloc", "smg_vec_free", "smg_vmult", "smg_residual", "smg_smooth",
     "smg_prolongate_add", "smg_restrict", "smg_coarse_solve", "smg_vcycle", "smg_solve", "smg_dot", "smg_axpy",
-    "smg_convert", "smg_vmult_host", "smg_vec_upload", "smg_vec_download",
+    "smg_convert", "smg_vmult_host", "smg_vec_upload", "smg_vec_download", "smg_slab_sizes", "smg_vmult_slab",
+    "smg_residual_slab", "smg_dot_slab",
 ]
 
 
@@ -80,6 +81,10 @@ def lib():
         L.smg_convert.argtypes = [P, I, I, P, I, P]
         L.smg_vmult_host.argtypes = [P, I, I, P, P, P, P]
         L.smg_vec_upload.argtypes = [P, I, I, P, P, P]
+        L.smg_slab_sizes.argtypes = [I, I, I, I, P]
+        L.smg_vmult_slab.argtypes = [P, I, I, P, P, I, I]
+        L.smg_residual_slab.argtypes = [P, I, I, P, P, P, I, I]
+        L.smg_dot_slab.argtypes = [P, I, I, P, P, I, I, ctypes.POINTER(D)]
         L.smg_vec_download.argtypes = [P, I, I, P, P, P]
         _LIB = L
     return _LIB

@@ -4,6 +4,7 @@
 // kernels from the host. No CPU fallback: every numeric operation runs on the device.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -553,6 +554,64 @@ int smg_solve(smg_context* h, int level, void* x, const void* b, double rel_tol,
     if (max_iter < 1) throw std::invalid_argument("max_iter must be >= 1");
     return smg::fgmres(c, level, static_cast<double*>(x), static_cast<const double*>(b), rel_tol, max_iter, vp,
                        iters, history);
+  });
+}
+
+int smg_slab_sizes(int degree, int level, int z0, int z1, int64_t sizes[5]) {
+  try {
+    const int m = 2 << level;
+    smg::LevelLayout l(degree, level, std::max(z0 - 1, 0), std::min(z1 + 1, m));
+    if (z0 < 0 || z1 > m || z0 >= z1) return SMG_EINVAL;
+    for (int i = 0; i < 4; ++i) sizes[i] = l.size[i];
+    sizes[4] = l.total;
+    return SMG_OK;
+  } catch (...) {
+    return SMG_EINVAL;
+  }
+}
+
+int smg_vmult_slab(smg_context* h, int level, int precision, void* y, const void* x, int z0, int z1) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!x || !y || x == y) throw std::invalid_argument("vmult_slab: x and y must be distinct non-null vectors");
+    smg::launch_vmult_slab(c, level, precision, y, x, nullptr, z0, z1);
+    return SMG_OK;
+  });
+}
+
+int smg_residual_slab(smg_context* h, int level, int precision, void* r, const void* b, const void* x, int z0, int z1) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!r || !b || !x || r == x || r == b) throw std::invalid_argument("residual_slab: r must differ from b and x");
+    smg::launch_vmult_slab(c, level, precision, r, x, b, z0, z1);
+    return SMG_OK;
+  });
+}
+
+int smg_dot_slab(smg_context* h, int level, int precision, const void* a, const void* b, int z0, int z1, double* out) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!out) throw std::invalid_argument("dot_slab: null output");
+    const int m = c.dev[0][level].lay.m, H = c.cfg.degree + 1;
+    if (z0 < 0 || z1 > m || z0 >= z1) throw std::invalid_argument("dot_slab: owned range out of range");
+    const smg::LevelLayout lay(c.cfg.degree, level, std::max(z0 - 1, 0), std::min(z1 + 1, m));
+    int64_t beg[4], len[4];
+    for (int blk = 0; blk < 4; ++blk) {
+      // owned node planes of the block (u_z: plus the constrained top plane on the last slab)
+      const int64_t p0 = static_cast<int64_t>(z0 - lay.zlo) * H;
+      int64_t p1 = static_cast<int64_t>(z1 - lay.zlo) * H;
+      if (blk == 2 && z1 == m) p1 += 1;
+      beg[blk] = lay.off[blk] + p0 * lay.plane[blk];
+      len[blk] = (p1 - p0) * lay.plane[blk];
+    }
+    *out = smg::dot_ranges(c, precision, a, b, beg, len, 4);
+    return SMG_OK;
   });
 }
 

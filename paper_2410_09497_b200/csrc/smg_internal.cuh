@@ -29,29 +29,48 @@ struct not_converged : std::runtime_error {
   } while (0)
 
 // Stored layout of one level vector.
+// A z-slab holds the cells [zlo, zhi) of the level (the whole level: [0, m)); each block keeps the
+// global x/y extents and the node planes of those cells (u_z: planes zlo*H .. zhi*H inclusive).
 struct LevelLayout {
   int k = 0, level = 0, m = 0, n = 0;
-  int64_t dims[3][3]{};  // dims[c][axis]
+  int zlo = 0, zhi = 0;
+  int64_t dims[3][3]{};  // dims[c][axis] of the held part
+  int64_t plane[4]{};    // elements per z node plane of each block
   int64_t off[4]{};
   int64_t size[4]{};
   int64_t total = 0;
   LevelLayout() = default;
-  LevelLayout(int kk, int lvl) : k(kk), level(lvl) {
+  LevelLayout(int kk, int lvl) : LevelLayout(kk, lvl, 0, 2 << lvl) {}
+  LevelLayout(int kk, int lvl, int z_lo, int z_hi) : k(kk), level(lvl), zlo(z_lo), zhi(z_hi) {
     if (kk < 1) throw std::invalid_argument("degree must be >= 1");
     if (lvl < 0 || lvl > 12) throw std::invalid_argument("level out of range");
     m = 2 << lvl;
     n = m * (k + 1);
+    if (zlo < 0 || zhi > m || zlo >= zhi) throw std::invalid_argument("slab cell range out of range");
+    const int64_t nz = static_cast<int64_t>(zhi - zlo) * (k + 1);
     int64_t o = 0;
     for (int c = 0; c < 3; ++c) {
-      for (int a = 0; a < 3; ++a) dims[c][a] = a == c ? n + 1 : n;
+      for (int a = 0; a < 2; ++a) dims[c][a] = a == c ? n + 1 : n;
+      dims[c][2] = c == 2 ? nz + 1 : nz;
+      plane[c] = dims[c][0] * dims[c][1];
       off[c] = o;
       size[c] = dims[c][0] * dims[c][1] * dims[c][2];
       o += size[c];
     }
     off[3] = o;
-    size[3] = static_cast<int64_t>(n) * n * n;
+    plane[3] = static_cast<int64_t>(n) * n;
+    size[3] = plane[3] * nz;
     total = o + size[3];
   }
+};
+
+// operator launch on a (slab) level vector: held cells [zlo, zhi), owned (computed) cells [z0, z1)
+struct VmultArgs {
+  void* y;
+  const void* x;
+  const void* b;  // residual r = b - A x if not null
+  bool slab;
+  int zlo, zhi, z0, z1;
 };
 
 // Device-resident constant data of one level in one precision.
@@ -65,9 +84,12 @@ struct DevLevel {
 
 struct TmapKey {
   const void* ptr;
-  int level, esize;
+  int level, esize, zlo;
   bool operator<(const TmapKey& o) const {
-    return ptr != o.ptr ? ptr < o.ptr : (level != o.level ? level < o.level : esize < o.esize);
+    if (ptr != o.ptr) return ptr < o.ptr;
+    if (level != o.level) return level < o.level;
+    if (esize != o.esize) return esize < o.esize;
+    return zlo < o.zlo;
   }
 };
 
@@ -109,11 +131,16 @@ void upload_reference_tables();  // __constant__ reference-cell blocks (vmult.cu
 
 // ---- launchers (stream-ordered) ----
 void launch_vmult(Context& c, int level, int prec, void* y, const void* x, const void* b /*residual if !null*/);
+// z-slab operator: x, y (, b) hold the cells [max(z0-1,0), min(z1+1,m)) in the slab layout; computes
+// the rows of the owned cells [z0, z1) (ghost layers must be current in x)
+void launch_vmult_slab(Context& c, int level, int prec, void* y, const void* x, const void* b, int z0, int z1);
 void launch_smooth_colour(Context& c, int level, int prec, int colour, void* x, const void* r);
 void launch_prolongate_add(Context& c, int coarse_level, int prec, void* xf, const void* xc);
 void launch_restrict(Context& c, int coarse_level, int prec, void* rc, const void* rf);
 void launch_coarse_apply(Context& c, int prec, void* x, const void* b);
 double dot(Context& c, int64_t n, int prec, const void* a, const void* b);
+double dot_ranges(Context& c, int prec, const void* a, const void* b, const int64_t* begin, const int64_t* len,
+                  int nranges);
 void launch_axpy(Context& c, int64_t n, int prec, double alpha, const void* x, void* y);
 void launch_axpby(Context& c, int64_t n, int prec, double alpha, const void* x, double beta, void* y);
 void launch_convert(Context& c, int64_t n, int dst_prec, void* dst, int src_prec, const void* src);

@@ -3,6 +3,8 @@
 // are deterministic run to run.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "smg_internal.cuh"
 
 namespace smg {
@@ -137,6 +139,37 @@ double dot(Context& c, int64_t n, int prec, const void* a, const void* b) {
                                                              static_cast<const float*>(b), n, part);
   dot_final_kernel<<<1, 1024, 0, c.stream>>>(part, g, part + kDotBlocks);
   c.launches += 2;
+  SMG_CUDA(cudaGetLastError());
+  double* h = static_cast<double*>(c.dot_host);
+  SMG_CUDA(cudaMemcpyAsync(h, part + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  SMG_CUDA(cudaStreamSynchronize(c.stream));
+  return h[0];
+}
+
+// dot over several contiguous index ranges of the same two vectors (the owned part of a z-slab)
+double dot_ranges(Context& c, int prec, const void* a, const void* b, const int64_t* begin, const int64_t* len,
+                  int nranges) {
+  double* part = static_cast<double*>(c.dot_partials);
+  const size_t es = elem_size(prec);
+  const int per = kDotBlocks / 4;
+  int used = 0;
+  for (int r = 0; r < nranges && r < 4; ++r) {
+    if (len[r] <= 0) continue;
+    const int g = std::min(grid_for(len[r]), per);
+    const char* pa = static_cast<const char*>(a) + begin[r] * es;
+    const char* pb = static_cast<const char*>(b) + begin[r] * es;
+    if (prec == SMG_F64)
+      dot_partial_kernel<double><<<g, kThreads, 0, c.stream>>>(reinterpret_cast<const double*>(pa),
+                                                                reinterpret_cast<const double*>(pb), len[r], part + used);
+    else
+      dot_partial_kernel<float><<<g, kThreads, 0, c.stream>>>(reinterpret_cast<const float*>(pa),
+                                                               reinterpret_cast<const float*>(pb), len[r], part + used);
+    used += g;
+    ++c.launches;
+  }
+  if (used == 0) return 0.0;
+  dot_final_kernel<<<1, 1024, 0, c.stream>>>(part, used, part + kDotBlocks);
+  ++c.launches;
   SMG_CUDA(cudaGetLastError());
   double* h = static_cast<double*>(c.dot_host);
   SMG_CUDA(cudaMemcpyAsync(h, part + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost, c.stream));

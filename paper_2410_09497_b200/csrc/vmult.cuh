@@ -5,7 +5,7 @@
 
 namespace smg {
 template <int K>
-void vmult_launch_k(Context& ctx, int level, int prec, void* y, const void* x, const void* b);
+void vmult_launch_k(Context& ctx, int level, int prec, const VmultArgs& a);
 template <int K>
 void vmult_upload_k(const double* t, const float* f);
 }  // namespace smg

@@ -148,8 +148,18 @@ struct Maps {
   CUtensorMap u0, u1, u2, p;  // u0 unused (u_x rows are bulk copies); 3D boxes of u_y, u_z, p
 };
 
+// per-block base pointers [u_x, u_y, u_z, p] in the GLOBAL index space of the level: for a z-slab
+// vector the bases are virtual (shifted back by the slab's first plane), so the kernel
+// indexes globally and only ever touches planes the slab holds.
+template <typename T>
+struct Blocks {
+  T* c[4];
+};
+
 struct Geo {
   int m, n;
+  int nlim[3];  // exclusive node limit of the outputs per axis (n, n, z_end * H)
+  int mlim[3];  // exclusive cell limit per axis (m, m, z_end)
   int c0[3];  // brick cell origin
   int g0[3];  // brick node origin
 };
@@ -225,7 +235,7 @@ __device__ __forceinline__ int row_shift0(const Geo& G, int H, int y) {
 // i.e. fp32 on level 0 with even k). Both write the same TMA box layout.
 // ---------------------------------------------------------------------------------------------
 template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, int C, bool TMA>
-__device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restrict__ x, const Maps& M, const Geo& G) {
+__device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const T>& X, const Maps& M, const Geo& G) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   constexpr int UX = BR::UX(C), UY = BR::UY(C), UZ = BR::UZ(C);
@@ -247,7 +257,7 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restric
             const int64_t sal = start >= 0 ? start / BR::VEC * BR::VEC : -((-start + BR::VEC - 1) / BR::VEC) * BR::VEC;
             const int64_t ss = sal > 0 ? sal : 0;
             const unsigned nb = static_cast<unsigned>((UX - (ss - sal)) * sizeof(T));
-            bulk_load(dst + (ss - sal), x + ss, nb, bar);
+            bulk_load(dst + (ss - sal), X.c[0] + ss, nb, bar);
             bytes += nb;
           } else {
 #pragma unroll
@@ -269,7 +279,7 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restric
   } else {
     int gd[3] = {n, n, n};
     gd[C] = n + 1;
-    const T* xc = x + C * (static_cast<int64_t>(n + 1) * n * n);
+    const T* xc = X.c[C];
     constexpr int XE = BR::XEXT(C);
     for (int i = tid; i < XE * UY * UZ; i += NT) {
       const int l[3] = {i % XE - H, (i / XE) % UY - H, i / (XE * UY) - H};
@@ -284,7 +294,7 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const T* __restric
 }
 
 template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, bool TMA>
-__device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const T* __restrict__ x, const Maps& M, const Geo& G) {
+__device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const Blocks<const T>& X, const Maps& M, const Geo& G) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   if constexpr (TMA) {
@@ -297,7 +307,7 @@ __device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const T* __restric
     constexpr int E0 = BR::N(0) + H, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
     const int n = G.n;
     const int sh = brick_shift<T>(G, H);
-    const T* xp = x + 3 * (static_cast<int64_t>(n + 1) * n * n);
+    const T* xp = X.c[3];
     for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
       const int lx = i % E0, ly = (i / E0) % E1, lz = i / (E0 * E1);
       const int gx = G.g0[0] + lx - H, gy = G.g0[1] + ly - H, gz = G.g0[2] + lz - H;
@@ -389,8 +399,8 @@ __device__ __forceinline__ void cell_sipg(const T (&pv)[K + 1], const T (&cu)[K 
 // the passes stay balanced and the dependency chains short (v5; v2-v4 used one thread per line).
 // ---------------------------------------------------------------------------------------------
 template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, int C, bool RESID, bool TMA>
-__device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const Geo* Gn, const T* __restrict__ x,
-                                          T* __restrict__ y, const T* __restrict__ b, const Maps& M, uint64_t* barP) {
+__device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const Geo* Gn, const Blocks<const T>& X,
+                                          const Blocks<T>& Y, const Blocks<const T>& B, const Maps& M, uint64_t* barP) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   using R = Ref<K>;
   constexpr int H = K + 1, P = K + 2;
@@ -401,7 +411,6 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
   constexpr int UX = BR::UX(C), UY = BR::UY(C);
   const int tid = threadIdx.x;
   const int n = G.n, m = G.m;
-  const int64_t sizeV = static_cast<int64_t>(n + 1) * n * n;
   int64_t gd[3] = {n, n, n};
   gd[C] = n + 1;
   const int64_t st[3] = {1, gd[0], gd[0] * gd[1]};
@@ -437,7 +446,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
     }
     fence_proxy_async();
     __syncthreads();
-    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, barP, x, M, *Gn);
+    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, barP, X, M, *Gn);
     if (!TMA && C == 2) cp_async_commit();
     // Q = M_o1 Q2
     constexpr int NL2 = (Nc + H) * No2;
@@ -531,8 +540,8 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
   T* sYC = sA1;  // C = 0: outputs staged in smem (A1 is dead) for a coalesced x-row write-out
   {
     const T h2 = h * h;
-    const T* __restrict__ bc = RESID ? b + C * sizeV : nullptr;
-    T* __restrict__ yc = y + C * sizeV;
+    const T* __restrict__ bc = RESID ? B.c[C] : nullptr;
+    T* __restrict__ yc = Y.c[C];
     constexpr int YSC = BR::stride(C, BR::YX, BR::N(1)), YSO1 = BR::stride(O1, BR::YX, BR::N(1)),
                   YSO2 = BR::stride(O2, BR::YX, BR::N(1));
     constexpr int NL = No1 * No2;
@@ -551,7 +560,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       int g[3];
       g[O1] = G.g0[O1] + oi;
       g[O2] = G.g0[O2] + oj;
-      const bool inside = g[O1] < n && g[O2] < n;
+      const bool inside = g[O1] < G.nlim[O1] && g[O2] < G.nlim[O2];
 #pragma unroll
       for (int a = 0; a < H; ++a) {
         T v = T(0), w = T(0);
@@ -570,7 +579,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
           sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
         } else {
           g[C] = G.g0[C] + e * H + a;
-          if (inside && g[C] < n) {
+          if (inside && g[C] < G.nlim[C]) {
             const int64_t gi = g[0] * st[0] + g[1] * st[1] + g[2] * st[2];
             T rr = val;
             if (g[C] == 0) rr = T(0);  // constrained boundary-normal row
@@ -589,7 +598,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         yp[(e * H + i) * YSC] += h2 * z;
       }
       // the constrained plane g_c = n belongs to the brick holding the last cell along c
-      if (C != 0 && e == NCc - 1 && inside && G.c0[C] + NCc >= m) {
+      if (C != 0 && e == NCc - 1 && inside && G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
         g[C] = n;
         yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
       }
@@ -603,7 +612,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         const int lx = i % (Nc + 1), r = i / (Nc + 1);
         const int ly = r % No1, lz = r / No1;
         const int gx = G.g0[0] + lx, gy = G.g0[1] + ly, gz = G.g0[2] + lz;
-        if (gy >= n || gz >= n || gx > n) continue;
+        if (gy >= G.nlim[1] || gz >= G.nlim[2] || gx > n) continue;
         if (lx == Nc && !(last && gx == n)) continue;
         const int64_t gi = (static_cast<int64_t>(gz) * n + gy) * (n + 1) + gx;
         T rr;
@@ -622,26 +631,25 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
 
 // write the pressure rows of this brick from the smem accumulator
 template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, bool RESID>
-__device__ __forceinline__ void write_pressure(const T* sYP, const Geo& G, T* __restrict__ y, const T* __restrict__ b,
-                                               int64_t offP) {
+__device__ __forceinline__ void write_pressure(const T* sYP, const Geo& G, T* __restrict__ y, const T* __restrict__ b) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int N0 = BR::N(0), N1 = BR::N(1), N2 = BR::N(2);
   const int n = G.n;
   for (int i = threadIdx.x; i < N0 * N1 * N2; i += NT) {
     const int lx = i % N0, ly = (i / N0) % N1, lz = i / (N0 * N1);
     const int gx = G.g0[0] + lx, gy = G.g0[1] + ly, gz = G.g0[2] + lz;
-    if (gx >= n || gy >= n || gz >= n) continue;
-    const int64_t gi = offP + (static_cast<int64_t>(gz) * n + gy) * n + gx;
+    if (gx >= n || gy >= G.nlim[1] || gz >= G.nlim[2]) continue;
+    const int64_t gi = (static_cast<int64_t>(gz) * n + gy) * n + gx;
     const T v = sYP[(lz * N1 + ly) * BR::YX + lx];
     y[gi] = RESID ? b[gi] - v : v;
   }
 }
 
-__device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, int bx, int by, int bz, int H) {
+__device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, int bx, int by, int bz, int H, int zc0) {
   const int ix = brick % nbx, iy = (brick / nbx) % nby, iz = brick / (nbx * nby);
   G.c0[0] = ix * bx;
   G.c0[1] = iy * by;
-  G.c0[2] = iz * bz;
+  G.c0[2] = zc0 + iz * bz;
   for (int a = 0; a < 3; ++a) G.g0[a] = G.c0[a] * H;
 }
 
@@ -650,21 +658,28 @@ __device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, i
 // the TMA staging of the next component -- and of the next brick's first component and pressure
 // box -- overlaps compute.
 template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, bool RESID, bool TMA>
-__global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const T* __restrict__ x, T* __restrict__ y,
-                                                             const T* __restrict__ b, int m, T h,
+__global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<const T> X, const Blocks<T> Y,
+                                                             const Blocks<const T> B, int m, int zc0, int zc1, T h,
                                                              const Maps* __restrict__ mapsp) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (BR::BYTES - 3 * 8));  // [buf0, buf1, P]
-  const int nbx = (m + BX - 1) / BX, nby = (m + BY - 1) / BY, nbz = (m + BZ - 1) / BZ;
+  // bricks cover the cells [0, m)^2 x [zc0, zc1) (the whole level, or the cells a z-slab owns)
+  const int nbx = (m + BX - 1) / BX, nby = (m + BY - 1) / BY, nbz = (zc1 - zc0 + BZ - 1) / BZ;
   const int nbricks = nbx * nby * nbz;
   Geo G, Gn;
   G.m = Gn.m = m;
   G.n = Gn.n = m * H;
-  const int n = G.n;
-  const int64_t offP = 3 * static_cast<int64_t>(n + 1) * n * n;
+  G.nlim[0] = G.nlim[1] = G.n;
+  G.nlim[2] = zc1 * H;
+  G.mlim[0] = G.mlim[1] = m;
+  G.mlim[2] = zc1;
+  for (int a = 0; a < 3; ++a) {
+    Gn.nlim[a] = G.nlim[a];
+    Gn.mlim[a] = G.mlim[a];
+  }
   T* sP = sm + BR::OFF_P;
   T* sYP = sm + BR::OFF_YP;
   const Maps& maps = *mapsp;  // tensor maps live in global memory (64-B aligned slots)
@@ -678,9 +693,9 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const T* __restri
   }
   fence_proxy_async();
   __syncthreads();
-  brick_geo(G, brick, nbx, nby, BX, BY, BZ, H);
-  issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, &bars[2], x, maps, G);
-  issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sm, &bars[0], x, maps, G);
+  brick_geo(G, brick, nbx, nby, BX, BY, BZ, H, zc0);
+  issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, &bars[2], X, maps, G);
+  issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sm, &bars[0], X, maps, G);
   if (!TMA) cp_async_commit();
   int u0 = 0;
   unsigned ph[2] = {0, 0}, phP = 0;  // mbarrier phase of buffer 0 / 1 / P
@@ -703,32 +718,32 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const T* __restri
     for (; brick < nbricks; brick += gridDim.x) {
       const int next = brick + gridDim.x;
       const bool has_next = next < nbricks;
-      if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H);
+      if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H, zc0);
       for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
       wait_u(true);
       if (TMA) {
         fix_columns<T, K, BX, BY, BZ, OCC, NT>(sm, nullptr, nullptr, sP, G);
         __syncthreads();
       }
-      component<T, K, BX, BY, BZ, OCC, NT, 0, RESID, TMA>(sm, sm, G, h, nullptr, x, y, b, maps, &bars[2]);
-      issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA>(sm, &bars[0], x, maps, G);
+      component<T, K, BX, BY, BZ, OCC, NT, 0, RESID, TMA>(sm, sm, G, h, nullptr, X, Y, B, maps, &bars[2]);
+      issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA>(sm, &bars[0], X, maps, G);
       wait_u(false);
       if (TMA) {
         fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, sm, nullptr, nullptr, G);
         __syncthreads();
       }
-      component<T, K, BX, BY, BZ, OCC, NT, 1, RESID, TMA>(sm, sm, G, h, nullptr, x, y, b, maps, &bars[2]);
-      issue_u<T, K, BX, BY, BZ, OCC, NT, 2, TMA>(sm, &bars[0], x, maps, G);
+      component<T, K, BX, BY, BZ, OCC, NT, 1, RESID, TMA>(sm, sm, G, h, nullptr, X, Y, B, maps, &bars[2]);
+      issue_u<T, K, BX, BY, BZ, OCC, NT, 2, TMA>(sm, &bars[0], X, maps, G);
       wait_u(false);
       if (TMA) {
         fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, nullptr, sm, nullptr, G);
         __syncthreads();
       }
-      component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, sm, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
+      component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, sm, G, h, has_next ? &Gn : nullptr, X, Y, B, maps,
                                                      &bars[2]);
-      write_pressure<T, K, BX, BY, BZ, OCC, NT, RESID>(sYP, G, y, b, offP);
+      write_pressure<T, K, BX, BY, BZ, OCC, NT, RESID>(sYP, G, Y.c[3], RESID ? B.c[3] : nullptr);
       __syncthreads();
-      if (has_next) issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sm, &bars[0], x, maps, Gn);
+      if (has_next) issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sm, &bars[0], X, maps, Gn);
       G = Gn;
     }
     if (!TMA) cp_async_wait<0>();
@@ -739,8 +754,8 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const T* __restri
     T* bufB = sm + (ib ? BR::OFF_U1 : 0);  // component 1, then component 0 of the next brick
     const int next = brick + gridDim.x;
     const bool has_next = next < nbricks;
-    if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H);
-    issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA>(bufB, &bars[ib], x, maps, G);
+    if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H, zc0);
+    issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA>(bufB, &bars[ib], X, maps, G);
     for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
     if (TMA) {
       mbar_wait(&bars[2], phP);
@@ -756,8 +771,8 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const T* __restri
       fix_columns<T, K, BX, BY, BZ, OCC, NT>(bufA, nullptr, nullptr, sP, G);
       __syncthreads();
     }
-    component<T, K, BX, BY, BZ, OCC, NT, 0, RESID, TMA>(sm, bufA, G, h, nullptr, x, y, b, maps, &bars[2]);
-    issue_u<T, K, BX, BY, BZ, OCC, NT, 2, TMA>(bufA, &bars[ia], x, maps, G);
+    component<T, K, BX, BY, BZ, OCC, NT, 0, RESID, TMA>(sm, bufA, G, h, nullptr, X, Y, B, maps, &bars[2]);
+    issue_u<T, K, BX, BY, BZ, OCC, NT, 2, TMA>(bufA, &bars[ia], X, maps, G);
     if (TMA) {
       mbar_wait(&bars[ib], ph[ib]);
       ph[ib] ^= 1;
@@ -770,8 +785,8 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const T* __restri
       fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, bufB, nullptr, nullptr, G);
       __syncthreads();
     }
-    component<T, K, BX, BY, BZ, OCC, NT, 1, RESID, TMA>(sm, bufB, G, h, nullptr, x, y, b, maps, &bars[2]);
-    if (has_next) issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(bufB, &bars[ib], x, maps, Gn);
+    component<T, K, BX, BY, BZ, OCC, NT, 1, RESID, TMA>(sm, bufB, G, h, nullptr, X, Y, B, maps, &bars[2]);
+    if (has_next) issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(bufB, &bars[ib], X, maps, Gn);
     if (TMA) {
       mbar_wait(&bars[ia], ph[ia]);
       ph[ia] ^= 1;
@@ -784,9 +799,9 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const T* __restri
       fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, nullptr, bufA, nullptr, G);
       __syncthreads();
     }
-    component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, x, y, b, maps,
+    component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, X, Y, B, maps,
                                                    &bars[2]);
-    write_pressure<T, K, BX, BY, BZ, OCC, NT, RESID>(sYP, G, y, b, offP);
+    write_pressure<T, K, BX, BY, BZ, OCC, NT, RESID>(sYP, G, Y.c[3], RESID ? B.c[3] : nullptr);
     __syncthreads();  // y_p accumulator is re-zeroed by the next brick
     G = Gn;
     u0 ^= 1;
@@ -837,63 +852,86 @@ bool tma_ok(int n) {
 }
 
 template <typename T, int K, int BX, int BY, int BZ, int OCC>
-Maps make_maps(const T* x, int n) {
+Maps make_maps(const Blocks<const T>& X, int n) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   Maps M;
   std::memset(&M, 0, sizeof(M));
   const uint64_t es = sizeof(T);
   const uint64_t nn = static_cast<uint64_t>(n);
-  const uint64_t sizeV = (nn + 1) * nn * nn;
+  // global-index maps over (virtual) block bases; a slab only ever addresses the planes it holds
   // u_x rows have the odd pitch n+1 (not a legal TMA stride): staged by non-tensor bulk copies
   {  // u_y: dims (x n, y n+1, z n); base one row in -> y' = y - 1 in [0, n-1)
     const uint64_t d[3] = {nn, nn - 1, nn};
     const uint64_t s[2] = {nn * es, nn * (nn + 1) * es};
     const uint32_t box[3] = {static_cast<uint32_t>(BR::UX(1)), static_cast<uint32_t>(BR::UY(1)),
                              static_cast<uint32_t>(BR::UZ(1))};
-    encode<T>(&M.u1, x + sizeV + nn, 3, d, s, box);
+    encode<T>(&M.u1, X.c[1] + nn, 3, d, s, box);
   }
   {  // u_z: dims (x n, y n, z n+1); base one plane in -> z' = z - 1 in [0, n-1)
     const uint64_t d[3] = {nn, nn, nn - 1};
     const uint64_t s[2] = {nn * es, nn * nn * es};
     const uint32_t box[3] = {static_cast<uint32_t>(BR::UX(2)), static_cast<uint32_t>(BR::UY(2)),
                              static_cast<uint32_t>(BR::UZ(2))};
-    encode<T>(&M.u2, x + 2 * sizeV + nn * nn, 3, d, s, box);
+    encode<T>(&M.u2, X.c[2] + nn * nn, 3, d, s, box);
   }
   {  // p
     const uint64_t d[3] = {nn, nn, nn};
     const uint64_t s[2] = {nn * es, nn * nn * es};
     const uint32_t box[3] = {static_cast<uint32_t>(BR::PXT), static_cast<uint32_t>(BR::N(1) + H),
                              static_cast<uint32_t>(BR::N(2) + H)};
-    encode<T>(&M.p, x + 3 * sizeV, 3, d, s, box);
+    encode<T>(&M.p, X.c[3], 3, d, s, box);
   }
   return M;
 }
 
+// virtual global-index bases of the four blocks of a (slab) level vector
+template <typename T>
+Blocks<T> block_bases(const LevelLayout& lay, T* v) {
+  Blocks<T> B;
+  const int H = lay.k + 1;
+  for (int c = 0; c < 4; ++c) B.c[c] = v ? v + lay.off[c] - static_cast<int64_t>(lay.zlo) * H * lay.plane[c] : nullptr;
+  return B;
+}
+
 template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT>
-void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
+void launch_t(Context& ctx, int level, const VmultArgs& a) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
-  const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
-  const int m = dl.lay.m, n = dl.lay.n;
+  const int m = ctx.dev[0][level].lay.m, n = ctx.dev[0][level].lay.n;
+  const LevelLayout lay = a.slab ? LevelLayout(K, level, a.zlo, a.zhi) : ctx.dev[0][level].lay;
+  if (a.slab) {
+    // the owned range must be whole bricks unless it ends at the domain top (bricks never read past
+    // the planes a slab holds), and the slab must hold one ghost cell beyond each interior end
+    if (a.z0 < 0 || a.z1 > m || a.z0 >= a.z1 || a.zlo != std::max(a.z0 - 1, 0) || a.zhi != std::min(a.z1 + 1, m))
+      throw std::invalid_argument("slab: held cells must be the owned cells plus one ghost cell per interior side");
+    if (a.z1 < m && (a.z1 - a.z0) % BZ != 0)
+      throw std::invalid_argument("slab: owned cell range must be a multiple of the brick depth (" + std::to_string(BZ) +
+                                  ") unless it ends at the top of the domain");
+  }
+  const Blocks<const T> X = block_bases(lay, static_cast<const T*>(a.x));
+  const Blocks<T> Y = block_bases(lay, static_cast<T*>(a.y));
+  const Blocks<const T> B = block_bases(lay, static_cast<const T*>(a.b));
   const T h = static_cast<T>(1.0 / m);
-  const int nbricks = ((m + BX - 1) / BX) * ((m + BY - 1) / BY) * ((m + BZ - 1) / BZ);
+  const int nbricks = ((m + BX - 1) / BX) * ((m + BY - 1) / BY) * ((a.z1 - a.z0 + BZ - 1) / BZ);
   static int num_sms = 0;
   if (num_sms == 0) SMG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ctx.device));
   const dim3 grid(std::min(nbricks, OCC * num_sms));
   const size_t smem = BR::BYTES;
   static const bool no_tma = std::getenv("SMG_NO_TMA") != nullptr;  // diagnostics: force the cp.async path
-  const bool tma = !no_tma && tma_ok<T, K, BX, BY, BZ, OCC>(n) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  bool aligned = true;
+  for (int c = 0; c < 4; ++c) aligned = aligned && reinterpret_cast<uintptr_t>(X.c[c]) % 16 == 0;
+  const bool tma = !no_tma && tma_ok<T, K, BX, BY, BZ, OCC>(n) && aligned;
   const Maps* dmaps = nullptr;
   if (tma) {
-    // tensor maps are cached per (input vector, level, precision) in 64-B aligned global slots,
-    // written stream-ordered before the launch
-    const TmapKey key{x, level, static_cast<int>(sizeof(T))};
+    // tensor maps are cached per (input vector, slab, level, precision) in 64-B aligned global
+    // slots, written stream-ordered before the launch
+    const TmapKey key{a.x, level, static_cast<int>(sizeof(T)), a.zlo};
     auto it = ctx.tmap_slots.find(key);
     if (it == ctx.tmap_slots.end()) {
       const int slot = ctx.tmap_next++ % kTmapSlots;
       for (auto e = ctx.tmap_slots.begin(); e != ctx.tmap_slots.end();)
         e = (e->second == slot) ? ctx.tmap_slots.erase(e) : std::next(e);
-      Maps mh = make_maps<T, K, BX, BY, BZ, OCC>(static_cast<const T*>(x), n);
+      Maps mh = make_maps<T, K, BX, BY, BZ, OCC>(X, n);
       char* dst = static_cast<char*>(ctx.tmap_dev) + static_cast<size_t>(slot) * kTmapSlotBytes;
       SMG_CUDA(cudaMemcpyAsync(dst, &mh, sizeof(Maps), cudaMemcpyHostToDevice, ctx.stream));
       SMG_CUDA(cudaStreamSynchronize(ctx.stream));  // mh is a stack temporary
@@ -904,11 +942,14 @@ void launch_t(Context& ctx, int level, void* y, const void* x, const void* b) {
   }
   static_assert(sizeof(Maps) <= kTmapSlotBytes, "tensor-map slot too small");
   auto go = [&](auto kern) {
-    SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, NT, smem, ctx.stream>>>(static_cast<const T*>(x), static_cast<T*>(y), static_cast<const T*>(b), m, h,
-                                         dmaps);
+    static bool attr_set = false;  // one instantiation per lambda call site / kernel
+    if (!attr_set) {
+      SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      attr_set = true;
+    }
+    kern<<<grid, NT, smem, ctx.stream>>>(X, Y, B, m, a.z0, a.z1, h, dmaps);
   };
-  if (b) {
+  if (a.b) {
     if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, OCC, NT, true, true>);
     else go(stokes_vmult_kernel<T, K, BX, BY, BZ, OCC, NT, true, false>);
   } else {
@@ -936,10 +977,10 @@ template <> struct BrickShape<double, 7> { static constexpr int X = 1, Y = 1, Z 
 template <> struct BrickShape<float, 7> { static constexpr int X = 2, Y = 1, Z = 1, NT = 256, OCC = 1; };
 
 template <typename T, int K, class S>
-void launch_shape(Context& ctx, int level, void* y, const void* x, const void* b) {
+void launch_shape(Context& ctx, int level, const VmultArgs& a) {
   static_assert(Brick<T, K, S::X, S::Y, S::Z, S::OCC>::BYTES <= (S::OCC == 1 ? 232448 : 233472 / S::OCC - 1024),
                 "brick exceeds the shared memory of its occupancy");
-  launch_t<T, K, S::X, S::Y, S::Z, S::OCC, S::NT>(ctx, level, y, x, b);
+  launch_t<T, K, S::X, S::Y, S::Z, S::OCC, S::NT>(ctx, level, a);
 }
 
 #ifdef SMG_TUNE
@@ -947,31 +988,31 @@ void launch_shape(Context& ctx, int level, void* y, const void* x, const void* b
 template <int X_, int Y_, int Z_, int NT_, int OCC_>
 struct Shape { static constexpr int X = X_, Y = Y_, Z = Z_, NT = NT_, OCC = OCC_; };
 template <typename T, int K>
-bool launch_variant(int v, Context& ctx, int level, void* y, const void* x, const void* b) {
+bool launch_variant(int v, Context& ctx, int level, const VmultArgs& a) {
   switch (v) {
-    case 1: launch_shape<T, K, Shape<4, 4, 2, 256, 2>>(ctx, level, y, x, b); return true;
-    case 2: launch_shape<T, K, Shape<4, 2, 2, 256, 2>>(ctx, level, y, x, b); return true;
-    case 3: launch_shape<T, K, Shape<2, 2, 2, 128, 4>>(ctx, level, y, x, b); return true;
-    case 4: launch_shape<T, K, Shape<4, 4, 2, 384, 2>>(ctx, level, y, x, b); return true;
-    case 5: launch_shape<T, K, Shape<8, 2, 2, 256, 2>>(ctx, level, y, x, b); return true;
-    case 6: launch_shape<T, K, Shape<4, 2, 2, 128, 3>>(ctx, level, y, x, b); return true;
+    case 1: launch_shape<T, K, Shape<4, 4, 2, 256, 2>>(ctx, level, a); return true;
+    case 2: launch_shape<T, K, Shape<4, 2, 2, 256, 2>>(ctx, level, a); return true;
+    case 3: launch_shape<T, K, Shape<2, 2, 2, 128, 4>>(ctx, level, a); return true;
+    case 4: launch_shape<T, K, Shape<4, 4, 2, 384, 2>>(ctx, level, a); return true;
+    case 5: launch_shape<T, K, Shape<8, 2, 2, 256, 2>>(ctx, level, a); return true;
+    case 6: launch_shape<T, K, Shape<4, 2, 2, 128, 3>>(ctx, level, a); return true;
     default: return false;
   }
 }
 #endif
 
 template <int K>
-void vmult_launch_k(Context& ctx, int level, int prec, void* y, const void* x, const void* b) {
+void vmult_launch_k(Context& ctx, int level, int prec, const VmultArgs& a) {
 #ifdef SMG_TUNE
   static const int variant = std::getenv("SMG_VMULT_VARIANT") ? std::atoi(std::getenv("SMG_VMULT_VARIANT")) : 0;
   if (K == 2 && variant > 0) {
-    if (prec == SMG_F64 ? launch_variant<double, K>(variant, ctx, level, y, x, b)
-                        : launch_variant<float, K>(variant, ctx, level, y, x, b))
+    if (prec == SMG_F64 ? launch_variant<double, K>(variant, ctx, level, a)
+                        : launch_variant<float, K>(variant, ctx, level, a))
       return;
   }
 #endif
-  if (prec == SMG_F64) launch_shape<double, K, BrickShape<double, K>>(ctx, level, y, x, b);
-  else launch_shape<float, K, BrickShape<float, K>>(ctx, level, y, x, b);
+  if (prec == SMG_F64) launch_shape<double, K, BrickShape<double, K>>(ctx, level, a);
+  else launch_shape<float, K, BrickShape<float, K>>(ctx, level, a);
 }
 
 template <int K>
@@ -981,7 +1022,7 @@ void vmult_upload_k(const double* t, const float* f) {
 }
 
 #define SMG_INSTANTIATE_VMULT(K)                                                                  \
-  template void vmult_launch_k<K>(Context&, int, int, void*, const void*, const void*);           \
+  template void vmult_launch_k<K>(Context&, int, int, const VmultArgs&);           \
   template void vmult_upload_k<K>(const double*, const float*);
 
 }  // namespace smg
