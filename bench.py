@@ -7,9 +7,10 @@ the CPU baseline on this box's host cores. Prints ONE JSON line on rank 0.
 Workload (configs[1] of BASELINE.json, the largest config that fits one GPU and that the metric is
 quoted on): 3D unit-cube Stokes, RT_2 velocity / DGQ_2 pressure, 64^3 cells (level 5), 28.4 M DoF.
 Each step is one fp64 operator apply y = A x; x and y are 227 MB each (> 126 MB L2), so no L2 flush
-is needed between steps. Under torchrun each rank runs the same workload on its own GPU (weak
-scaling, no data-path collective yet: the slab-partitioned multi-GPU operator is future work, see
-DESIGN.md §Multi-GPU); value = all DoF processed / max-over-ranks time.
+is needed between steps. Under torchrun (N > 1) the SAME global problem is split into N z-slabs, one
+per GPU (strong scaling): each step is the ghost-layer exchange over NCCL (P2P send/recv of one cell
+layer per neighbour and block) followed by the slab operator; value = global DoF / max-over-ranks
+step time. The smoother and the MG solve are single-GPU in round 1 (reported at N = 1 only).
 """
 import argparse
 import json
@@ -168,6 +169,8 @@ def main():
     ap.add_argument("--level", type=int, default=LEVEL)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to test the multi-rank "
+                    "logic on a single-GPU box (CPU-staged exchange, timings meaningless)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -181,11 +184,12 @@ def main():
 
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(args.dist_backend)
 
     def barrier():
         if dist:
@@ -195,120 +199,150 @@ def main():
     def max_over_ranks(v):
         if not dist:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64, device="cuda" if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     k, level = args.degree, args.level
     N = dofs(k, level)
     ctx = smg.Context(k, level, device=local, cg_max_iter=30, cg_tol=1e-5, cg_fixed=False, cg_precond=1)
-    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    g = torch.Generator(device="cuda").manual_seed(1234)
     x = torch.rand(N, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
-    y = torch.empty_like(x)
     stream = torch.cuda.current_stream()
-
-    # ---- headline: fp64 vmult, inputs resident in HBM ----
-    for _ in range(args.warmup):
-        ctx.apply_stokes(level, x, out=y)
-    barrier()
-    l0 = ctx.launch_count
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+
+    def timed(fn, steps, clocks=False):
+        for _ in range(args.warmup):
+            fn()
+        barrier()
+        sampler = ClockSampler(local) if clocks else None
+        if sampler:
+            sampler.__enter__()
         ev0.record(stream)
-        for _ in range(args.steps):
-            ctx.apply_stokes(level, x, out=y)
+        for _ in range(steps):
+            fn()
         ev1.record(stream)
         torch.cuda.synchronize()
-    barrier()
-    launches = ctx.launch_count - l0
-    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    value = N * world / (ms * 1e-3)
+        if sampler:
+            sampler.__exit__(None, None, None)
+        barrier()
+        return max_over_ranks(ev0.elapsed_time(ev1) / steps), sampler
 
-    # ---- fp32 vmult ----
-    x32 = x.float()
-    y32 = torch.empty_like(x32)
-    for _ in range(args.warmup):
-        ctx.apply_stokes(level, x32, out=y32)
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        ctx.apply_stokes(level, x32, out=y32)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms32 = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    extra = {}
+    if world == 1:
+        # ---- headline: fp64 vmult, inputs resident in HBM ----
+        y = torch.empty_like(x)
+        l0 = ctx.launch_count
+        ms, clk = timed(lambda: ctx.apply_stokes(level, x, out=y), args.steps, clocks=True)
+        launches = (ctx.launch_count - l0) * args.steps // (args.steps + args.warmup)
+        ms_kernel = ms
+        owned = N
 
-    # ---- fp32 smoothing step (8 colours: residual + patch solve each) ----
-    b32 = ctx.apply_stokes(level, x32)
-    xs = torch.zeros_like(b32)
-    ctx.smooth(level, xs, b32, zero_init=True)
-    torch.cuda.synchronize()
-    nsm = max(1, min(args.steps, 3))
-    ev0.record(stream)
-    for _ in range(nsm):
-        ctx.smooth(level, xs, b32, zero_init=False)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms_smooth = max_over_ranks(ev0.elapsed_time(ev1) / nsm)
+        # ---- fp32 vmult ----
+        x32 = x.float()
+        y32 = torch.empty_like(x32)
+        ms32, _ = timed(lambda: ctx.apply_stokes(level, x32, out=y32), args.steps)
+        extra["fp32_vmult"] = {"value": N / (ms32 * 1e-3), "unit": "DoF/s", "ms": ms32}
 
-    # ---- MG-FGMRES solve (mixed precision: fp64 Krylov, fp32 V-cycle) ----
-    solve = None
-    if not args.no_solve:
-        b = ctx.apply_stokes(level, x)
-        ctx.solve(level, b, 1e-8, 30, smg.F32, allow_not_converged=True)  # warm-up
-        torch.cuda.synchronize()
+        # ---- fp32 smoothing step (8 colours: residual + patch solve each) ----
+        b32 = ctx.apply_stokes(level, x32)
+        xs = torch.zeros_like(b32)
+        ms_smooth, _ = timed(lambda: ctx.smooth(level, xs, b32, zero_init=False), max(1, min(args.steps, 3)))
+        extra["smoother_fp32"] = {"value": N / (ms_smooth * 1e-3), "unit": "DoF/s", "ms_per_step": ms_smooth,
+                                  "ns_per_dof": ms_smooth * 1e6 / N}
+
+        # ---- MG-FGMRES solve (mixed precision: fp64 Krylov, fp32 V-cycle) ----
+        if not args.no_solve:
+            b = ctx.apply_stokes(level, x)
+            ctx.solve(level, b, 1e-8, 30, smg.F32, allow_not_converged=True)  # warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            xsol, it, hist = ctx.solve(level, b, 1e-8, 30, smg.F32, allow_not_converged=True)
+            torch.cuda.synchronize()
+            ts = time.perf_counter() - t0
+            nu = -8.0 / np.log10((hist[-1] / hist[0]) ** (1.0 / it)) if it > 0 and hist[-1] > 0 else None
+            extra["solve"] = {"iterations": it, "rel_residual": float(hist[-1] / hist[0]), "fractional_count_nu": nu,
+                              "time_s": ts, "ns_per_dof": ts / N * 1e9, "tol": 1e-8,
+                              "precision": "fp64 FGMRES + fp32 V-cycle"}
+
+        # ---- e2e: host BlockVector buffers through the C ABI, copies inside the timed region ----
+        s = ctx.sizes(level)
+        xbn = [torch.empty(s[i], dtype=torch.float64, pin_memory=True).numpy() for i in range(4)]
+        ybn = [torch.empty(s[i], dtype=torch.float64, pin_memory=True).numpy() for i in range(4)]
+        for i, blk in enumerate(smg.to_blockvector(x.cpu().numpy(), k, level)):
+            xbn[i][:] = blk
+        for _ in range(args.warmup):
+            ctx.vmult_host(level, xbn, smg.F64, out=ybn)
         t0 = time.perf_counter()
-        xsol, it, hist = ctx.solve(level, b, 1e-8, 30, smg.F32, allow_not_converged=True)
-        torch.cuda.synchronize()
-        ts = max_over_ranks(time.perf_counter() - t0)
-        nu = -8.0 / np.log10((hist[-1] / hist[0]) ** (1.0 / it)) if it > 0 and hist[-1] > 0 else None
-        solve = {"iterations": it, "rel_residual": float(hist[-1] / hist[0]), "fractional_count_nu": nu,
-                 "time_s": ts, "ns_per_dof": ts / N * 1e9, "tol": 1e-8, "precision": "fp64 FGMRES + fp32 V-cycle"}
+        for _ in range(args.steps):
+            ctx.vmult_host(level, xbn, smg.F64, out=ybn)
+        te = (time.perf_counter() - t0) / args.steps
+        e2e = {"value": N / te, "unit": "DoF/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
+               "path": "smg_vmult_host: BlockVector host arrays (pinned) -> H2D -> vmult -> D2H"}
+        parallelism = "single GPU"
+    else:
+        # ---- z-slab partition of the same global problem, NCCL ghost exchange per apply ----
+        from paper_2410_09497_b200 import slab
+        z0, z1 = slab.partition(level, world)[rank]
+        op = slab.SlabOperator(ctx, level, z0, z1, rank, world)
+        L = op.lay
+        xsl = L.extract(x).contiguous()
+        del x
+        torch.cuda.empty_cache()
+        ysl = op.new_vector()
+        l0 = ctx.launch_count
+        ms, clk = timed(lambda: op.vmult(ysl, xsl), args.steps, clocks=True)
+        launches = (ctx.launch_count - l0) * args.steps // (args.steps + args.warmup)
+        ms_kernel, _ = timed(lambda: op.vmult(ysl, xsl, exchange=False), args.steps)
+        owned = sum((b1 - a1) * L.plane[c] for c, (a1, b1) in enumerate(L.owned_planes(c) for c in range(4)))
+        xh = torch.empty(L.total, dtype=torch.float64, pin_memory=True)
+        yh = torch.empty(L.total, dtype=torch.float64, pin_memory=True)
+        xh.copy_(xsl)
 
-    # ---- e2e: host BlockVector buffers through the C ABI, copies inside the timed region ----
-    s = ctx.sizes(level)
-    xb = [torch.empty(s[i], dtype=torch.float64, pin_memory=True) for i in range(4)]
-    yb = [torch.empty(s[i], dtype=torch.float64, pin_memory=True) for i in range(4)]
-    off = 0
-    xh = x.cpu()
-    for i in range(4):
-        xb[i].copy_(xh[off:off + s[i]])
-        off += s[i]
-    xbn, ybn = [t.numpy() for t in xb], [t.numpy() for t in yb]
-    for _ in range(args.warmup):
-        ctx.vmult_host(level, xbn, smg.F64, out=ybn)
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        ctx.vmult_host(level, xbn, smg.F64, out=ybn)
-    te = max_over_ranks((time.perf_counter() - t0) / args.steps)
-    e2e = {"value": N * world / te, "unit": "DoF/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N}
+        def e2e_step():
+            xsl.copy_(xh, non_blocking=True)
+            op.vmult(ysl, xsl)
+            yh.copy_(ysl, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        for _ in range(args.warmup):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        te = max_over_ranks((time.perf_counter() - t0) / args.steps)
+        e2e = {"value": N / te, "unit": "DoF/s", "h2d_bytes_per_step": 8 * L.total, "d2h_bytes_per_step": 8 * L.total,
+               "path": "per rank: pinned slab -> H2D -> NCCL ghost exchange -> smg_vmult_slab -> D2H"}
+        extra["kernel_ms"] = ms_kernel
+        extra["slab"] = {"z_cells": [z0, z1], "owned_dofs": owned, "held_dofs": L.total}
+        parallelism = f"z-slabs x{world} (NCCL ghost exchange)"
+    value = N / (ms * 1e-3)
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
     peak, peak_src = measured_peaks()
-    bytes_per_launch = 16 * N  # algorithmic: read x + write y, fp64
-    achieved = bytes_per_launch / (ms * 1e-3) / 1e9
-    traffic = ncu_traffic(f"k{k}_l{level}_f64")
-    cpu = None if args.no_cpu else cpu_baseline(k, level)
+    bytes_per_launch = 16 * owned  # algorithmic: read x + write y of the owned DoF, fp64
+    achieved = bytes_per_launch / (ms_kernel * 1e-3) / 1e9
+    traffic = ncu_traffic(f"k{k}_l{level}_f64") if world == 1 else None
+    cpu = None if (args.no_cpu or world > 1) else cpu_baseline(k, level)
     out = {
         "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform random x, seed 1234)",
         "config": {"workload": f"C2: 3D unit-cube Stokes RT_{k}/DGQ_{k}, {2 << level}^3 cells (level {level}), "
                                f"fp64 operator apply", "degree": k, "level": level, "dofs": N,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "parallelism": parallelism,
                    "l2": "inputs larger than L2 (x, y 227 MB each vs 126 MB L2); no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_per_launch, "kernel": "stokes_vmult_kernel<double,2,4,4,2,OCC=2,NT=384>"},
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "kernel": f"stokes_vmult_kernel<double,{k}> (k=2: 4x4x2-cell bricks, 2 CTAs/SM, 384 threads)"},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
-        "fp32_vmult": {"value": N * world / (ms32 * 1e-3), "unit": "DoF/s", "ms": ms32},
-        "smoother_fp32": {"value": N * world / (ms_smooth * 1e-3), "unit": "DoF/s", "ms_per_step": ms_smooth,
-                          "ns_per_dof": ms_smooth * 1e6 / N},
-        "solve": solve,
     }
+    out.update(extra)
     print(json.dumps(out))
     if dist:
         dist.destroy_process_group()

@@ -192,18 +192,13 @@ void vcycle(Context& c, int level, int prec, void* x, const void* b) {
 int fgmres(Context& c, int level, double* x, const double* b, double tol, int max_iter, int vp, int* iters,
            double* hist) {
   const int64_t N = c.dev[0][level].lay.total;
-  std::vector<double*> V, Z, owned;
-  struct Guard {
-    std::vector<double*>* v;
-    ~Guard() {
-      for (double* p : *v) cudaFree(p);
-    }
-  } guard{&owned};
+  std::vector<double*> V, Z;
+  // Krylov basis vectors come from a per-context pool (finest-level size, grown on first use and
+  // kept): no allocation inside the solve after the first call
+  size_t used = 0;
   auto newvec = [&]() {
-    void* d = nullptr;
-    SMG_CUDA(cudaMalloc(&d, N * sizeof(double)));
-    owned.push_back(static_cast<double*>(d));
-    return static_cast<double*>(d);
+    if (used == c.krylov.size()) c.krylov.push_back(alloc_vec(c, c.cfg.max_level, SMG_F64));
+    return static_cast<double*>(c.krylov[used++]);
   };
   void *vb = nullptr, *vx = nullptr;
   if (vp == SMG_F32) ensure_work(c, SMG_F32);

@@ -113,6 +113,7 @@ struct Context {
   std::vector<void*> allocations;
   // per-level work vectors for the smoother / V-cycle (allocated lazily): [prec][level]
   std::vector<void*> work_r[2], work_x[2], work_b[2];
+  std::vector<void*> krylov;  // FGMRES basis pool (fp64, finest-level size)
   void* pstage[2] = {nullptr, nullptr};  // pressure staging for the BlockVector host path (finest level size)
   // TMA descriptors of input vectors (vmult.cu)
   void* tmap_dev = nullptr;

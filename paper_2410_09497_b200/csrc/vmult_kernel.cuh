@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <set>
 
 #include "smg_internal.cuh"
 #include "vmult.cuh"
@@ -160,6 +161,7 @@ struct Geo {
   int m, n;
   int nlim[3];  // exclusive node limit of the outputs per axis (n, n, z_end * H)
   int mlim[3];  // exclusive cell limit per axis (m, m, z_end)
+  int zoff;     // first z node plane the vector holds (0, or zlo * H for a slab): TMA maps are slab-local
   int c0[3];  // brick cell origin
   int g0[3];  // brick node origin
 };
@@ -255,7 +257,9 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
           if (y >= 0 && y < n && z >= 0 && z < n) {
             const int64_t start = (static_cast<int64_t>(z) * n + y) * (n + 1) + G.g0[0] - H;
             const int64_t sal = start >= 0 ? start / BR::VEC * BR::VEC : -((-start + BR::VEC - 1) / BR::VEC) * BR::VEC;
-            const int64_t ss = sal > 0 ? sal : 0;
+            // rows at y = 0 must not reach back into plane z - 1 (for a slab, that plane may not be held)
+            const int64_t row0 = static_cast<int64_t>(z) * n * (n + 1);
+            const int64_t ss = (y == 0 && sal < row0) ? row0 : sal;
             const unsigned nb = static_cast<unsigned>((UX - (ss - sal)) * sizeof(T));
             bulk_load(dst + (ss - sal), X.c[0] + ss, nb, bar);
             bytes += nb;
@@ -272,8 +276,8 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
         mbar_expect(bar, static_cast<unsigned>(BR::sizeU(C) * sizeof(T)));
         // u_y / u_z maps start one row / plane in, so the constrained planes 0 and n fall outside
         const int xs = max(floor_to(G.g0[0] - H, BR::VEC), 0);
-        if (C == 1) tma_load_3d(sU + BR::PADF, &M.u1, xs, G.g0[1] - H - 1, G.g0[2] - H, bar);
-        else tma_load_3d(sU + BR::PADF, &M.u2, xs, G.g0[1] - H, G.g0[2] - H - 1, bar);
+        if (C == 1) tma_load_3d(sU + BR::PADF, &M.u1, xs, G.g0[1] - H - 1, G.g0[2] - H - G.zoff, bar);
+        else tma_load_3d(sU + BR::PADF, &M.u2, xs, G.g0[1] - H, G.g0[2] - H - G.zoff, bar);
       }
     }
   } else {
@@ -301,7 +305,7 @@ __device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const Blocks<const
     if (threadIdx.x == 0) {
       mbar_expect(bar, static_cast<unsigned>(BR::PBOX * sizeof(T)));
       const int xs = max(floor_to(G.g0[0] - H, BR::VEC), 0);
-      tma_load_3d(sP + BR::PADF, &M.p, xs, G.g0[1] - H, G.g0[2] - H, bar);
+      tma_load_3d(sP + BR::PADF, &M.p, xs, G.g0[1] - H, G.g0[2] - H - G.zoff, bar);
     }
   } else {
     constexpr int E0 = BR::N(0) + H, E1 = BR::N(1) + H, E2 = BR::N(2) + H;
@@ -327,6 +331,15 @@ __device__ __forceinline__ void fix_columns(T* sU0, T* sU1, T* sU2, T* sP, const
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   const int x0 = G.g0[0] - H;
+  if (sU2) {
+    // u_z boxes hold every z plane of the vector: zero the constrained planes z = 0 and z = n
+    constexpr int PL = BR::UY(2) * BR::UX(2);
+    const int zb = G.g0[2] - H;  // global plane of box plane 0
+    if (zb <= 0)
+      for (int i = threadIdx.x; i < PL; i += NT) sU2[BR::PADF + (0 - zb) * PL + i] = T(0);
+    if (zb + BR::UZ(2) > G.n)
+      for (int i = threadIdx.x; i < PL; i += NT) sU2[BR::PADF + (G.n - zb) * PL + i] = T(0);
+  }
   if (x0 > 0 && x0 + BR::XEXT(0) <= G.n) return;
   if (sU0) {
     constexpr int XE = BR::XEXT(0), UY = BR::UY(0), ROWS = BR::UY(0) * BR::UZ(0);
@@ -659,7 +672,8 @@ __device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, i
 // box -- overlaps compute.
 template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, bool RESID, bool TMA>
 __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<const T> X, const Blocks<T> Y,
-                                                             const Blocks<const T> B, int m, int zc0, int zc1, T h,
+                                                             const Blocks<const T> B, int m, int zc0, int zc1, int zlo,
+                                                             T h,
                                                              const Maps* __restrict__ mapsp) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
@@ -676,6 +690,7 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
   G.nlim[2] = zc1 * H;
   G.mlim[0] = G.mlim[1] = m;
   G.mlim[2] = zc1;
+  G.zoff = Gn.zoff = zlo * H;
   for (int a = 0; a < 3; ++a) {
     Gn.nlim[a] = G.nlim[a];
     Gn.mlim[a] = G.mlim[a];
@@ -839,48 +854,52 @@ void encode(CUtensorMap* map, const void* base, int rank, const uint64_t* dims, 
 // TMA needs 16-B aligned row pitches / base offsets (n * sizeof(T) % 16 == 0); boxes are kept no
 // larger than the tensor (small coarse levels take the cp.async path).
 template <typename T, int K, int BX, int BY, int BZ, int OCC>
-bool tma_ok(int n) {
+bool tma_ok(int n, int nz) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   if ((static_cast<int64_t>(n) * sizeof(T)) % 16 != 0) return false;
-  const int lim = n - 1;  // smallest extent among the u_y / u_z maps
-  const int ext[] = {BR::UX(1), BR::UY(1), BR::UZ(1), BR::UX(2), BR::UY(2), BR::UZ(2), BR::PXT, BR::N(1) + H,
-                     BR::N(2) + H};
-  for (int e : ext)
-    if (e > lim) return false;
+  // boxes no larger than the maps: x / y extents against n - 1 (u_y drops two rows), z against the
+  // held planes nz
+  const int xy[] = {BR::UX(1), BR::UY(1), BR::UX(2), BR::UY(2), BR::PXT, BR::N(1) + H};
+  for (int e : xy)
+    if (e > n - 1) return false;
+  const int zz[] = {BR::UZ(1), BR::UZ(2), BR::N(2) + H};
+  for (int e : zz)
+    if (e > nz) return false;
   return true;
 }
 
 template <typename T, int K, int BX, int BY, int BZ, int OCC>
-Maps make_maps(const Blocks<const T>& X, int n) {
+Maps make_maps(const LevelLayout& lay, const T* x) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
   Maps M;
   std::memset(&M, 0, sizeof(M));
   const uint64_t es = sizeof(T);
-  const uint64_t nn = static_cast<uint64_t>(n);
-  // global-index maps over (virtual) block bases; a slab only ever addresses the planes it holds
+  const uint64_t nn = static_cast<uint64_t>(lay.n);
+  const uint64_t nz = static_cast<uint64_t>(lay.zhi - lay.zlo) * H;  // held z node planes
+  // maps over the held part of each block (slab-local z = global z - zlo H; the kernel shifts);
   // u_x rows have the odd pitch n+1 (not a legal TMA stride): staged by non-tensor bulk copies
-  {  // u_y: dims (x n, y n+1, z n); base one row in -> y' = y - 1 in [0, n-1)
-    const uint64_t d[3] = {nn, nn - 1, nn};
+  {  // u_y: dims (x n, y n+1, z); base one row in -> y' = y - 1 in [0, n-1): the constrained rows are OOB
+    const uint64_t d[3] = {nn, nn - 1, nz};
     const uint64_t s[2] = {nn * es, nn * (nn + 1) * es};
     const uint32_t box[3] = {static_cast<uint32_t>(BR::UX(1)), static_cast<uint32_t>(BR::UY(1)),
                              static_cast<uint32_t>(BR::UZ(1))};
-    encode<T>(&M.u1, X.c[1] + nn, 3, d, s, box);
+    encode<T>(&M.u1, x + lay.off[1] + nn, 3, d, s, box);
   }
-  {  // u_z: dims (x n, y n, z n+1); base one plane in -> z' = z - 1 in [0, n-1)
-    const uint64_t d[3] = {nn, nn, nn - 1};
+  {  // u_z: dims (x n, y n, z planes incl. the top one); constrained planes zeroed after landing
+    const uint64_t d[3] = {nn, nn, nz + 1};
     const uint64_t s[2] = {nn * es, nn * nn * es};
     const uint32_t box[3] = {static_cast<uint32_t>(BR::UX(2)), static_cast<uint32_t>(BR::UY(2)),
                              static_cast<uint32_t>(BR::UZ(2))};
-    encode<T>(&M.u2, X.c[2] + nn * nn, 3, d, s, box);
+    encode<T>(&M.u2, x + lay.off[2], 3, d, s, box);
   }
   {  // p
-    const uint64_t d[3] = {nn, nn, nn};
+    const uint64_t d[3] = {nn, nn, nz};
     const uint64_t s[2] = {nn * es, nn * nn * es};
     const uint32_t box[3] = {static_cast<uint32_t>(BR::PXT), static_cast<uint32_t>(BR::N(1) + H),
                              static_cast<uint32_t>(BR::N(2) + H)};
-    encode<T>(&M.p, X.c[3], 3, d, s, box);
+    encode<T>(&M.p, x + lay.off[3], 3, d, s, box);
   }
   return M;
 }
@@ -919,8 +938,9 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
   const size_t smem = BR::BYTES;
   static const bool no_tma = std::getenv("SMG_NO_TMA") != nullptr;  // diagnostics: force the cp.async path
   bool aligned = true;
-  for (int c = 0; c < 4; ++c) aligned = aligned && reinterpret_cast<uintptr_t>(X.c[c]) % 16 == 0;
-  const bool tma = !no_tma && tma_ok<T, K, BX, BY, BZ, OCC>(n) && aligned;
+  for (int c = 0; c < 4; ++c)
+    aligned = aligned && (reinterpret_cast<uintptr_t>(a.x) + lay.off[c] * sizeof(T)) % 16 == 0;
+  const bool tma = !no_tma && tma_ok<T, K, BX, BY, BZ, OCC>(n, (lay.zhi - lay.zlo) * (K + 1)) && aligned;
   const Maps* dmaps = nullptr;
   if (tma) {
     // tensor maps are cached per (input vector, slab, level, precision) in 64-B aligned global
@@ -931,7 +951,7 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
       const int slot = ctx.tmap_next++ % kTmapSlots;
       for (auto e = ctx.tmap_slots.begin(); e != ctx.tmap_slots.end();)
         e = (e->second == slot) ? ctx.tmap_slots.erase(e) : std::next(e);
-      Maps mh = make_maps<T, K, BX, BY, BZ, OCC>(X, n);
+      Maps mh = make_maps<T, K, BX, BY, BZ, OCC>(lay, static_cast<const T*>(a.x));
       char* dst = static_cast<char*>(ctx.tmap_dev) + static_cast<size_t>(slot) * kTmapSlotBytes;
       SMG_CUDA(cudaMemcpyAsync(dst, &mh, sizeof(Maps), cudaMemcpyHostToDevice, ctx.stream));
       SMG_CUDA(cudaStreamSynchronize(ctx.stream));  // mh is a stack temporary
@@ -942,12 +962,10 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
   }
   static_assert(sizeof(Maps) <= kTmapSlotBytes, "tensor-map slot too small");
   auto go = [&](auto kern) {
-    static bool attr_set = false;  // one instantiation per lambda call site / kernel
-    if (!attr_set) {
+    static std::set<const void*> attr_set;  // kernels whose smem limit is raised already
+    if (attr_set.insert(reinterpret_cast<const void*>(kern)).second)
       SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-      attr_set = true;
-    }
-    kern<<<grid, NT, smem, ctx.stream>>>(X, Y, B, m, a.z0, a.z1, h, dmaps);
+    kern<<<grid, NT, smem, ctx.stream>>>(X, Y, B, m, a.z0, a.z1, a.zlo, h, dmaps);
   };
   if (a.b) {
     if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, OCC, NT, true, true>);

@@ -115,6 +115,12 @@ class HaloExchange:
 
     def exchange(self, v):
         import torch.distributed as dist
+        if v.is_cuda and dist.get_backend(self.group) == "gloo":
+            # gloo has no CUDA P2P: stage through host memory (test mode on single-GPU boxes)
+            h = v.cpu()
+            self.exchange(h)
+            v.copy_(h)
+            return v
         ops = self._ops(v)
         if ops:
             for w in dist.batch_isend_irecv(ops):
@@ -188,7 +194,8 @@ class SlabOperator:
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            t = torch.tensor([out.value], dtype=torch.float64, device=a.device)
-            dist.all_reduce(t)
+            gloo = dist.get_backend(self.halo.group) == "gloo"
+            t = torch.tensor([out.value], dtype=torch.float64, device="cpu" if gloo else a.device)
+            dist.all_reduce(t, group=self.halo.group)
             return float(t.item())
         return out.value
