@@ -127,19 +127,24 @@ struct Brick {
   // two U buffers (staging of the next component overlaps compute) when they fit in the per-CTA share
   // of the 228 KB SM (OCC resident CTAs, 1 KB reserved per CTA), else one
   static constexpr size_t kSmemCap = OCC == 1 ? 232448 : 233472 / OCC - 1024;
-  static constexpr size_t bytes_for(int nbuf) {
-    return (static_cast<size_t>(nbuf * U + PBUF + A1 + 2 * ST + YP + (ALIAS ? 0 : 2 * ST)) * sizeof(T) + 15) / 16 *
-               16 + 3 * 8;
+  static constexpr size_t rup16(size_t b) { return (b + 15) / 16 * 16 + 3 * 8; }
+  // double-buffered layout: [U0][U1][P][A1][B1][Q][YP] (+[S][T] unless they alias the dead U buffer)
+  static constexpr size_t bytes_db() {
+    return rup16(static_cast<size_t>(2 * U + PBUF + A1 + 2 * ST + YP + (ALIAS ? 0 : 2 * ST)) * sizeof(T));
   }
-  static constexpr bool DB = bytes_for(2) <= kSmemCap;
+  // single-buffered "early release" layout: [U][P][A1][B1=T][Q][YP][S]; U is dead after pass 1, so the
+  // next component's staging is issued there and overlaps passes 2-3 and the next Q passes
+  static constexpr size_t bytes_sb() { return rup16(static_cast<size_t>(U + PBUF + A1 + 3 * ST + YP) * sizeof(T)); }
+  static constexpr size_t bytes_for(int nbuf) { return nbuf == 2 ? bytes_db() : bytes_sb(); }
+  static constexpr bool DB = bytes_db() <= kSmemCap;
   static constexpr int OFF_U1 = DB ? U : 0;
   static constexpr int OFF_P = (DB ? 2 : 1) * U;
   static constexpr int OFF_A1 = OFF_P + PBUF;
   static constexpr int OFF_B1 = OFF_A1 + A1;
   static constexpr int OFF_Q = OFF_B1 + ST;
   static constexpr int OFF_YP = OFF_Q + ST;
-  static constexpr int OFF_ST = OFF_YP + YP;  // only used when !ALIAS
-  static constexpr int END = OFF_YP + YP + (ALIAS ? 0 : 2 * ST);
+  static constexpr int OFF_ST = OFF_YP + YP;  // DB && !ALIAS: S, T; SB: S
+  static constexpr int END = DB ? OFF_YP + YP + (ALIAS ? 0 : 2 * ST) : OFF_YP + YP + ST;
   static constexpr size_t BYTES = (static_cast<size_t>(END) * sizeof(T) + 15) / 16 * 16 + 3 * 8;
   static_assert(BYTES == bytes_for(DB ? 2 : 1), "smem layout");
   static constexpr int stride(int axis, int a0, int a1) { return axis == 0 ? 1 : (axis == 1 ? a0 : a0 * a1); }
@@ -172,8 +177,11 @@ struct Geo {
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -246,12 +254,13 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
   if constexpr (TMA) {
     if constexpr (C == 0) {
       // one bulk copy per x-row inside the domain (rows have the odd pitch n+1, so no tensor map);
-      // warp 0 issues, rows outside the domain are zero-filled directly. A row may read past the
-      // end of u_x into u_y (same allocation); those columns are zeroed by fix_columns.
-      if (tid < 32) {
+      // every warp issues its share of the rows and arrives once on the U barrier (initialised with
+      // NT/32 arrivals) with its bytes; rows outside the domain are zero-filled directly. A row may
+      // read past the end of u_x into u_y (same allocation); those columns are zeroed by fix_columns.
+      {
         const int y0 = G.g0[1] - H, z0 = G.g0[2] - H;
         unsigned bytes = 0;
-        for (int r = tid; r < UY * UZ; r += 32) {
+        for (int r = tid; r < UY * UZ; r += NT) {
           const int y = y0 + r % UY, z = z0 + r / UY;
           T* dst = sU + r * UX;
           if (y >= 0 && y < n && z >= 0 && z < n) {
@@ -269,15 +278,17 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
           }
         }
         bytes = __reduce_add_sync(0xffffffffu, bytes);
-        if (tid == 0) mbar_expect(bar, bytes);  // arrive + expect_tx after the copies: tx may go negative first
+        if ((tid & 31) == 0) mbar_expect(bar, bytes);  // arrive + expect_tx after the copies: tx may go negative first
       }
     } else {
       if (tid == 0) {
         mbar_expect(bar, static_cast<unsigned>(BR::sizeU(C) * sizeof(T)));
-        // u_y / u_z maps start one row / plane in, so the constrained planes 0 and n fall outside
+        // the u_y map starts one row in, so its constrained rows 0 and n fall outside
         const int xs = max(floor_to(G.g0[0] - H, BR::VEC), 0);
         if (C == 1) tma_load_3d(sU + BR::PADF, &M.u1, xs, G.g0[1] - H - 1, G.g0[2] - H - G.zoff, bar);
         else tma_load_3d(sU + BR::PADF, &M.u2, xs, G.g0[1] - H, G.g0[2] - H - G.zoff, bar);
+      } else if ((tid & 31) == 0) {
+        mbar_arrive(bar);  // the U barriers count one arrival per warp
       }
     }
   } else {
@@ -413,7 +424,9 @@ __device__ __forceinline__ void cell_sipg(const T (&pv)[K + 1], const T (&cu)[K 
 // ---------------------------------------------------------------------------------------------
 template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, int C, bool RESID, bool TMA>
 __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const Geo* Gn, const Blocks<const T>& X,
-                                          const Blocks<T>& Y, const Blocks<const T>& B, const Maps& M, uint64_t* barP) {
+                                          const Blocks<T>& Y, const Blocks<const T>& B, const Maps& M, uint64_t* barP,
+                                          uint64_t* barU = nullptr, unsigned* phU = nullptr, int nextC = -1,
+                                          const Geo* Gnext = nullptr) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   using R = Ref<K>;
   constexpr int H = K + 1, P = K + 2;
@@ -433,8 +446,8 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
   T* sQ = sm + BR::OFF_Q;
   T* sP = sm + BR::OFF_P;
   T* sYP = sm + BR::OFF_YP;
-  T* sS = BR::ALIAS ? sU : sm + BR::OFF_ST;
-  T* sT = sS + BR::ST;
+  T* sS = (BR::DB && BR::ALIAS) ? sU : sm + BR::OFF_ST;
+  T* sT = BR::DB ? sS + BR::ST : sB1;  // single-buffer layout: T overwrites B1 in place (same cell block)
 
   // ---- Q2 = M_o2 p over c in [-H, N_c), o1 owned, o2 owned (from the P box) ----
   {
@@ -474,6 +487,22 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       for (int a = 0; a < H; ++a) sQ[(oj * No1 + e1 * H + a) * PC + ci] = out[a];
     }
     __syncthreads();
+  }
+  if constexpr (!BR::DB) {
+    // single-buffer mode: U of this component was issued during the previous component's passes 2-3
+    if (TMA) {
+      mbar_wait(barU, *phU);
+      *phU ^= 1;
+    } else {
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (TMA) {
+      fix_columns<T, K, BX, BY, BZ, OCC, NT>(C == 0 ? sU : nullptr, C == 1 ? sU : nullptr, C == 2 ? sU : nullptr,
+                                             nullptr, G);
+      __syncthreads();
+    }
   }
   // ---- pass 1 (along o2): A1 = M_o2 U (c full, o1 with halo, o2 owned); B1 = L_o2 U (o1 owned) ----
   {
@@ -517,7 +546,16 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       for (int a = 0; a < H; ++a) sB1[((e2 * H + a) * No1 + o) * PC + ci] = out[a];
     }
   }
-  __syncthreads();
+  if constexpr (!BR::DB) {
+    fence_proxy_async();  // generic reads of U happen-before the async-proxy writes of the next staging
+    __syncthreads();
+    if (nextC == 0) issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sU, barU, X, M, *Gnext);
+    else if (nextC == 1) issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA>(sU, barU, X, M, *Gnext);
+    else if (nextC == 2) issue_u<T, K, BX, BY, BZ, OCC, NT, 2, TMA>(sU, barU, X, M, *Gnext);
+    if (!TMA) cp_async_commit();
+  } else {
+    __syncthreads();
+  }
   // ---- pass 2 (along o1): S = M_o1 A1, T = L_o1 A1 + M_o1 B1 (c full, o1/o2 owned) ----
   {
     const int cell_o1 = G.c0[O1];
@@ -701,9 +739,9 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
   int brick = blockIdx.x;
   if (brick >= nbricks) return;
   if (TMA && threadIdx.x == 0) {
-    mbar_init(&bars[0]);
-    mbar_init(&bars[1]);
-    mbar_init(&bars[2]);
+    mbar_init(&bars[0], NT / 32);  // U buffers: one arrival per warp (issue_u)
+    mbar_init(&bars[1], NT / 32);
+    mbar_init(&bars[2], 1);        // P box: thread 0
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   fence_proxy_async();
@@ -715,50 +753,30 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
   int u0 = 0;
   unsigned ph[2] = {0, 0}, phP = 0;  // mbarrier phase of buffer 0 / 1 / P
   if constexpr (!BR::DB) {
-    // single U buffer (large degrees): stage, compute, stage the next component
-    auto wait_u = [&](bool withP) {
-      if (TMA) {
-        if (withP) {
-          mbar_wait(&bars[2], phP);
-          phP ^= 1;
-        }
-        mbar_wait(&bars[0], ph[0]);
-        ph[0] ^= 1;
-      } else {
-        cp_async_commit();
-        cp_async_wait<0>();
-      }
-      __syncthreads();
-    };
+    // single U buffer, released early (component(): next staging issued after pass 1)
     for (; brick < nbricks; brick += gridDim.x) {
       const int next = brick + gridDim.x;
       const bool has_next = next < nbricks;
       if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H, zc0);
       for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
-      wait_u(true);
       if (TMA) {
-        fix_columns<T, K, BX, BY, BZ, OCC, NT>(sm, nullptr, nullptr, sP, G);
+        mbar_wait(&bars[2], phP);
+        phP ^= 1;
         __syncthreads();
+        fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, nullptr, nullptr, sP, G);
+      } else {
+        cp_async_commit();
+        cp_async_wait<0>();
       }
-      component<T, K, BX, BY, BZ, OCC, NT, 0, RESID, TMA>(sm, sm, G, h, nullptr, X, Y, B, maps, &bars[2]);
-      issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA>(sm, &bars[0], X, maps, G);
-      wait_u(false);
-      if (TMA) {
-        fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, sm, nullptr, nullptr, G);
-        __syncthreads();
-      }
-      component<T, K, BX, BY, BZ, OCC, NT, 1, RESID, TMA>(sm, sm, G, h, nullptr, X, Y, B, maps, &bars[2]);
-      issue_u<T, K, BX, BY, BZ, OCC, NT, 2, TMA>(sm, &bars[0], X, maps, G);
-      wait_u(false);
-      if (TMA) {
-        fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, nullptr, sm, nullptr, G);
-        __syncthreads();
-      }
+      __syncthreads();
+      component<T, K, BX, BY, BZ, OCC, NT, 0, RESID, TMA>(sm, sm, G, h, nullptr, X, Y, B, maps, &bars[2], &bars[0],
+                                                          &ph[0], 1, &G);
+      component<T, K, BX, BY, BZ, OCC, NT, 1, RESID, TMA>(sm, sm, G, h, nullptr, X, Y, B, maps, &bars[2], &bars[0],
+                                                          &ph[0], 2, &G);
       component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, sm, G, h, has_next ? &Gn : nullptr, X, Y, B, maps,
-                                                     &bars[2]);
+                                                          &bars[2], &bars[0], &ph[0], has_next ? 0 : -1, &Gn);
       write_pressure<T, K, BX, BY, BZ, OCC, NT, RESID>(sYP, G, Y.c[3], RESID ? B.c[3] : nullptr);
       __syncthreads();
-      if (has_next) issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sm, &bars[0], X, maps, Gn);
       G = Gn;
     }
     if (!TMA) cp_async_wait<0>();
