@@ -339,7 +339,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "kernel": f"stokes_vmult_kernel<double,{k}> (k=2: 4x4x2-cell bricks, 2 CTAs/SM, 384 threads)"},
+                     "kernel": f"stokes_vmult_kernel<double,{k}> (k=2: 4x4x2-cell bricks, 2 CTAs/SM, 256 threads)"},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
     }
     out.update(extra)

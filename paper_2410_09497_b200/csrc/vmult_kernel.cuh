@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <set>
+#include <type_traits>
 
 #include "smg_internal.cuh"
 #include "vmult.cuh"
@@ -370,51 +371,62 @@ __device__ __forceinline__ void fix_columns(T* sU0, T* sU1, T* sU2, T* sP, const
 }
 
 // ---------------------------------------------------------------------------------------------
-// per-cell 1D kernels on register arrays (one work item = one cell of one 1D line)
+// 1D kernels on register arrays: one work item = a segment of NC consecutive cells of one 1D line
 // ---------------------------------------------------------------------------------------------
-// DG mass, one cell block: out[a] = sum_b MO[a][b] cu[b]
-template <typename T, int K>
-__device__ __forceinline__ void cell_mass(const T (&cu)[K + 1], T (&out)[K + 1]) {
+// DG mass, block diagonal: out[e*H+a] = sum_b MO[a][b] in[e*H+b]
+template <typename T, int K, int NC>
+__device__ __forceinline__ void seg_mass(const T (&in)[NC * (K + 1)], T (&out)[NC * (K + 1)]) {
   constexpr int H = K + 1;
 #pragma unroll
-  for (int a = 0; a < H; ++a) {
-    T s = T(0);
+  for (int e = 0; e < NC; ++e)
 #pragma unroll
-    for (int b = 0; b < H; ++b) s += cref<T>(Ref<K>::MO + a * H + b) * cu[b];
-    out[a] = s;
-  }
+    for (int a = 0; a < H; ++a) {
+      T s = T(0);
+#pragma unroll
+      for (int b = 0; b < H; ++b) s += cref<T>(Ref<K>::MO + a * H + b) * in[e * H + b];
+      out[e * H + a] = s;
+    }
 }
-// DG SIPG rows of one cell from its (previous, current, next) cell values. The off-diagonal blocks
-// are cross shaped for the Gauss-Lobatto basis (LOM[a][b] != 0 only if a == 0 or b == K, LOP only
-// if a == K or b == 0). first / last: the cell is the first / last of the global line (Nitsche end
-// rows DLF / DLL); neighbours outside the domain arrive zero-filled.
-template <typename T, int K>
-__device__ __forceinline__ void cell_sipg(const T (&pv)[K + 1], const T (&cu)[K + 1], const T (&nx)[K + 1], bool first,
-                                          bool last, T (&out)[K + 1]) {
+// DG SIPG rows of NC cells from NC+2 cells of input (one neighbour cell each side, zero-filled
+// outside the domain). The off-diagonal blocks are cross shaped for the Gauss-Lobatto basis
+// (LOM[a][b] != 0 only if a == 0 or b == K, LOP only if a == K or b == 0). BND: the segment may hold
+// the first / last cell of the global line (local index efirst / elast, -1 if not): Nitsche rows.
+template <typename T, int K, int NC, bool BND>
+__device__ __forceinline__ void seg_sipg(const T (&in)[(NC + 2) * (K + 1)], T (&out)[NC * (K + 1)], int efirst,
+                                         int elast) {
   constexpr int H = K + 1;
   using R = Ref<K>;
 #pragma unroll
-  for (int a = 0; a < H; ++a) {
-    T s = T(0);
+  for (int e = 0; e < NC; ++e)
 #pragma unroll
-    for (int b = 0; b < H; ++b) s += cref<T>(R::LO0 + a * H + b) * cu[b];
+    for (int a = 0; a < H; ++a) {
+      T s = T(0);
 #pragma unroll
-    for (int b = 0; b < H; ++b)
-      if (a == 0 || b == K) s += cref<T>(R::LOM + a * H + b) * pv[b];
+      for (int b = 0; b < H; ++b) s += cref<T>(R::LO0 + a * H + b) * in[(e + 1) * H + b];
 #pragma unroll
-    for (int b = 0; b < H; ++b)
-      if (a == K || b == 0) s += cref<T>(R::LOP + a * H + b) * nx[b];
-    if (first) {
+      for (int b = 0; b < H; ++b)
+        if (a == 0 || b == K) s += cref<T>(R::LOM + a * H + b) * in[e * H + b];
 #pragma unroll
-      for (int b = 0; b < H; ++b) s += cref<T>(R::DLF + a * H + b) * cu[b];
+      for (int b = 0; b < H; ++b)
+        if (a == K || b == 0) s += cref<T>(R::LOP + a * H + b) * in[(e + 2) * H + b];
+      if (BND) {
+        if (e == efirst) {
+#pragma unroll
+          for (int b = 0; b < H; ++b) s += cref<T>(R::DLF + a * H + b) * in[(e + 1) * H + b];
+        }
+        if (e == elast) {
+#pragma unroll
+          for (int b = 0; b < H; ++b) s += cref<T>(R::DLL + a * H + b) * in[(e + 1) * H + b];
+        }
+      }
+      out[e * H + a] = s;
     }
-    if (last) {
-#pragma unroll
-      for (int b = 0; b < H; ++b) s += cref<T>(R::DLL + a * H + b) * cu[b];
-    }
-    out[a] = s;
-  }
 }
+template <bool V>
+using bool_c = std::integral_constant<bool, V>;
+// cells per work item along a brick axis of nc cells: segments of 2 cells for low degrees (shared
+// neighbour loads, fewer index computations), single cells otherwise
+constexpr int seg_cells(int nc, int k) { return (nc % 2 == 0 && k <= 3) ? 2 : 1; }
 
 // ---------------------------------------------------------------------------------------------
 // one velocity component (U already staged in sU); if C == 2 and Gn != nullptr, the next brick's
@@ -449,6 +461,8 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
   T* sS = (BR::DB && BR::ALIAS) ? sU : sm + BR::OFF_ST;
   T* sT = BR::DB ? sS + BR::ST : sB1;  // single-buffer layout: T overwrites B1 in place (same cell block)
 
+  constexpr int SQ2 = seg_cells(NO2, K), SQ = seg_cells(NO1, K), S1 = seg_cells(NO2, K), S2 = seg_cells(NO1, K),
+                S3 = seg_cells(NCc, K);
   // ---- Q2 = M_o2 p over c in [-H, N_c), o1 owned, o2 owned (from the P box) ----
   {
     T* sQ2 = sA1;
@@ -457,18 +471,18 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
                   PSO2 = BR::stride(O2, BR::PXT, E1P);
     constexpr int NL = (Nc + H) * No1;
     const int psh = brick_shift<T>(G, H);
-    for (int it = tid; it < NL * NO2; it += NT) {
-      const int e2 = it / NL, r = it - e2 * NL;
+    for (int it = tid; it < NL * (NO2 / SQ2); it += NT) {
+      const int e2 = (it / NL) * SQ2, r = it % NL;
       // consecutive items walk the P-box x axis (c for C=0, o1 otherwise): conflict-free
       const int ci = C == 0 ? r % (Nc + H) : r / No1;
       const int oi = C == 0 ? r / (Nc + H) : r % No1;
       const T* src = sP + psh + ci * PSC + (oi + H) * PSO1 + (e2 + 1) * H * PSO2;
-      T cu[H], out[H];
+      T cu[SQ2 * H], out[SQ2 * H];
 #pragma unroll
-      for (int j = 0; j < H; ++j) cu[j] = src[j * PSO2];
-      cell_mass<T, K>(cu, out);
+      for (int j = 0; j < SQ2 * H; ++j) cu[j] = src[j * PSO2];
+      seg_mass<T, K, SQ2>(cu, out);
 #pragma unroll
-      for (int a = 0; a < H; ++a) sQ2[((e2 * H + a) * No1 + oi) * PC + ci] = out[a];
+      for (int a = 0; a < SQ2 * H; ++a) sQ2[((e2 * H + a) * No1 + oi) * PC + ci] = out[a];
     }
     fence_proxy_async();
     __syncthreads();
@@ -476,15 +490,15 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
     if (!TMA && C == 2) cp_async_commit();
     // Q = M_o1 Q2
     constexpr int NL2 = (Nc + H) * No2;
-    for (int it = tid; it < NL2 * NO1; it += NT) {
-      const int e1 = it / NL2, r = it - e1 * NL2;
+    for (int it = tid; it < NL2 * (NO1 / SQ); it += NT) {
+      const int e1 = (it / NL2) * SQ, r = it % NL2;
       const int ci = r % (Nc + H), oj = r / (Nc + H);
-      T cu[H], out[H];
+      T cu[SQ * H], out[SQ * H];
 #pragma unroll
-      for (int j = 0; j < H; ++j) cu[j] = sQ2[(oj * No1 + e1 * H + j) * PC + ci];
-      cell_mass<T, K>(cu, out);
+      for (int j = 0; j < SQ * H; ++j) cu[j] = sQ2[(oj * No1 + e1 * H + j) * PC + ci];
+      seg_mass<T, K, SQ>(cu, out);
 #pragma unroll
-      for (int a = 0; a < H; ++a) sQ[(oj * No1 + e1 * H + a) * PC + ci] = out[a];
+      for (int a = 0; a < SQ * H; ++a) sQ[(oj * No1 + e1 * H + a) * PC + ci] = out[a];
     }
     __syncthreads();
   }
@@ -514,37 +528,39 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
                     : (C == 1 ? ci * UX + oi : ci * UY * UX + oi) + bsh;
     };
     constexpr int NLA = LC * LO1H;
-    for (int it = tid; it < NLA * NO2; it += NT) {
-      const int e2 = it / NLA, r = it - e2 * NLA;
+    for (int it = tid; it < NLA * (NO2 / S1); it += NT) {
+      const int e2 = (it / NLA) * S1, r = it % NLA;
       // consecutive items walk the staged box's x axis: c for C=0, o1 for C=1,2
       const int ci = C == 0 ? r % LC : r / LO1H;
       const int oi = C == 0 ? r / LC : r % LO1H;
       const T* src = sU + ub(ci, oi) + (e2 + 1) * H * US;
-      T cu[H], out[H];
+      T cu[S1 * H], out[S1 * H];
 #pragma unroll
-      for (int j = 0; j < H; ++j) cu[j] = src[j * US];
-      cell_mass<T, K>(cu, out);
+      for (int j = 0; j < S1 * H; ++j) cu[j] = src[j * US];
+      seg_mass<T, K, S1>(cu, out);
 #pragma unroll
-      for (int a = 0; a < H; ++a) sA1[((e2 * H + a) * LO1H + oi) * PC + ci] = out[a];
+      for (int a = 0; a < S1 * H; ++a) sA1[((e2 * H + a) * LO1H + oi) * PC + ci] = out[a];
     }
     const int cell_o2 = G.c0[O2];
-    constexpr int NLB = LC * No1;
-    for (int it = tid; it < NLB * NO2; it += NT) {
-      const int e2 = it / NLB, r = it - e2 * NLB;
-      const int ci = C == 0 ? r % LC : r / No1;
-      const int o = C == 0 ? r / LC : r % No1;
-      const T* src = sU + ub(ci, o + H) + e2 * H * US;
-      T pv[H], cu[H], nx[H], out[H];
+    auto passB = [&](auto bnd) {
+      constexpr bool BND = decltype(bnd)::value;
+      constexpr int NLB = LC * No1;
+      for (int it = tid; it < NLB * (NO2 / S1); it += NT) {
+        const int e2 = (it / NLB) * S1, r = it % NLB;
+        const int ci = C == 0 ? r % LC : r / No1;
+        const int o = C == 0 ? r / LC : r % No1;
+        const T* src = sU + ub(ci, o + H) + e2 * H * US;
+        T in[(S1 + 2) * H], out[S1 * H];
 #pragma unroll
-      for (int j = 0; j < H; ++j) {
-        pv[j] = src[j * US];
-        cu[j] = src[(H + j) * US];
-        nx[j] = src[(2 * H + j) * US];
+        for (int j = 0; j < (S1 + 2) * H; ++j) in[j] = src[j * US];
+        const int eg = cell_o2 + e2;  // global cell of the segment's first cell
+        seg_sipg<T, K, S1, BND>(in, out, eg == 0 ? 0 : -1, (m - 1 - eg < S1) ? m - 1 - eg : -1);
+#pragma unroll
+        for (int a = 0; a < S1 * H; ++a) sB1[((e2 * H + a) * No1 + o) * PC + ci] = out[a];
       }
-      cell_sipg<T, K>(pv, cu, nx, cell_o2 + e2 == 0, cell_o2 + e2 == m - 1, out);
-#pragma unroll
-      for (int a = 0; a < H; ++a) sB1[((e2 * H + a) * No1 + o) * PC + ci] = out[a];
-    }
+    };
+    if (cell_o2 == 0 || cell_o2 + NO2 >= m) passB(bool_c<true>());
+    else passB(bool_c<false>());
   }
   if constexpr (!BR::DB) {
     fence_proxy_async();  // generic reads of U happen-before the async-proxy writes of the next staging
@@ -559,34 +575,41 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
   // ---- pass 2 (along o1): S = M_o1 A1, T = L_o1 A1 + M_o1 B1 (c full, o1/o2 owned) ----
   {
     const int cell_o1 = G.c0[O1];
-    constexpr int NL = LC * No2;
-    for (int it = tid; it < NL * NO1; it += NT) {
-      const int e1 = it / NL, r = it - e1 * NL;
-      const int ci = r % LC, oj = r / LC;
-      const T* a1 = sA1 + (oj * LO1H + e1 * H) * PC + ci;
-      const T* b1 = sB1 + (oj * No1 + e1 * H) * PC + ci;
-      T pv[H], cu[H], nx[H], bb[H];
+    auto pass2 = [&](auto bnd) {
+      constexpr bool BND = decltype(bnd)::value;
+      constexpr int NL = LC * No2;
+      for (int it = tid; it < NL * (NO1 / S2); it += NT) {
+        const int e1 = (it / NL) * S2, r = it % NL;
+        const int ci = r % LC, oj = r / LC;
+        const T* a1 = sA1 + (oj * LO1H + e1 * H) * PC + ci;
+        const T* b1 = sB1 + (oj * No1 + e1 * H) * PC + ci;
+        T in[(S2 + 2) * H], bb[S2 * H];
 #pragma unroll
-      for (int j = 0; j < H; ++j) {
-        pv[j] = a1[j * PC];
-        cu[j] = a1[(H + j) * PC];
-        nx[j] = a1[(2 * H + j) * PC];
-        bb[j] = b1[j * PC];
-      }
-      T sv[H], tv[H], mb[H];
-      cell_mass<T, K>(cu, sv);
-      cell_sipg<T, K>(pv, cu, nx, cell_o1 + e1 == 0, cell_o1 + e1 == m - 1, tv);
-      cell_mass<T, K>(bb, mb);
+        for (int j = 0; j < (S2 + 2) * H; ++j) in[j] = a1[j * PC];
 #pragma unroll
-      for (int a = 0; a < H; ++a) {
-        sS[(oj * No1 + e1 * H + a) * PC + ci] = sv[a];
-        sT[(oj * No1 + e1 * H + a) * PC + ci] = tv[a] + mb[a];
+        for (int j = 0; j < S2 * H; ++j) bb[j] = b1[j * PC];
+        T cu[S2 * H];
+#pragma unroll
+        for (int j = 0; j < S2 * H; ++j) cu[j] = in[H + j];
+        T sv[S2 * H], tv[S2 * H], mb[S2 * H];
+        seg_mass<T, K, S2>(cu, sv);
+        const int eg = cell_o1 + e1;
+        seg_sipg<T, K, S2, BND>(in, tv, eg == 0 ? 0 : -1, (m - 1 - eg < S2) ? m - 1 - eg : -1);
+        seg_mass<T, K, S2>(bb, mb);
+#pragma unroll
+        for (int a = 0; a < S2 * H; ++a) {
+          sS[(oj * No1 + e1 * H + a) * PC + ci] = sv[a];
+          sT[(oj * No1 + e1 * H + a) * PC + ci] = tv[a] + mb[a];
+        }
       }
-    }
+    };
+    if (cell_o1 == 0 || cell_o1 + NO1 >= m) pass2(bool_c<true>());
+    else pass2(bool_c<false>());
   }
   __syncthreads();
   // ---- pass 3 (along c): y_c = h (L_c S + M_c T) + h^2 D^T Q ;  y_p += h^2 D S ----
-  // item (o1 line oi, o2 line oj, cell e) reads the window [eH, eH + 2H] of the c pencils
+  // item (o1 line oi, o2 line oj, cells e0 .. e0+S3-1) reads the window [e0 H, (e0 + S3 + 1) H] of the
+  // c pencils
   constexpr int NCP = odd(Nc);
   T* sYC = sA1;  // C = 0: outputs staged in smem (A1 is dead) for a coalesced x-row write-out
   {
@@ -596,60 +619,66 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
     constexpr int YSC = BR::stride(C, BR::YX, BR::N(1)), YSO1 = BR::stride(O1, BR::YX, BR::N(1)),
                   YSO2 = BR::stride(O2, BR::YX, BR::N(1));
     constexpr int NL = No1 * No2;
-    for (int it = tid; it < NL * NCc; it += NT) {
-      const int e = it / NL, r = it - e * NL;
+    constexpr int W = (S3 + 1) * H;  // window length of q; s and t have one more node
+    for (int it = tid; it < NL * (NCc / S3); it += NT) {
+      const int e0 = (it / NL) * S3, r = it % NL;
       const int oi = r % No1, oj = r / No1;
-      const int base = (oj * No1 + oi) * PC + e * H;
-      T s[2 * H + 1], t[2 * H + 1], q[2 * H];
+      const int base = (oj * No1 + oi) * PC + e0 * H;
+      T s[W + 1], t[W + 1], q[W];
 #pragma unroll
-      for (int j = 0; j < 2 * H + 1; ++j) {
+      for (int j = 0; j < W + 1; ++j) {
         s[j] = sS[base + j];
         t[j] = sT[base + j];
       }
 #pragma unroll
-      for (int j = 0; j < 2 * H; ++j) q[j] = sQ[base + j];
+      for (int j = 0; j < W; ++j) q[j] = sQ[base + j];
       int g[3];
       g[O1] = G.g0[O1] + oi;
       g[O2] = G.g0[O2] + oj;
       const bool inside = g[O1] < G.nlim[O1] && g[O2] < G.nlim[O2];
-#pragma unroll
-      for (int a = 0; a < H; ++a) {
-        T v = T(0), w = T(0);
-#pragma unroll
-        for (int bq = 0; bq < P; ++bq) {
-          v += cref<T>(R::LP + a * P + bq) * s[H + bq] + cref<T>(R::MP + a * P + bq) * t[H + bq];
-          if (a == 0) v += cref<T>(R::LP + (K + 1) * P + bq) * s[bq] + cref<T>(R::MP + (K + 1) * P + bq) * t[bq];
-        }
-#pragma unroll
-        for (int i = 0; i < H; ++i) {
-          w += cref<T>(R::D + i * P + a) * q[H + i];
-          if (a == 0) w += cref<T>(R::D + i * P + H) * q[i];
-        }
-        const T val = h * v + h2 * w;
-        if (C == 0) {
-          sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
-        } else {
-          g[C] = G.g0[C] + e * H + a;
-          if (inside && g[C] < G.nlim[C]) {
-            const int64_t gi = g[0] * st[0] + g[1] * st[1] + g[2] * st[2];
-            T rr = val;
-            if (g[C] == 0) rr = T(0);  // constrained boundary-normal row
-            else if (RESID) rr = bc[gi] - rr;
-            yc[gi] = rr;
-          }
-        }
-      }
-      // pressure rows of cell e: y_p += h^2 D S
       T* yp = sYP + oi * YSO1 + oj * YSO2;
 #pragma unroll
-      for (int i = 0; i < H; ++i) {
-        T z = T(0);
+      for (int ee = 0; ee < S3; ++ee) {
+        const int e = e0 + ee;
 #pragma unroll
-        for (int bq = 0; bq < P; ++bq) z += cref<T>(R::D + i * P + bq) * s[H + bq];
-        yp[(e * H + i) * YSC] += h2 * z;
+        for (int a = 0; a < H; ++a) {
+          T v = T(0), w = T(0);
+#pragma unroll
+          for (int bq = 0; bq < P; ++bq) {
+            v += cref<T>(R::LP + a * P + bq) * s[ee * H + H + bq] + cref<T>(R::MP + a * P + bq) * t[ee * H + H + bq];
+            if (a == 0)
+              v += cref<T>(R::LP + (K + 1) * P + bq) * s[ee * H + bq] + cref<T>(R::MP + (K + 1) * P + bq) * t[ee * H + bq];
+          }
+#pragma unroll
+          for (int i = 0; i < H; ++i) {
+            w += cref<T>(R::D + i * P + a) * q[ee * H + H + i];
+            if (a == 0) w += cref<T>(R::D + i * P + H) * q[ee * H + i];
+          }
+          const T val = h * v + h2 * w;
+          if (C == 0) {
+            sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
+          } else {
+            g[C] = G.g0[C] + e * H + a;
+            if (inside && g[C] < G.nlim[C]) {
+              const int64_t gi = g[0] * st[0] + g[1] * st[1] + g[2] * st[2];
+              T rr = val;
+              if (g[C] == 0) rr = T(0);  // constrained boundary-normal row
+              else if (RESID) rr = bc[gi] - rr;
+              yc[gi] = rr;
+            }
+          }
+        }
+        // pressure rows of cell e: y_p += h^2 D S
+#pragma unroll
+        for (int i = 0; i < H; ++i) {
+          T z = T(0);
+#pragma unroll
+          for (int bq = 0; bq < P; ++bq) z += cref<T>(R::D + i * P + bq) * s[ee * H + H + bq];
+          yp[(e * H + i) * YSC] += h2 * z;
+        }
       }
       // the constrained plane g_c = n belongs to the brick holding the last cell along c
-      if (C != 0 && e == NCc - 1 && inside && G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
+      if (C != 0 && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
         g[C] = n;
         yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
       }
@@ -1001,9 +1030,9 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
 // Brick shape (cells) per degree: fp64 SMEM ~80-200 KB, one persistent CTA per SM.
 template <typename T, int K> struct BrickShape;
 // NT: threads per CTA; OCC: resident CTAs per SM (persistent grid of OCC x #SMs, __launch_bounds__(NT, OCC))
-template <typename T> struct BrickShape<T, 1> { static constexpr int X = 8, Y = 4, Z = 4, NT = 512, OCC = 1; };
-template <typename T> struct BrickShape<T, 2> { static constexpr int X = 4, Y = 4, Z = 2, NT = 384, OCC = 2; };
-template <typename T> struct BrickShape<T, 3> { static constexpr int X = 4, Y = 2, Z = 2, NT = 512, OCC = 1; };
+template <typename T> struct BrickShape<T, 1> { static constexpr int X = 8, Y = 4, Z = 4, NT = 256, OCC = 2; };
+template <typename T> struct BrickShape<T, 2> { static constexpr int X = 4, Y = 4, Z = 2, NT = 256, OCC = 2; };
+template <typename T> struct BrickShape<T, 3> { static constexpr int X = 4, Y = 2, Z = 2, NT = 256, OCC = 1; };
 template <typename T> struct BrickShape<T, 4> { static constexpr int X = 2, Y = 2, Z = 2, NT = 384, OCC = 1; };
 template <> struct BrickShape<double, 5> { static constexpr int X = 2, Y = 1, Z = 1, NT = 256, OCC = 1; };
 template <> struct BrickShape<float, 5> { static constexpr int X = 2, Y = 2, Z = 1, NT = 256, OCC = 1; };
@@ -1023,27 +1052,57 @@ void launch_shape(Context& ctx, int level, const VmultArgs& a) {
 // tuning build only: alternative brick shapes selected by SMG_VMULT_VARIANT=1..N
 template <int X_, int Y_, int Z_, int NT_, int OCC_>
 struct Shape { static constexpr int X = X_, Y = Y_, Z = Z_, NT = NT_, OCC = OCC_; };
-template <typename T, int K>
-bool launch_variant(int v, Context& ctx, int level, const VmultArgs& a) {
-  switch (v) {
-    case 1: launch_shape<T, K, Shape<4, 4, 2, 256, 2>>(ctx, level, a); return true;
-    case 2: launch_shape<T, K, Shape<4, 2, 2, 256, 2>>(ctx, level, a); return true;
-    case 3: launch_shape<T, K, Shape<2, 2, 2, 128, 4>>(ctx, level, a); return true;
-    case 4: launch_shape<T, K, Shape<4, 4, 2, 384, 2>>(ctx, level, a); return true;
-    case 5: launch_shape<T, K, Shape<8, 2, 2, 256, 2>>(ctx, level, a); return true;
-    case 6: launch_shape<T, K, Shape<4, 2, 2, 128, 3>>(ctx, level, a); return true;
-    default: return false;
+template <int K>
+struct Variants;
+template <>
+struct Variants<1> {
+  template <typename T>
+  static bool run(int v, Context& ctx, int level, const VmultArgs& a) {
+    switch (v) {
+      case 1: launch_shape<T, 1, Shape<8, 4, 2, 256, 2>>(ctx, level, a); return true;
+      case 2: launch_shape<T, 1, Shape<4, 4, 4, 256, 2>>(ctx, level, a); return true;
+      case 3: launch_shape<T, 1, Shape<8, 4, 4, 256, 2>>(ctx, level, a); return true;
+      case 4: launch_shape<T, 1, Shape<8, 8, 2, 256, 2>>(ctx, level, a); return true;
+      default: return false;
+    }
   }
-}
+};
+template <>
+struct Variants<2> {
+  template <typename T>
+  static bool run(int v, Context& ctx, int level, const VmultArgs& a) {
+    switch (v) {
+      case 1: launch_shape<T, 2, Shape<4, 4, 2, 384, 2>>(ctx, level, a); return true;
+      case 2: launch_shape<T, 2, Shape<4, 2, 2, 256, 2>>(ctx, level, a); return true;
+      case 3: launch_shape<T, 2, Shape<2, 2, 2, 128, 4>>(ctx, level, a); return true;
+      case 4: launch_shape<T, 2, Shape<4, 4, 4, 512, 1>>(ctx, level, a); return true;
+      case 5: launch_shape<T, 2, Shape<8, 2, 2, 256, 2>>(ctx, level, a); return true;
+      default: return false;
+    }
+  }
+};
+template <>
+struct Variants<3> {
+  template <typename T>
+  static bool run(int v, Context& ctx, int level, const VmultArgs& a) {
+    switch (v) {
+      case 1: launch_shape<T, 3, Shape<2, 2, 2, 256, 2>>(ctx, level, a); return true;
+      case 2: launch_shape<T, 3, Shape<4, 2, 2, 256, 1>>(ctx, level, a); return true;
+      case 3: launch_shape<T, 3, Shape<4, 2, 2, 384, 1>>(ctx, level, a); return true;
+      case 4: launch_shape<T, 3, Shape<4, 2, 1, 256, 2>>(ctx, level, a); return true;
+      default: return false;
+    }
+  }
+};
 #endif
 
 template <int K>
 void vmult_launch_k(Context& ctx, int level, int prec, const VmultArgs& a) {
 #ifdef SMG_TUNE
   static const int variant = std::getenv("SMG_VMULT_VARIANT") ? std::atoi(std::getenv("SMG_VMULT_VARIANT")) : 0;
-  if (K == 2 && variant > 0) {
-    if (prec == SMG_F64 ? launch_variant<double, K>(variant, ctx, level, a)
-                        : launch_variant<float, K>(variant, ctx, level, a))
+  if (variant > 0) {
+    if (prec == SMG_F64 ? Variants<K>::template run<double>(variant, ctx, level, a)
+                        : Variants<K>::template run<float>(variant, ctx, level, a))
       return;
   }
 #endif
