@@ -22,6 +22,11 @@
 namespace smg {
 namespace {
 
+// Packed patch tables (pack_patch_tables; sizes in elements of T). Every matrix is stored twice, as
+// rows of M and rows of M^T, each row padded to a multiple of 4 elements (R4), so that a contraction
+// reads the coefficients of one output as 16-byte vectors (LDS.128) -- the coefficient broadcasts
+// were the largest instruction class after FFMA (profiles/r01 ncu_smoother_v6).
+constexpr int R4(int v) { return (v + 3) / 4 * 4; }
 template <int K>
 struct PD {
   static constexpr int NP = 2 * K + 1;  // parallel (C0 interior nodes of the 2-cell patch)
@@ -29,24 +34,42 @@ struct PD {
   static constexpr int NV = NP * NO * NO;
   static constexpr int NPR = NO * NO * NO;
   static constexpr int BIG = NV > NPR ? NV : NPR;
-  // packed table offsets (pack_patch_tables)
-  static constexpr int PAR_S = 0;                     // NP x NP
-  static constexpr int PAR_L = PAR_S + NP * NP;       // NP
-  static constexpr int ORTH_S = PAR_L + NP;           // 4 x NO x NO
-  static constexpr int ORTH_L = ORTH_S + 4 * NO * NO;  // 4 x NO
-  static constexpr int G_PAR = ORTH_L + 4 * NO;       // NO x NP  (D S_par)
-  static constexpr int G_ORTH = G_PAR + NO * NP;      // 4 x NO x NO (M' S_orth)
-  static constexpr int MPI = G_ORTH + 4 * NO * NO;    // NO x NO (M'^-1)
-  static constexpr int TAB = MPI + NO * NO;
+  static constexpr int SQP = NP * R4(NP), SQO = NO * R4(NO);
+  static constexpr int PAR_S = 0;                        // S_par rows          NP x R4(NP)
+  static constexpr int PAR_ST = PAR_S + SQP;             // S_par^T rows        NP x R4(NP)
+  static constexpr int PAR_L = PAR_ST + SQP;             // eigenvalues         R4(NP)
+  static constexpr int ORTH_S = PAR_L + R4(NP);          // 4 x S_orth rows     NO x R4(NO)
+  static constexpr int ORTH_ST = ORTH_S + 4 * SQO;       // 4 x S_orth^T rows
+  static constexpr int ORTH_L = ORTH_ST + 4 * SQO;       // 4 x R4(NO)
+  static constexpr int G_PAR = ORTH_L + 4 * R4(NO);      // (D S_par) rows      NO x R4(NP)
+  static constexpr int G_PART = G_PAR + NO * R4(NP);     // (D S_par)^T rows    NP x R4(NO)
+  static constexpr int G_ORTH = G_PART + NP * R4(NO);    // 4 x (M' S_orth) rows
+  static constexpr int G_ORTHT = G_ORTH + 4 * SQO;       // 4 x transposed
+  static constexpr int MPI = G_ORTHT + 4 * SQO;          // M'^-1 rows          NO x R4(NO)
+  static constexpr int TAB = MPI + SQO;
   static constexpr int TABP = (TAB + 3) / 4 * 4;
   // per-warp workspace: Fh (3 NV) | r z d q x (5 NPR) | T1 T2 (2 BIG)
   static constexpr int WS = 3 * NV + 5 * NPR + 2 * BIG;
   static constexpr int dv(int c, int a) { return a == c ? NP : NO; }
 };
 
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using type = float4;
+  static constexpr int N = 4;
+};
+template <>
+struct Vec16<double> {
+  using type = double2;
+  static constexpr int N = 2;
+};
+
 // out = (M applied along axis AX) in;  in dims (D0,D1,D2), out extent along AX = R.
-// M(i,j) = TRANS ? A[j*LDA + i] : A[i*LDA + j]. One pencil per lane, coefficients broadcast from SMEM.
-template <typename T, int D0, int D1, int D2, int AX, int R, int LDA, bool TRANS>
+// M(i,j) = A[i * R4(C) + j] (rows padded to 16 B). One pencil per lane; the coefficients of output i
+// are read as 16-byte vectors (broadcast LDS.128).
+template <typename T, int D0, int D1, int D2, int AX, int R>
 __device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __restrict__ A, T* __restrict__ out,
                                           int lane) {
   constexpr int DI[3] = {D0, D1, D2};
@@ -69,14 +92,28 @@ __device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __r
       bi = v * D0 + u;
       bo = v * DO0 + u;
     }
-    T x[C];
+    using V = typename Vec16<T>::type;
+    constexpr int NV = Vec16<T>::N, LD = R4(C), NVR = (C + NV - 1) / NV;
+    T x[NVR * NV];
 #pragma unroll
-    for (int j = 0; j < C; ++j) x[j] = in[bi + j * SI];
+    for (int j = 0; j < NVR * NV; ++j) x[j] = j < C ? in[bi + j * SI] : T(0);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
+      const V* Ai = reinterpret_cast<const V*>(A + i * LD);
       T s = T(0);
 #pragma unroll
-      for (int j = 0; j < C; ++j) s += (TRANS ? A[j * LDA + i] : A[i * LDA + j]) * x[j];
+      for (int q = 0; q < NVR; ++q) {
+        const V a = Ai[q];
+        if constexpr (Vec16<T>::N == 4) {
+          s += a.x * x[4 * q];
+          if (4 * q + 1 < C) s += a.y * x[4 * q + 1];
+          if (4 * q + 2 < C) s += a.z * x[4 * q + 2];
+          if (4 * q + 3 < C) s += a.w * x[4 * q + 3];
+        } else {
+          s += a.x * x[2 * q];
+          if (2 * q + 1 < C) s += a.y * x[2 * q + 1];
+        }
+      }
       out[bo + i * SO] = s;
     }
   }
@@ -96,12 +133,13 @@ struct Patch {
   int var[3];
   int lane;
 
-  __device__ const T* S(int c, int a) const {
-    return a == c ? tab + P::PAR_S : tab + P::ORTH_S + var[a] * P::NO * P::NO;
+  // rows of S (TR = false) or of S^T (TR = true) along axis a of component c
+  __device__ const T* S(int c, int a, bool tr) const {
+    return a == c ? tab + (tr ? P::PAR_ST : P::PAR_S) : tab + (tr ? P::ORTH_ST : P::ORTH_S) + var[a] * P::SQO;
   }
-  __device__ const T* L(int c, int a) const { return a == c ? tab + P::PAR_L : tab + P::ORTH_L + var[a] * P::NO; }
-  __device__ const T* G(int c, int a) const {
-    return a == c ? tab + P::G_PAR : tab + P::G_ORTH + var[a] * P::NO * P::NO;
+  __device__ const T* L(int c, int a) const { return a == c ? tab + P::PAR_L : tab + P::ORTH_L + var[a] * R4(P::NO); }
+  __device__ const T* G(int c, int a, bool tr) const {
+    return a == c ? tab + (tr ? P::G_PART : P::G_PAR) : tab + (tr ? P::G_ORTHT : P::G_ORTH) + var[a] * P::SQO;
   }
 
   // eigen-space transforms of a velocity-shaped array of component C (S square per axis):
@@ -109,11 +147,11 @@ struct Patch {
   template <int C, bool TR>
   __device__ void s3(const T* in, T* out, T* tmp) const {
     constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, A0, A1, A2, 0, A0, A0, TR>(in, S(C, 0), out, lane);
+    warp_axis<T, A0, A1, A2, 0, A0>(in, S(C, 0, TR), out, lane);
     __syncwarp();
-    warp_axis<T, A0, A1, A2, 1, A1, A1, TR>(out, S(C, 1), tmp, lane);
+    warp_axis<T, A0, A1, A2, 1, A1>(out, S(C, 1, TR), tmp, lane);
     __syncwarp();
-    warp_axis<T, A0, A1, A2, 2, A2, A2, TR>(tmp, S(C, 2), out, lane);
+    warp_axis<T, A0, A1, A2, 2, A2>(tmp, S(C, 2, TR), out, lane);
     __syncwarp();
   }
   // pressure (NO^3) -> eigen space of component C: out = (G0 (x) G1 (x) G2)^T in
@@ -121,11 +159,11 @@ struct Patch {
   __device__ void gt3(const T* in, T* out, T* tmp) const {
     constexpr int NO = P::NO;
     constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, NO, NO, NO, 0, A0, A0, true>(in, G(C, 0), out, lane);
+    warp_axis<T, NO, NO, NO, 0, A0>(in, G(C, 0, true), out, lane);
     __syncwarp();
-    warp_axis<T, A0, NO, NO, 1, A1, A1, true>(out, G(C, 1), tmp, lane);
+    warp_axis<T, A0, NO, NO, 1, A1>(out, G(C, 1, true), tmp, lane);
     __syncwarp();
-    warp_axis<T, A0, A1, NO, 2, A2, A2, true>(tmp, G(C, 2), out, lane);
+    warp_axis<T, A0, A1, NO, 2, A2>(tmp, G(C, 2, true), out, lane);
     __syncwarp();
   }
   // eigen space of component C -> pressure: out = (G0 (x) G1 (x) G2) in
@@ -133,11 +171,11 @@ struct Patch {
   __device__ void g3(const T* in, T* out, T* tmp) const {
     constexpr int NO = P::NO;
     constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, A0, A1, A2, 0, NO, A0, false>(in, G(C, 0), out, lane);
+    warp_axis<T, A0, A1, A2, 0, NO>(in, G(C, 0, false), out, lane);
     __syncwarp();
-    warp_axis<T, NO, A1, A2, 1, NO, A1, false>(out, G(C, 1), tmp, lane);
+    warp_axis<T, NO, A1, A2, 1, NO>(out, G(C, 1, false), tmp, lane);
     __syncwarp();
-    warp_axis<T, NO, NO, A2, 2, NO, A2, false>(tmp, G(C, 2), out, lane);
+    warp_axis<T, NO, NO, A2, 2, NO>(tmp, G(C, 2, false), out, lane);
     __syncwarp();
   }
   // t *= Lambda_C^-1 (eigen space of component C)
@@ -241,11 +279,11 @@ __global__ void __launch_bounds__(32 * W) patch_smooth_kernel(T* __restrict__ x,
   auto precond = [&](const T* rr, T* zz) {
     if (cg_precond) {
       const T* Mi = tab + P::MPI;
-      warp_axis<T, NO, NO, NO, 0, NO, NO, false>(rr, Mi, zz, lane);
+      warp_axis<T, NO, NO, NO, 0, NO>(rr, Mi, zz, lane);
       __syncwarp();
-      warp_axis<T, NO, NO, NO, 1, NO, NO, false>(zz, Mi, T1, lane);
+      warp_axis<T, NO, NO, NO, 1, NO>(zz, Mi, T1, lane);
       __syncwarp();
-      warp_axis<T, NO, NO, NO, 2, NO, NO, false>(T1, Mi, zz, lane);
+      warp_axis<T, NO, NO, NO, 2, NO>(T1, Mi, zz, lane);
       __syncwarp();
     } else {
       for (int o = lane; o < P::NPR; o += 32) zz[o] = rr[o];
@@ -350,35 +388,45 @@ void launch_smooth_colour(Context& ctx, int level, int prec, int colour, void* x
   else launch_prec<float>(ctx, level, colour, x, r);
 }
 
-// packed patch table (order of PD<K> offsets)
+// packed patch table (order of PD<K> offsets): every matrix as padded rows of M and of M^T
 std::vector<double> pack_patch_tables(const PatchTables& P) {
   const int k = P.k, NP = 2 * k + 1, NO = 2 * k + 2;
   std::vector<double> t;
-  for (int i = 0; i < NP; ++i)
-    for (int j = 0; j < NP; ++j) t.push_back(P.par_S(i, j));
-  for (int i = 0; i < NP; ++i) t.push_back(P.par_lam[i]);
-  for (int v = 0; v < 4; ++v)
-    for (int i = 0; i < NO; ++i)
-      for (int j = 0; j < NO; ++j) t.push_back(P.orth_S[v](i, j));
-  for (int v = 0; v < 4; ++v)
-    for (int i = 0; i < NO; ++i) t.push_back(P.orth_lam[v][i]);
-  // G_par = D S_par  (NO x NP)
+  auto rows = [&](int nr, int nc, auto f) {  // rows of an nr x nc matrix, padded to R4(nc)
+    for (int i = 0; i < nr; ++i)
+      for (int j = 0; j < R4(nc); ++j) t.push_back(j < nc ? f(i, j) : 0.0);
+  };
+  auto vec = [&](const std::vector<double>& v) {
+    for (int j = 0; j < R4(static_cast<int>(v.size())); ++j) t.push_back(j < static_cast<int>(v.size()) ? v[j] : 0.0);
+  };
+  Dense Gp(NO, NP);  // D S_par
   for (int i = 0; i < NO; ++i)
     for (int j = 0; j < NP; ++j) {
       double s = 0.0;
       for (int l = 0; l < NP; ++l) s += P.D(i, l) * P.par_S(l, j);
-      t.push_back(s);
+      Gp(i, j) = s;
     }
-  // G_orth[v] = M' S_orth[v]  (NO x NO)
-  for (int v = 0; v < 4; ++v)
+  Dense Go[4];  // M' S_orth[v]
+  for (int v = 0; v < 4; ++v) {
+    Go[v] = Dense(NO, NO);
     for (int i = 0; i < NO; ++i)
       for (int j = 0; j < NO; ++j) {
         double s = 0.0;
         for (int l = 0; l < NO; ++l) s += P.Mp(i, l) * P.orth_S[v](l, j);
-        t.push_back(s);
+        Go[v](i, j) = s;
       }
-  for (int i = 0; i < NO; ++i)
-    for (int j = 0; j < NO; ++j) t.push_back(P.Mpinv(i, j));
+  }
+  rows(NP, NP, [&](int i, int j) { return P.par_S(i, j); });
+  rows(NP, NP, [&](int i, int j) { return P.par_S(j, i); });
+  vec(P.par_lam);
+  for (int v = 0; v < 4; ++v) rows(NO, NO, [&](int i, int j) { return P.orth_S[v](i, j); });
+  for (int v = 0; v < 4; ++v) rows(NO, NO, [&](int i, int j) { return P.orth_S[v](j, i); });
+  for (int v = 0; v < 4; ++v) vec(P.orth_lam[v]);
+  rows(NO, NP, [&](int i, int j) { return Gp(i, j); });
+  rows(NP, NO, [&](int i, int j) { return Gp(j, i); });
+  for (int v = 0; v < 4; ++v) rows(NO, NO, [&](int i, int j) { return Go[v](i, j); });
+  for (int v = 0; v < 4; ++v) rows(NO, NO, [&](int i, int j) { return Go[v](j, i); });
+  rows(NO, NO, [&](int i, int j) { return P.Mpinv(i, j); });
   return t;
 }
 
