@@ -206,8 +206,8 @@ struct Patch {
   }
 };
 
-template <typename T, int K, int W>
-__global__ void __launch_bounds__(32 * W) patch_smooth_kernel(T* __restrict__ x, const T* __restrict__ r,
+template <typename T, int K, int W, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB) patch_smooth_kernel(T* __restrict__ x, const T* __restrict__ r,
                                                               const T* __restrict__ ptab, int m, int colour,
                                                               int cg_max_iter, T cg_tol, int cg_fixed,
                                                               int cg_precond) {
@@ -361,7 +361,10 @@ void launch_k(Context& ctx, int level, int colour, void* x, const void* r) {
   const int npatch = cnt(colour & 1) * cnt((colour >> 1) & 1) * cnt((colour >> 2) & 1);
   if (npatch <= 0) return;
   const size_t smem = sizeof(T) * (P::TABP + W * P::WS);
-  auto kern = patch_smooth_kernel<T, K, W>;
+  // as many resident CTAs as shared memory allows (up to 3): registers are capped accordingly
+  constexpr size_t smem_c = sizeof(T) * (P::TABP + W * P::WS) + 1024;
+  constexpr int MINB = smem_c * 3 <= 233472 ? 3 : (smem_c * 2 <= 233472 ? 2 : 1);
+  auto kern = patch_smooth_kernel<T, K, W, MINB>;
   SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<(npatch + W - 1) / W, 32 * W, smem, ctx.stream>>>(
       static_cast<T*>(x), static_cast<const T*>(r), static_cast<const T*>(dl.patch), m, colour, ctx.cfg.cg_max_iter,
