@@ -69,7 +69,7 @@ struct Vec16<double> {
 // out = (M applied along axis AX) in;  in dims (D0,D1,D2), out extent along AX = R.
 // M(i,j) = A[i * R4(C) + j] (rows padded to 16 B). One pencil per lane; the coefficients of output i
 // are read as 16-byte vectors (broadcast LDS.128).
-template <typename T, int D0, int D1, int D2, int AX, int R>
+template <typename T, int D0, int D1, int D2, int AX, int R, int GS>
 __device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __restrict__ A, T* __restrict__ out,
                                           int lane) {
   constexpr int DI[3] = {D0, D1, D2};
@@ -79,7 +79,7 @@ __device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __r
   constexpr int SO = AX == 0 ? 1 : (AX == 1 ? DO0 : DO0 * DO1);
   constexpr int QA = AX == 0 ? D1 : D0;  // the two other axes, in order
   constexpr int NPEN = D0 * D1 * D2 / C;
-  for (int p = lane; p < NPEN; p += 32) {
+  for (int p = lane; p < NPEN; p += GS) {
     const int u = p % QA, v = p / QA;
     int bi, bo;
     if (AX == 0) {
@@ -126,7 +126,32 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-template <typename T, int K>
+// a patch is solved by a group of GS threads: one warp (GS = 32, many patches per CTA, warp-synchronous)
+// or a whole CTA (GS > 32, coarse levels where there are too few patches to fill the GPU and the
+// per-patch latency dominates)
+template <int GS>
+__device__ __forceinline__ void gsync() {
+  if constexpr (GS == 32) gsync<GS>();
+  else __syncthreads();
+}
+template <int GS, typename T>
+__device__ __forceinline__ T group_sum(T v) {
+  v = warp_sum(v);
+  if constexpr (GS == 32) {
+    return v;
+  } else {
+    __shared__ T red[GS / 32];
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    T s = T(0);
+#pragma unroll
+    for (int w = 0; w < GS / 32; ++w) s += red[w];
+    return s;
+  }
+}
+
+template <typename T, int K, int GS>
 struct Patch {
   using P = PD<K>;
   const T* tab;
@@ -147,36 +172,36 @@ struct Patch {
   template <int C, bool TR>
   __device__ void s3(const T* in, T* out, T* tmp) const {
     constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, A0, A1, A2, 0, A0>(in, S(C, 0, TR), out, lane);
-    __syncwarp();
-    warp_axis<T, A0, A1, A2, 1, A1>(out, S(C, 1, TR), tmp, lane);
-    __syncwarp();
-    warp_axis<T, A0, A1, A2, 2, A2>(tmp, S(C, 2, TR), out, lane);
-    __syncwarp();
+    warp_axis<T, A0, A1, A2, 0, A0, GS>(in, S(C, 0, TR), out, lane);
+    gsync<GS>();
+    warp_axis<T, A0, A1, A2, 1, A1, GS>(out, S(C, 1, TR), tmp, lane);
+    gsync<GS>();
+    warp_axis<T, A0, A1, A2, 2, A2, GS>(tmp, S(C, 2, TR), out, lane);
+    gsync<GS>();
   }
   // pressure (NO^3) -> eigen space of component C: out = (G0 (x) G1 (x) G2)^T in
   template <int C>
   __device__ void gt3(const T* in, T* out, T* tmp) const {
     constexpr int NO = P::NO;
     constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, NO, NO, NO, 0, A0>(in, G(C, 0, true), out, lane);
-    __syncwarp();
-    warp_axis<T, A0, NO, NO, 1, A1>(out, G(C, 1, true), tmp, lane);
-    __syncwarp();
-    warp_axis<T, A0, A1, NO, 2, A2>(tmp, G(C, 2, true), out, lane);
-    __syncwarp();
+    warp_axis<T, NO, NO, NO, 0, A0, GS>(in, G(C, 0, true), out, lane);
+    gsync<GS>();
+    warp_axis<T, A0, NO, NO, 1, A1, GS>(out, G(C, 1, true), tmp, lane);
+    gsync<GS>();
+    warp_axis<T, A0, A1, NO, 2, A2, GS>(tmp, G(C, 2, true), out, lane);
+    gsync<GS>();
   }
   // eigen space of component C -> pressure: out = (G0 (x) G1 (x) G2) in
   template <int C>
   __device__ void g3(const T* in, T* out, T* tmp) const {
     constexpr int NO = P::NO;
     constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, A0, A1, A2, 0, NO>(in, G(C, 0, false), out, lane);
-    __syncwarp();
-    warp_axis<T, NO, A1, A2, 1, NO>(out, G(C, 1, false), tmp, lane);
-    __syncwarp();
-    warp_axis<T, NO, NO, A2, 2, NO>(tmp, G(C, 2, false), out, lane);
-    __syncwarp();
+    warp_axis<T, A0, A1, A2, 0, NO, GS>(in, G(C, 0, false), out, lane);
+    gsync<GS>();
+    warp_axis<T, NO, A1, A2, 1, NO, GS>(out, G(C, 1, false), tmp, lane);
+    gsync<GS>();
+    warp_axis<T, NO, NO, A2, 2, NO, GS>(tmp, G(C, 2, false), out, lane);
+    gsync<GS>();
   }
   // t *= Lambda_C^-1 (eigen space of component C)
   template <int C>
@@ -185,29 +210,29 @@ struct Patch {
     const T* l0 = L(C, 0);
     const T* l1 = L(C, 1);
     const T* l2 = L(C, 2);
-    for (int o = lane; o < P::NV; o += 32) {
+    for (int o = lane; o < P::NV; o += GS) {
       const int x = o % A0, y = (o / A0) % A1, z = o / (A0 * A1);
       t[o] = t[o] / (l0[x] + l1[y] + l2[z]);
     }
-    __syncwarp();
+    gsync<GS>();
   }
   __device__ void project(T* p) const {
     T s = T(0);
-    for (int o = lane; o < P::NPR; o += 32) s += p[o];
-    s = warp_sum(s) / T(P::NPR);
-    __syncwarp();
-    for (int o = lane; o < P::NPR; o += 32) p[o] -= s;
-    __syncwarp();
+    for (int o = lane; o < P::NPR; o += GS) s += p[o];
+    s = group_sum<GS>(s) / T(P::NPR);
+    gsync<GS>();
+    for (int o = lane; o < P::NPR; o += GS) p[o] -= s;
+    gsync<GS>();
   }
   __device__ T dot(const T* a, const T* b) const {
     T s = T(0);
-    for (int o = lane; o < P::NPR; o += 32) s += a[o] * b[o];
-    return warp_sum(s);
+    for (int o = lane; o < P::NPR; o += GS) s += a[o] * b[o];
+    return group_sum<GS>(s);
   }
 };
 
-template <typename T, int K, int W, int MINB>
-__global__ void __launch_bounds__(32 * W, MINB) patch_smooth_kernel(T* __restrict__ x, const T* __restrict__ r,
+template <typename T, int K, int W, int MINB, int GS>
+__global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(T* __restrict__ x, const T* __restrict__ r,
                                                               const T* __restrict__ ptab, int m, int colour,
                                                               int cg_max_iter, T cg_tol, int cg_fixed,
                                                               int cg_precond) {
@@ -217,7 +242,7 @@ __global__ void __launch_bounds__(32 * W, MINB) patch_smooth_kernel(T* __restric
   T* tab = reinterpret_cast<T*>(smem_raw);
   for (int i = threadIdx.x; i < P::TAB; i += blockDim.x) tab[i] = ptab[i];
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x / GS, lane = threadIdx.x % GS;  // patch slot in the CTA, thread in its group
   const int cnt[3] = {(colour & 1) ? m / 2 : m / 2 - 1, ((colour >> 1) & 1) ? m / 2 : m / 2 - 1,
                       ((colour >> 2) & 1) ? m / 2 : m / 2 - 1};
   const int npatch = cnt[0] * cnt[1] * cnt[2];
@@ -235,7 +260,7 @@ __global__ void __launch_bounds__(32 * W, MINB) patch_smooth_kernel(T* __restric
   T* T1 = Px + P::NPR;       // scratch (BIG)
   T* T2 = T1 + P::BIG;       // scratch (BIG)
 
-  Patch<T, K> ps;
+  Patch<T, K, GS> ps;
   ps.tab = tab;
   ps.lane = lane;
   for (int a = 0; a < 3; ++a) ps.var[a] = 2 * (v[a] == 1) + (v[a] == m - 1);
@@ -259,44 +284,44 @@ __global__ void __launch_bounds__(32 * W, MINB) patch_smooth_kernel(T* __restric
 #define SMG_FOR_C(...) \
   { constexpr int C = 0; __VA_ARGS__ } { constexpr int C = 1; __VA_ARGS__ } { constexpr int C = 2; __VA_ARGS__ }
   SMG_FOR_C({
-    for (int o = lane; o < P::NV; o += 32) T1[o] = r[vel_index(C, o)];
-    __syncwarp();
+    for (int o = lane; o < P::NV; o += GS) T1[o] = r[vel_index(C, o)];
+    gsync<GS>();
     ps.template s3<C, true>(T1, Fh + C * P::NV, T2);
   })
-  for (int o = lane; o < P::NPR; o += 32) Pq[o] = r[pres_index(o)];
+  for (int o = lane; o < P::NPR; o += GS) Pq[o] = r[pres_index(o)];
   // ---- rhs = sum_c G_c Lambda_c^-1 Fh_c - G  (projected) -> Pr ----
-  for (int o = lane; o < P::NPR; o += 32) Pr[o] = -Pq[o];
-  __syncwarp();
+  for (int o = lane; o < P::NPR; o += GS) Pr[o] = -Pq[o];
+  gsync<GS>();
   SMG_FOR_C({
-    for (int o = lane; o < P::NV; o += 32) T1[o] = Fh[C * P::NV + o];
-    __syncwarp();
+    for (int o = lane; o < P::NV; o += GS) T1[o] = Fh[C * P::NV + o];
+    gsync<GS>();
     ps.template lam_inv<C>(T1);
     ps.template g3<C>(T1, T2, Pq);  // result in T2 (Pq used as scratch)
-    for (int o = lane; o < P::NPR; o += 32) Pr[o] += T2[o];
-    __syncwarp();
+    for (int o = lane; o < P::NPR; o += GS) Pr[o] += T2[o];
+    gsync<GS>();
   })
   ps.project(Pr);
   auto precond = [&](const T* rr, T* zz) {
     if (cg_precond) {
       const T* Mi = tab + P::MPI;
-      warp_axis<T, NO, NO, NO, 0, NO>(rr, Mi, zz, lane);
-      __syncwarp();
-      warp_axis<T, NO, NO, NO, 1, NO>(zz, Mi, T1, lane);
-      __syncwarp();
-      warp_axis<T, NO, NO, NO, 2, NO>(T1, Mi, zz, lane);
-      __syncwarp();
+      warp_axis<T, NO, NO, NO, 0, NO, GS>(rr, Mi, zz, lane);
+      gsync<GS>();
+      warp_axis<T, NO, NO, NO, 1, NO, GS>(zz, Mi, T1, lane);
+      gsync<GS>();
+      warp_axis<T, NO, NO, NO, 2, NO, GS>(T1, Mi, zz, lane);
+      gsync<GS>();
     } else {
-      for (int o = lane; o < P::NPR; o += 32) zz[o] = rr[o];
-      __syncwarp();
+      for (int o = lane; o < P::NPR; o += GS) zz[o] = rr[o];
+      gsync<GS>();
     }
     ps.project(zz);
   };
   precond(Pr, Pz);
-  for (int o = lane; o < P::NPR; o += 32) {
+  for (int o = lane; o < P::NPR; o += GS) {
     Pd[o] = Pz[o];
     Px[o] = T(0);
   }
-  __syncwarp();
+  gsync<GS>();
   T rz = ps.dot(Pr, Pz);
   const T r0 = sqrt(ps.dot(Pr, Pr));
   for (int it = 0; it < cg_max_iter; ++it) {
@@ -304,43 +329,43 @@ __global__ void __launch_bounds__(32 * W, MINB) patch_smooth_kernel(T* __restric
       if (sqrt(ps.dot(Pr, Pr)) <= cg_tol * r0) break;
     }
     // Pq = S Pd = sum_c G_c Lambda_c^-1 G_c^T Pd
-    for (int o = lane; o < P::NPR; o += 32) Pq[o] = T(0);
-    __syncwarp();
+    for (int o = lane; o < P::NPR; o += GS) Pq[o] = T(0);
+    gsync<GS>();
     SMG_FOR_C({
       ps.template gt3<C>(Pd, T1, T2);
       ps.template lam_inv<C>(T1);
       ps.template g3<C>(T1, T2, Pz);  // result in T2; Pz is free scratch here (recomputed below)
-      for (int o = lane; o < P::NPR; o += 32) Pq[o] += T2[o];
-      __syncwarp();
+      for (int o = lane; o < P::NPR; o += GS) Pq[o] += T2[o];
+      gsync<GS>();
     })
     const T dq = ps.dot(Pd, Pq);
     if (!(dq > T(0)) || rz == T(0)) break;
     const T alpha = rz / dq;
-    for (int o = lane; o < P::NPR; o += 32) {
+    for (int o = lane; o < P::NPR; o += GS) {
       Px[o] += alpha * Pd[o];
       Pr[o] -= alpha * Pq[o];
     }
-    __syncwarp();
+    gsync<GS>();
     ps.project(Pr);
     precond(Pr, Pz);
     const T rzn = ps.dot(Pr, Pz);
     const T beta = rzn / rz;
     rz = rzn;
-    for (int o = lane; o < P::NPR; o += 32) Pd[o] = Pz[o] + beta * Pd[o];
-    __syncwarp();
+    for (int o = lane; o < P::NPR; o += GS) Pd[o] = Pz[o] + beta * Pd[o];
+    gsync<GS>();
   }
   ps.project(Px);
   // ---- U_c = (S (x) S (x) S) Lambda_c^-1 [Fh_c - G_c^T P];  x += R^T (U, P) ----
   SMG_FOR_C({
     ps.template gt3<C>(Px, T1, T2);
-    for (int o = lane; o < P::NV; o += 32) T1[o] = Fh[C * P::NV + o] - T1[o];
-    __syncwarp();
+    for (int o = lane; o < P::NV; o += GS) T1[o] = Fh[C * P::NV + o] - T1[o];
+    gsync<GS>();
     ps.template lam_inv<C>(T1);
     ps.template s3<C, false>(T1, T2, Pz);
-    for (int o = lane; o < P::NV; o += 32) x[vel_index(C, o)] += T2[o];
+    for (int o = lane; o < P::NV; o += GS) x[vel_index(C, o)] += T2[o];
   })
 #undef SMG_FOR_C
-  for (int o = lane; o < P::NPR; o += 32) x[pres_index(o)] += Px[o];
+  for (int o = lane; o < P::NPR; o += GS) x[pres_index(o)] += Px[o];
 }
 
 template <typename T, int K>
@@ -351,26 +376,38 @@ constexpr int warps_per_cta() {
   return w >= 8 ? 8 : (w >= 4 ? 4 : (w >= 2 ? 2 : 1));
 }
 
+template <typename T, int K, int W, int GS>
+void launch_group(Context& ctx, const DevLevel& dl, int npatch, int colour, void* x, const void* r) {
+  using P = PD<K>;
+  const size_t smem = sizeof(T) * (P::TABP + W * P::WS);
+  // as many resident CTAs as shared memory allows (up to 3): registers are capped accordingly
+  constexpr size_t smem_c = sizeof(T) * (P::TABP + W * P::WS) + 1024;
+  constexpr int MINB = smem_c * 3 <= 233472 ? 3 : (smem_c * 2 <= 233472 ? 2 : 1);
+  auto kern = patch_smooth_kernel<T, K, W, MINB, GS>;
+  static bool attr = false;
+  if (!attr) {
+    SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr = true;
+  }
+  kern<<<(npatch + W - 1) / W, GS * W, smem, ctx.stream>>>(
+      static_cast<T*>(x), static_cast<const T*>(r), static_cast<const T*>(dl.patch), dl.lay.m, colour,
+      ctx.cfg.cg_max_iter, static_cast<T>(ctx.cfg.cg_tol), ctx.cfg.cg_fixed, ctx.cfg.cg_precond);
+  SMG_CUDA(cudaGetLastError());
+  ++ctx.launches;
+}
+
 template <typename T, int K>
 void launch_k(Context& ctx, int level, int colour, void* x, const void* r) {
-  using P = PD<K>;
-  constexpr int W = warps_per_cta<T, K>();
   const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
   const int m = dl.lay.m;
   auto cnt = [&](int bit) { return bit ? m / 2 : m / 2 - 1; };
   const int npatch = cnt(colour & 1) * cnt((colour >> 1) & 1) * cnt((colour >> 2) & 1);
   if (npatch <= 0) return;
-  const size_t smem = sizeof(T) * (P::TABP + W * P::WS);
-  // as many resident CTAs as shared memory allows (up to 3): registers are capped accordingly
-  constexpr size_t smem_c = sizeof(T) * (P::TABP + W * P::WS) + 1024;
-  constexpr int MINB = smem_c * 3 <= 233472 ? 3 : (smem_c * 2 <= 233472 ? 2 : 1);
-  auto kern = patch_smooth_kernel<T, K, W, MINB>;
-  SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  kern<<<(npatch + W - 1) / W, 32 * W, smem, ctx.stream>>>(
-      static_cast<T*>(x), static_cast<const T*>(r), static_cast<const T*>(dl.patch), m, colour, ctx.cfg.cg_max_iter,
-      static_cast<T>(ctx.cfg.cg_tol), ctx.cfg.cg_fixed, ctx.cfg.cg_precond);
-  SMG_CUDA(cudaGetLastError());
-  ++ctx.launches;
+  // few patches (coarse levels): a 4-warp CTA per patch cuts the per-patch latency; many patches: one
+  // warp per patch, several per CTA
+  if (npatch <= 148) launch_group<T, K, 1, 256>(ctx, dl, npatch, colour, x, r);
+  else if (npatch < 148 * 8) launch_group<T, K, 1, 128>(ctx, dl, npatch, colour, x, r);
+  else launch_group<T, K, warps_per_cta<T, K>(), 32>(ctx, dl, npatch, colour, x, r);
 }
 
 template <typename T>
