@@ -463,45 +463,12 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
 
   constexpr int SQ2 = seg_cells(NO2, K), SQ = seg_cells(NO1, K), S1 = seg_cells(NO2, K), S2 = seg_cells(NO1, K),
                 S3 = seg_cells(NCc, K);
-  // ---- Q2 = M_o2 p over c in [-H, N_c), o1 owned, o2 owned (from the P box) ----
-  {
-    T* sQ2 = sA1;
-    constexpr int E1P = BR::N(1) + H;
-    constexpr int PSC = BR::stride(C, BR::PXT, E1P), PSO1 = BR::stride(O1, BR::PXT, E1P),
-                  PSO2 = BR::stride(O2, BR::PXT, E1P);
-    constexpr int NL = (Nc + H) * No1;
-    const int psh = brick_shift<T>(G, H);
-    for (int it = tid; it < NL * (NO2 / SQ2); it += NT) {
-      const int e2 = (it / NL) * SQ2, r = it % NL;
-      // consecutive items walk the P-box x axis (c for C=0, o1 otherwise): conflict-free
-      const int ci = C == 0 ? r % (Nc + H) : r / No1;
-      const int oi = C == 0 ? r / (Nc + H) : r % No1;
-      const T* src = sP + psh + ci * PSC + (oi + H) * PSO1 + (e2 + 1) * H * PSO2;
-      T cu[SQ2 * H], out[SQ2 * H];
-#pragma unroll
-      for (int j = 0; j < SQ2 * H; ++j) cu[j] = src[j * PSO2];
-      seg_mass<T, K, SQ2>(cu, out);
-#pragma unroll
-      for (int a = 0; a < SQ2 * H; ++a) sQ2[((e2 * H + a) * No1 + oi) * PC + ci] = out[a];
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, barP, X, M, *Gn);
-    if (!TMA && C == 2) cp_async_commit();
-    // Q = M_o1 Q2
-    constexpr int NL2 = (Nc + H) * No2;
-    for (int it = tid; it < NL2 * (NO1 / SQ); it += NT) {
-      const int e1 = (it / NL2) * SQ, r = it % NL2;
-      const int ci = r % (Nc + H), oj = r / (Nc + H);
-      T cu[SQ * H], out[SQ * H];
-#pragma unroll
-      for (int j = 0; j < SQ * H; ++j) cu[j] = sQ2[(oj * No1 + e1 * H + j) * PC + ci];
-      seg_mass<T, K, SQ>(cu, out);
-#pragma unroll
-      for (int a = 0; a < SQ * H; ++a) sQ[(oj * No1 + e1 * H + a) * PC + ci] = out[a];
-    }
-    __syncthreads();
-  }
+  // Q = M_o1 M_o2 p (c in [-H, N_c), o1 / o2 owned) is computed inside passes 1 and 2: Q2 = M_o2 p
+  // with the B1 items, then Q = M_o1 Q2 in place (block-diagonal mass: same cell block) with the S/T
+  // items -- no separate passes or barriers for the pressure.
+  constexpr int E1P = BR::N(1) + H;
+  constexpr int PSC = BR::stride(C, BR::PXT, E1P), PSO1 = BR::stride(O1, BR::PXT, E1P),
+                PSO2 = BR::stride(O2, BR::PXT, E1P);
   if constexpr (!BR::DB) {
     // single-buffer mode: U of this component was issued during the previous component's passes 2-3
     if (TMA) {
@@ -542,6 +509,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       for (int a = 0; a < S1 * H; ++a) sA1[((e2 * H + a) * LO1H + oi) * PC + ci] = out[a];
     }
     const int cell_o2 = G.c0[O2];
+    const int psh = brick_shift<T>(G, H);
     auto passB = [&](auto bnd) {
       constexpr bool BND = decltype(bnd)::value;
       constexpr int NLB = LC * No1;
@@ -557,20 +525,33 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         seg_sipg<T, K, S1, BND>(in, out, eg == 0 ? 0 : -1, (m - 1 - eg < S1) ? m - 1 - eg : -1);
 #pragma unroll
         for (int a = 0; a < S1 * H; ++a) sB1[((e2 * H + a) * No1 + o) * PC + ci] = out[a];
+        if (ci < Nc + H) {  // Q2 = M_o2 p at the same (c, o1, o2-segment); the P box has the same origin
+          const T* ps = sP + psh + ci * PSC + (o + H) * PSO1 + (e2 + 1) * H * PSO2;
+          T pc[S1 * H], q2[S1 * H];
+#pragma unroll
+          for (int j = 0; j < S1 * H; ++j) pc[j] = ps[j * PSO2];
+          seg_mass<T, K, S1>(pc, q2);
+#pragma unroll
+          for (int a = 0; a < S1 * H; ++a) sQ[((e2 * H + a) * No1 + o) * PC + ci] = q2[a];
+        }
       }
     };
     if (cell_o2 == 0 || cell_o2 + NO2 >= m) passB(bool_c<true>());
     else passB(bool_c<false>());
   }
   if constexpr (!BR::DB) {
-    fence_proxy_async();  // generic reads of U happen-before the async-proxy writes of the next staging
+    fence_proxy_async();  // generic reads of U / P happen-before the async-proxy writes of the next staging
     __syncthreads();
+    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, barP, X, M, *Gn);
     if (nextC == 0) issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sU, barU, X, M, *Gnext);
     else if (nextC == 1) issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA>(sU, barU, X, M, *Gnext);
     else if (nextC == 2) issue_u<T, K, BX, BY, BZ, OCC, NT, 2, TMA>(sU, barU, X, M, *Gnext);
     if (!TMA) cp_async_commit();
   } else {
+    fence_proxy_async();
     __syncthreads();
+    if (C == 2 && Gn != nullptr) issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, barP, X, M, *Gn);
+    if (!TMA && C == 2) cp_async_commit();
   }
   // ---- pass 2 (along o1): S = M_o1 A1, T = L_o1 A1 + M_o1 B1 (c full, o1/o2 owned) ----
   {
@@ -600,6 +581,15 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         for (int a = 0; a < S2 * H; ++a) {
           sS[(oj * No1 + e1 * H + a) * PC + ci] = sv[a];
           sT[(oj * No1 + e1 * H + a) * PC + ci] = tv[a] + mb[a];
+        }
+        if (ci < Nc + H) {  // Q = M_o1 Q2 in place
+          T* q = sQ + (oj * No1 + e1 * H) * PC + ci;
+          T q2[S2 * H], qq[S2 * H];
+#pragma unroll
+          for (int j = 0; j < S2 * H; ++j) q2[j] = q[j * PC];
+          seg_mass<T, K, S2>(q2, qq);
+#pragma unroll
+          for (int j = 0; j < S2 * H; ++j) q[j * PC] = qq[j];
         }
       }
     };
