@@ -664,7 +664,19 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
           T z = T(0);
 #pragma unroll
           for (int bq = 0; bq < P; ++bq) z += cref<T>(R::D + i * P + bq) * s[ee * H + H + bq];
-          yp[(e * H + i) * YSC] += h2 * z;
+          // y_p = h^2 (D_x S_x + D_y S_y + D_z S_z): component 0 stores, 1 accumulates, 2 writes HBM
+          if (C == 0) {
+            yp[(e * H + i) * YSC] = h2 * z;
+          } else if (C == 1) {
+            yp[(e * H + i) * YSC] += h2 * z;
+          } else {
+            const int gz = G.g0[2] + e * H + i;
+            if (inside && gz < G.nlim[2]) {
+              const int64_t gi = (static_cast<int64_t>(gz) * n + g[1]) * n + g[0];
+              const T vp = yp[(e * H + i) * YSC] + h2 * z;
+              Y.c[3][gi] = RESID ? B.c[3][gi] - vp : vp;
+            }
+          }
         }
       }
       // the constrained plane g_c = n belongs to the brick holding the last cell along c
@@ -699,24 +711,10 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
   __syncthreads();
 }
 
-// write the pressure rows of this brick from the smem accumulator
-template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, bool RESID>
-__device__ __forceinline__ void write_pressure(const T* sYP, const Geo& G, T* __restrict__ y, const T* __restrict__ b) {
-  using BR = Brick<T, K, BX, BY, BZ, OCC>;
-  constexpr int N0 = BR::N(0), N1 = BR::N(1), N2 = BR::N(2);
-  const int n = G.n;
-  for (int i = threadIdx.x; i < N0 * N1 * N2; i += NT) {
-    const int lx = i % N0, ly = (i / N0) % N1, lz = i / (N0 * N1);
-    const int gx = G.g0[0] + lx, gy = G.g0[1] + ly, gz = G.g0[2] + lz;
-    if (gx >= n || gy >= G.nlim[1] || gz >= G.nlim[2]) continue;
-    const int64_t gi = (static_cast<int64_t>(gz) * n + gy) * n + gx;
-    const T v = sYP[(lz * N1 + ly) * BR::YX + lx];
-    y[gi] = RESID ? b[gi] - v : v;
-  }
-}
-
-__device__ __forceinline__ void brick_geo(Geo& G, int brick, int nbx, int nby, int bx, int by, int bz, int H, int zc0) {
-  const int ix = brick % nbx, iy = (brick / nbx) % nby, iz = brick / (nbx * nby);
+__device__ __forceinline__ void brick_geo(Geo& G, int brick, int lnbx, int lnby, int bx, int by, int bz, int H,
+                                          int zc0) {
+  // bricks per x / y row are powers of two (m and the brick sizes are): shifts, no integer division
+  const int ix = brick & ((1 << lnbx) - 1), iy = (brick >> lnbx) & ((1 << lnby) - 1), iz = brick >> (lnbx + lnby);
   G.c0[0] = ix * bx;
   G.c0[1] = iy * by;
   G.c0[2] = zc0 + iz * bz;
@@ -739,6 +737,7 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (BR::BYTES - 3 * 8));  // [buf0, buf1, P]
   // bricks cover the cells [0, m)^2 x [zc0, zc1) (the whole level, or the cells a z-slab owns)
   const int nbx = (m + BX - 1) / BX, nby = (m + BY - 1) / BY, nbz = (zc1 - zc0 + BZ - 1) / BZ;
+  const int lnbx = 31 - __clz(nbx), lnby = 31 - __clz(nby);
   const int nbricks = nbx * nby * nbz;
   Geo G, Gn;
   G.m = Gn.m = m;
@@ -753,7 +752,6 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
     Gn.mlim[a] = G.mlim[a];
   }
   T* sP = sm + BR::OFF_P;
-  T* sYP = sm + BR::OFF_YP;
   const Maps& maps = *mapsp;  // tensor maps live in global memory (64-B aligned slots)
   int brick = blockIdx.x;
   if (brick >= nbricks) return;
@@ -765,7 +763,7 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
   }
   fence_proxy_async();
   __syncthreads();
-  brick_geo(G, brick, nbx, nby, BX, BY, BZ, H, zc0);
+  brick_geo(G, brick, lnbx, lnby, BX, BY, BZ, H, zc0);
   issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, &bars[2], X, maps, G);
   issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sm, &bars[0], X, maps, G);
   if (!TMA) cp_async_commit();
@@ -776,8 +774,7 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
     for (; brick < nbricks; brick += gridDim.x) {
       const int next = brick + gridDim.x;
       const bool has_next = next < nbricks;
-      if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H, zc0);
-      for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
+      if (has_next) brick_geo(Gn, next, lnbx, lnby, BX, BY, BZ, H, zc0);
       if (TMA) {
         mbar_wait(&bars[2], phP);
         phP ^= 1;
@@ -794,7 +791,6 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
                                                           &ph[0], 2, &G);
       component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, sm, G, h, has_next ? &Gn : nullptr, X, Y, B, maps,
                                                           &bars[2], &bars[0], &ph[0], has_next ? 0 : -1, &Gn);
-      write_pressure<T, K, BX, BY, BZ, OCC, NT, RESID>(sYP, G, Y.c[3], RESID ? B.c[3] : nullptr);
       __syncthreads();
       G = Gn;
     }
@@ -806,9 +802,8 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
     T* bufB = sm + (ib ? BR::OFF_U1 : 0);  // component 1, then component 0 of the next brick
     const int next = brick + gridDim.x;
     const bool has_next = next < nbricks;
-    if (has_next) brick_geo(Gn, next, nbx, nby, BX, BY, BZ, H, zc0);
+    if (has_next) brick_geo(Gn, next, lnbx, lnby, BX, BY, BZ, H, zc0);
     issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA>(bufB, &bars[ib], X, maps, G);
-    for (int i = threadIdx.x; i < BR::YP; i += NT) sYP[i] = T(0);
     if (TMA) {
       mbar_wait(&bars[2], phP);
       phP ^= 1;
@@ -853,8 +848,7 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
     }
     component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, X, Y, B, maps,
                                                    &bars[2]);
-    write_pressure<T, K, BX, BY, BZ, OCC, NT, RESID>(sYP, G, Y.c[3], RESID ? B.c[3] : nullptr);
-    __syncthreads();  // y_p accumulator is re-zeroed by the next brick
+    __syncthreads();
     G = Gn;
     u0 ^= 1;
   }
