@@ -424,6 +424,12 @@ __device__ __forceinline__ void seg_sipg(const T (&in)[(NC + 2) * (K + 1)], T (&
 }
 template <bool V>
 using bool_c = std::integral_constant<bool, V>;
+// u_x outputs (x = the pencil axis of component 0) staged in smem for coalesced x-row stores, or
+// stored directly from the pencils
+#ifndef SMG_STAGE_UX
+#define SMG_STAGE_UX 0
+#endif
+constexpr bool kStageUx = SMG_STAGE_UX;
 // cells per work item along a brick axis of nc cells: segments of 2 cells for low degrees (shared
 // neighbour loads, fewer index computations), single cells otherwise
 constexpr int seg_cells(int nc, int k) { return (nc % 2 == 0 && k <= 3) ? 2 : 1; }
@@ -645,7 +651,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
             if (a == 0) w += cref<T>(R::D + i * P + H) * q[ee * H + i];
           }
           const T val = h * v + h2 * w;
-          if (C == 0) {
+          if (C == 0 && kStageUx) {
             sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
           } else {
             g[C] = G.g0[C] + e * H + a;
@@ -680,12 +686,12 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         }
       }
       // the constrained plane g_c = n belongs to the brick holding the last cell along c
-      if (C != 0 && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
+      if ((C != 0 || !kStageUx) && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
         g[C] = n;
         yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
       }
     }
-    if (C == 0) {
+    if (C == 0 && kStageUx) {
       __syncthreads();
       // coalesced write-out of the u_x rows (x = c fastest), plus the constrained plane x = n
       const bool last = G.c0[0] + NCc >= m;
