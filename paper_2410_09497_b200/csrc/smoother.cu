@@ -48,7 +48,8 @@ struct PD {
   static constexpr int MPI = G_ORTHT + 4 * SQO;          // M'^-1 rows          NO x R4(NO)
   static constexpr int TAB = MPI + SQO;
   static constexpr int TABP = (TAB + 3) / 4 * 4;
-  // per-warp workspace: Fh (3 NV) | r z d q x (5 NPR) | T1 T2 (2 BIG)
+  static constexpr int LINV = (3 * NV + 3) / 4 * 4;  // CTA-shared reciprocal eigenvalue sums (interior)
+  // per-patch workspace: Fh (3 NV) | r z d q x (5 NPR) | T1 T2 (2 BIG)
   static constexpr int WS = 3 * NV + 5 * NPR + 2 * BIG;
   static constexpr int dv(int c, int a) { return a == c ? NP : NO; }
 };
@@ -155,6 +156,8 @@ template <typename T, int K, int GS>
 struct Patch {
   using P = PD<K>;
   const T* tab;
+  const T* linv;  // 3 x NV reciprocal eigenvalue sums of the interior variant (CTA-shared)
+  bool interior;
   int var[3];
   int lane;
 
@@ -203,16 +206,23 @@ struct Patch {
     warp_axis<T, NO, NO, A2, 2, NO, GS>(tmp, G(C, 2, false), out, lane);
     gsync<GS>();
   }
-  // t *= Lambda_C^-1 (eigen space of component C)
+  // t *= Lambda_C^-1 (eigen space of component C). Interior patches (all end variants 0, the vast
+  // majority) multiply by the reciprocal eigenvalue sums tabulated once per CTA (linv); patches at the
+  // domain boundary divide (the division inside the CG loop was 11 % of the smoother's instructions)
   template <int C>
   __device__ void lam_inv(T* t) const {
-    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1);
-    const T* l0 = L(C, 0);
-    const T* l1 = L(C, 1);
-    const T* l2 = L(C, 2);
-    for (int o = lane; o < P::NV; o += GS) {
-      const int x = o % A0, y = (o / A0) % A1, z = o / (A0 * A1);
-      t[o] = t[o] / (l0[x] + l1[y] + l2[z]);
+    if (interior) {
+      const T* li = linv + C * P::NV;
+      for (int o = lane; o < P::NV; o += GS) t[o] *= li[o];
+    } else {
+      constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1);
+      const T* l0 = L(C, 0);
+      const T* l1 = L(C, 1);
+      const T* l2 = L(C, 2);
+      for (int o = lane; o < P::NV; o += GS) {
+        const int x = o % A0, y = (o / A0) % A1, z = o / (A0 * A1);
+        t[o] = t[o] / (l0[x] + l1[y] + l2[z]);
+      }
     }
     gsync<GS>();
   }
@@ -242,6 +252,18 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(T* __restric
   T* tab = reinterpret_cast<T*>(smem_raw);
   for (int i = threadIdx.x; i < P::TAB; i += blockDim.x) tab[i] = ptab[i];
   __syncthreads();
+  {  // reciprocal eigenvalue sums of interior patches (end variant 0 on every axis), per component
+    T* li = tab + P::TABP;
+    for (int i = threadIdx.x; i < 3 * P::NV; i += blockDim.x) {
+      const int c = i / P::NV, o = i % P::NV;
+      const int A0 = P::dv(c, 0), A1 = P::dv(c, 1);
+      const int xyz[3] = {o % A0, (o / A0) % A1, o / (A0 * A1)};
+      T sum = T(0);
+      for (int a = 0; a < 3; ++a) sum += a == c ? tab[P::PAR_L + xyz[a]] : tab[P::ORTH_L + xyz[a]];
+      li[i] = T(1) / sum;
+    }
+    __syncthreads();
+  }
   const int warp = threadIdx.x / GS, lane = threadIdx.x % GS;  // patch slot in the CTA, thread in its group
   const int cnt[3] = {(colour & 1) ? m / 2 : m / 2 - 1, ((colour >> 1) & 1) ? m / 2 : m / 2 - 1,
                       ((colour >> 2) & 1) ? m / 2 : m / 2 - 1};
@@ -250,7 +272,7 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(T* __restric
   if (pid >= npatch) return;
   const int v[3] = {((colour & 1) ? 1 : 2) + 2 * (pid % cnt[0]), (((colour >> 1) & 1) ? 1 : 2) + 2 * ((pid / cnt[0]) % cnt[1]),
                     (((colour >> 2) & 1) ? 1 : 2) + 2 * (pid / (cnt[0] * cnt[1]))};
-  T* ws = tab + P::TABP + warp * P::WS;
+  T* ws = tab + P::TABP + P::LINV + warp * P::WS;
   T* Fh = ws;                // 3 x NV eigen coefficients of F_c
   T* Pr = Fh + 3 * P::NV;    // CG residual
   T* Pz = Pr + P::NPR;       // preconditioned residual
@@ -264,6 +286,8 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(T* __restric
   ps.tab = tab;
   ps.lane = lane;
   for (int a = 0; a < 3; ++a) ps.var[a] = 2 * (v[a] == 1) + (v[a] == m - 1);
+  ps.linv = tab + P::TABP;  // CTA-shared table filled above
+  ps.interior = ps.var[0] == 0 && ps.var[1] == 0 && ps.var[2] == 0;
   const int n = m * H;
   const int64_t sizeV = static_cast<int64_t>(n + 1) * n * n;
 
@@ -379,9 +403,9 @@ constexpr int warps_per_cta() {
 template <typename T, int K, int W, int GS>
 void launch_group(Context& ctx, const DevLevel& dl, int npatch, int colour, void* x, const void* r) {
   using P = PD<K>;
-  const size_t smem = sizeof(T) * (P::TABP + W * P::WS);
+  const size_t smem = sizeof(T) * (P::TABP + P::LINV + W * P::WS);
   // as many resident CTAs as shared memory allows (up to 3): registers are capped accordingly
-  constexpr size_t smem_c = sizeof(T) * (P::TABP + W * P::WS) + 1024;
+  constexpr size_t smem_c = sizeof(T) * (P::TABP + P::LINV + W * P::WS) + 1024;
   constexpr int MINB = smem_c * 3 <= 233472 ? 3 : (smem_c * 2 <= 233472 ? 2 : 1);
   auto kern = patch_smooth_kernel<T, K, W, MINB, GS>;
   static bool attr = false;
