@@ -70,7 +70,7 @@ struct Vec16<double> {
 // out = (M applied along axis AX) in;  in dims (D0,D1,D2), out extent along AX = R.
 // M(i,j) = A[i * R4(C) + j] (rows padded to 16 B). One pencil per lane; the coefficients of output i
 // are read as 16-byte vectors (broadcast LDS.128).
-template <typename T, int D0, int D1, int D2, int AX, int R, int GS>
+template <typename T, int D0, int D1, int D2, int AX, int R, int GS, bool ACC = false>
 __device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __restrict__ A, T* __restrict__ out,
                                           int lane) {
   constexpr int DI[3] = {D0, D1, D2};
@@ -115,7 +115,8 @@ __device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __r
           if (2 * q + 1 < C) s += a.y * x[2 * q + 1];
         }
       }
-      out[bo + i * SO] = s;
+      if (ACC) out[bo + i * SO] += s;
+      else out[bo + i * SO] = s;
     }
   }
 }
@@ -195,6 +196,18 @@ struct Patch {
     gsync<GS>();
   }
   // eigen space of component C -> pressure: out = (G0 (x) G1 (x) G2) in
+  // acc (=|+=) (G0 (x) G1 (x) G2) in; s1, s2 scratch
+  template <int C, bool ACC>
+  __device__ void g3acc(const T* in, T* acc, T* s1, T* s2) const {
+    constexpr int NO = P::NO;
+    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
+    warp_axis<T, A0, A1, A2, 0, NO, GS>(in, G(C, 0, false), s1, lane);
+    gsync<GS>();
+    warp_axis<T, NO, A1, A2, 1, NO, GS>(s1, G(C, 1, false), s2, lane);
+    gsync<GS>();
+    warp_axis<T, NO, NO, A2, 2, NO, GS, ACC>(s2, G(C, 2, false), acc, lane);
+    gsync<GS>();
+  }
   template <int C>
   __device__ void g3(const T* in, T* out, T* tmp) const {
     constexpr int NO = P::NO;
@@ -353,14 +366,11 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(T* __restric
       if (sqrt(ps.dot(Pr, Pr)) <= cg_tol * r0) break;
     }
     // Pq = S Pd = sum_c G_c Lambda_c^-1 G_c^T Pd
-    for (int o = lane; o < P::NPR; o += GS) Pq[o] = T(0);
-    gsync<GS>();
+
     SMG_FOR_C({
       ps.template gt3<C>(Pd, T1, T2);
       ps.template lam_inv<C>(T1);
-      ps.template g3<C>(T1, T2, Pz);  // result in T2; Pz is free scratch here (recomputed below)
-      for (int o = lane; o < P::NPR; o += GS) Pq[o] += T2[o];
-      gsync<GS>();
+      ps.template g3acc<C, C != 0>(T1, Pq, T2, Pz);  // Pz is free scratch here (recomputed below)
     })
     const T dq = ps.dot(Pd, Pq);
     if (!(dq > T(0)) || rz == T(0)) break;
