@@ -278,7 +278,7 @@ def main():
             ctx.vmult_host(level, xbn, smg.F64, out=ybn)
         te = (time.perf_counter() - t0) / args.steps
         e2e = {"value": N / te, "unit": "DoF/s", "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * N,
-               "path": "smg_vmult_host: BlockVector host arrays (pinned) -> H2D -> vmult -> D2H"}
+               "path": "smg_vmult_host: BlockVector host arrays (pinned), pipelined over z-chunks: H2D / vmult / D2H on three streams"}
         parallelism = "single GPU"
     else:
         # ---- z-slab partition of the same global problem, NCCL ghost exchange per apply ----

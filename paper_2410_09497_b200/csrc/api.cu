@@ -304,6 +304,89 @@ void download_blocks(Context& c, int level, int prec, void* const vel[3], void* 
   SMG_CUDA(cudaMemcpyAsync(p, st, lay.size[3] * es, cudaMemcpyDeviceToHost, c.stream));
 }
 
+// Host BlockVector apply, pipelined over z-chunks of the level: chunk k's copy in
+// (stream s_in: velocity planes + cell-local pressure, then the pressure permutation), the operator
+// rows of chunk k once chunks k and k+1 are resident (context stream; the kernel's z range), and
+// chunk k's copy out (stream s_out: pressure permutation back, then the copies) overlap, so the
+// PCIe transfers in both directions and the compute run concurrently.
+void vmult_host_pipelined(Context& c, int level, int prec, void* const y_vel[3], void* y_p, const void* const x_vel[3],
+                          const void* x_p) {
+  ensure_work(c, prec);
+  const LevelLayout& lay = c.dev[0][level].lay;
+  const size_t es = elem_size(prec);
+  const int H = c.cfg.degree + 1;
+  char* dx = static_cast<char*>(c.work_x[prec][level]);
+  char* dy = static_cast<char*>(c.work_b[prec][level]);
+  char* pin = pressure_stage(c, prec);
+  if (!c.pstage_out[prec]) c.pstage_out[prec] = alloc_vec(c, c.cfg.max_level, prec);
+  char* pout = static_cast<char*>(c.pstage_out[prec]);
+  if (!c.s_in) {
+    SMG_CUDA(cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking));
+    SMG_CUDA(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking));
+  }
+  // chunks of 4k cells (every brick depth divides 4), at most 8
+  const int m = lay.m;
+  int chunk = std::max(4, (m / 8) / 4 * 4);
+  if (m < 8) chunk = m;
+  const int nchunk = (m + chunk - 1) / chunk;
+  std::vector<cudaEvent_t> ev_in(nchunk), ev_comp(nchunk);
+  for (int k = 0; k < nchunk; ++k) {
+    SMG_CUDA(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
+    SMG_CUDA(cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming));
+  }
+  struct EvGuard {
+    std::vector<cudaEvent_t>* a;
+    std::vector<cudaEvent_t>* b;
+    ~EvGuard() {
+      for (auto e : *a) cudaEventDestroy(e);
+      for (auto e : *b) cudaEventDestroy(e);
+    }
+  } guard{&ev_in, &ev_comp};
+  cudaEvent_t start;
+  SMG_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  SMG_CUDA(cudaEventRecord(start, c.stream));  // the copies are ordered after earlier work on the context stream
+  SMG_CUDA(cudaStreamWaitEvent(c.s_in, start, 0));
+  SMG_CUDA(cudaStreamWaitEvent(c.s_out, start, 0));
+  cudaEventDestroy(start);
+  // byte range [a, b) of block blk for the node planes of cells [z0, z1) (+ the top u_z plane at the end)
+  auto span = [&](int blk, int z0, int z1, int64_t& off, int64_t& len) {
+    const int64_t plane = blk == 3 ? static_cast<int64_t>(lay.n) * lay.n : lay.dims[blk][0] * lay.dims[blk][1];
+    const int64_t p0 = static_cast<int64_t>(z0) * H, p1 = static_cast<int64_t>(z1) * H + (blk == 2 && z1 == m ? 1 : 0);
+    off = p0 * plane;
+    len = (p1 - p0) * plane;
+  };
+  for (int k = 0; k < nchunk; ++k) {
+    const int z0 = k * chunk, z1 = std::min(m, z0 + chunk);
+    for (int blk = 0; blk < 4; ++blk) {
+      int64_t off, len;
+      span(blk, z0, z1, off, len);
+      const char* src = static_cast<const char*>(blk < 3 ? x_vel[blk] : x_p) + off * es;
+      char* dst = (blk < 3 ? dx + lay.off[blk] * es : pin) + off * es;
+      SMG_CUDA(cudaMemcpyAsync(dst, src, len * es, cudaMemcpyHostToDevice, c.s_in));
+    }
+    launch_pressure_permute(c, level, prec, dx + lay.off[3] * es, pin, false, z0, z1, c.s_in);
+    SMG_CUDA(cudaEventRecord(ev_in[k], c.s_in));
+  }
+  for (int k = 0; k < nchunk; ++k) {
+    const int z0 = k * chunk, z1 = std::min(m, z0 + chunk);
+    SMG_CUDA(cudaStreamWaitEvent(c.stream, ev_in[k], 0));
+    if (k + 1 < nchunk) SMG_CUDA(cudaStreamWaitEvent(c.stream, ev_in[k + 1], 0));
+    launch_vmult_zrange(c, level, prec, dy, dx, nullptr, z0, z1);
+    SMG_CUDA(cudaEventRecord(ev_comp[k], c.stream));
+    SMG_CUDA(cudaStreamWaitEvent(c.s_out, ev_comp[k], 0));
+    launch_pressure_permute(c, level, prec, pout, dy + lay.off[3] * es, true, z0, z1, c.s_out);
+    for (int blk = 0; blk < 4; ++blk) {
+      int64_t off, len;
+      span(blk, z0, z1, off, len);
+      const char* src = (blk < 3 ? dy + lay.off[blk] * es : pout) + off * es;
+      char* dst = static_cast<char*>(blk < 3 ? y_vel[blk] : y_p) + off * es;
+      SMG_CUDA(cudaMemcpyAsync(dst, src, len * es, cudaMemcpyDeviceToHost, c.s_out));
+    }
+  }
+  SMG_CUDA(cudaStreamSynchronize(c.s_out));
+  SMG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
 template <class F>
 int guarded(smg_context* h, F&& f) {
   Context* c = reinterpret_cast<Context*>(h);
@@ -336,6 +419,8 @@ void check_prec(int p) {
 }  // namespace
 
 Context::~Context() {
+  if (s_in) cudaStreamDestroy(s_in);
+  if (s_out) cudaStreamDestroy(s_out);
   for (void* p : allocations) cudaFree(p);
   if (dot_host) cudaFreeHost(dot_host);
 }
@@ -672,14 +757,7 @@ int smg_vmult_host(smg_context* h, int level, int precision, void* const y_vel[3
     smg::check_level(c, level);
     smg::check_prec(precision);
     if (!x_vel || !y_vel || !x_p || !y_p) throw std::invalid_argument("vmult_host: null pointer");
-    // device staging buffers: the level's work vectors of this precision
-    smg::ensure_work(c, precision);
-    char* dx = static_cast<char*>(c.work_x[precision][level]);
-    char* dy = static_cast<char*>(c.work_b[precision][level]);
-    smg::upload_blocks(c, level, precision, dx, x_vel, x_p);
-    smg::launch_vmult(c, level, precision, dy, dx, nullptr);
-    smg::download_blocks(c, level, precision, y_vel, y_p, dy);
-    SMG_CUDA(cudaStreamSynchronize(c.stream));
+    smg::vmult_host_pipelined(c, level, precision, y_vel, y_p, x_vel, x_p);
     return SMG_OK;
   });
 }

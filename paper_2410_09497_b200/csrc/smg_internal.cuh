@@ -114,7 +114,9 @@ struct Context {
   // per-level work vectors for the smoother / V-cycle (allocated lazily): [prec][level]
   std::vector<void*> work_r[2], work_x[2], work_b[2];
   std::vector<void*> krylov;  // FGMRES basis pool (fp64, finest-level size)
-  void* pstage[2] = {nullptr, nullptr};  // pressure staging for the BlockVector host path (finest level size)
+  void* pstage[2] = {nullptr, nullptr};
+  void* pstage_out[2] = {nullptr, nullptr};
+  cudaStream_t s_in = nullptr, s_out = nullptr;  // host-path copy streams (created on first use)  // pressure staging for the BlockVector host path (finest level size)
   // TMA descriptors of input vectors (vmult.cu)
   void* tmap_dev = nullptr;
   std::map<TmapKey, int> tmap_slots;
@@ -135,6 +137,8 @@ void launch_vmult(Context& c, int level, int prec, void* y, const void* x, const
 // z-slab operator: x, y (, b) hold the cells [max(z0-1,0), min(z1+1,m)) in the slab layout; computes
 // the rows of the owned cells [z0, z1) (ghost layers must be current in x)
 void launch_vmult_slab(Context& c, int level, int prec, void* y, const void* x, const void* b, int z0, int z1);
+// operator rows of the cells [z0, z1) of a whole-level vector (bricks restricted to that z range)
+void launch_vmult_zrange(Context& c, int level, int prec, void* y, const void* x, const void* b, int z0, int z1);
 void launch_smooth_colour(Context& c, int level, int prec, int colour, void* x, const void* r);
 void launch_prolongate_add(Context& c, int coarse_level, int prec, void* xf, const void* xc);
 void launch_restrict(Context& c, int coarse_level, int prec, void* rc, const void* rf);
@@ -149,6 +153,7 @@ void launch_zero(Context& c, int64_t n, int prec, void* x);
 void launch_scale(Context& c, int64_t n, int prec, double alpha, void* x);
 void launch_sub_pressure_mean(Context& c, int level, int prec, void* x);  // mass-weighted mean removal
 // pressure block global lexicographic <-> cell-local (BlockVector / DoFLayout order)
-void launch_pressure_permute(Context& c, int level, int prec, void* dst, const void* src, bool to_cell_local);
+void launch_pressure_permute(Context& c, int level, int prec, void* dst, const void* src, bool to_cell_local,
+                             int z0 = 0, int z1 = -1, cudaStream_t stream = nullptr);
 
 }  // namespace smg

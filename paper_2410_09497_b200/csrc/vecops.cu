@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "smg_internal.cuh"
 
@@ -106,10 +107,10 @@ __global__ void sub_scalar_kernel(int64_t n, T* __restrict__ p, const double* __
 // DoFLayout: cells x-fastest, (k+1)^3 nodes per cell x-fastest). One thread per DoF,
 // indexed by the global lexicographic position (coalesced on that side).
 template <typename T, bool TO_CELL>
-__global__ void pressure_permute_kernel(T* __restrict__ dst, const T* __restrict__ src, int m, int H) {
+__global__ void pressure_permute_kernel(T* __restrict__ dst, const T* __restrict__ src, int m, int H, int64_t begin,
+                                        int64_t end) {
   const int n = m * H;
-  const int64_t total = static_cast<int64_t>(n) * n * n;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+  for (int64_t i = begin + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < end;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int gx = static_cast<int>(i % n), gy = static_cast<int>((i / n) % n), gz = static_cast<int>(i / (int64_t(n) * n));
     const int64_t cell = (static_cast<int64_t>(gz / H) * m + gy / H) * m + gx / H;
@@ -230,24 +231,24 @@ void launch_convert(Context& c, int64_t n, int dst_prec, void* dst, int src_prec
   SMG_CUDA(cudaGetLastError());
 }
 
-void launch_pressure_permute(Context& c, int level, int prec, void* dst, const void* src, bool to_cell_local) {
+void launch_pressure_permute(Context& c, int level, int prec, void* dst, const void* src, bool to_cell_local, int z0,
+                             int z1, cudaStream_t stream) {
   const LevelLayout& lay = c.dev[0][level].lay;
-  const int g = grid_for(lay.size[3]), H = c.cfg.degree + 1;
-  if (prec == SMG_F64) {
-    if (to_cell_local)
-      pressure_permute_kernel<double, true><<<g, kThreads, 0, c.stream>>>(static_cast<double*>(dst),
-                                                                          static_cast<const double*>(src), lay.m, H);
-    else
-      pressure_permute_kernel<double, false><<<g, kThreads, 0, c.stream>>>(static_cast<double*>(dst),
-                                                                           static_cast<const double*>(src), lay.m, H);
-  } else {
-    if (to_cell_local)
-      pressure_permute_kernel<float, true><<<g, kThreads, 0, c.stream>>>(static_cast<float*>(dst),
-                                                                         static_cast<const float*>(src), lay.m, H);
-    else
-      pressure_permute_kernel<float, false><<<g, kThreads, 0, c.stream>>>(static_cast<float*>(dst),
-                                                                          static_cast<const float*>(src), lay.m, H);
-  }
+  const int H = c.cfg.degree + 1;
+  if (z1 < 0) z1 = lay.m;
+  // the pressure of the cells [z0, z1) is the global-lexicographic range of their node planes (and a
+  // contiguous range of the cell-local numbering as well)
+  const int64_t plane = static_cast<int64_t>(lay.n) * lay.n;
+  const int64_t begin = static_cast<int64_t>(z0) * H * plane, end = static_cast<int64_t>(z1) * H * plane;
+  const int g = grid_for(end - begin);
+  if (stream == nullptr) stream = c.stream;
+  auto go = [&](auto* d, auto* s) {
+    using T = std::remove_const_t<std::remove_pointer_t<decltype(s)>>;
+    if (to_cell_local) pressure_permute_kernel<T, true><<<g, kThreads, 0, stream>>>(d, s, lay.m, H, begin, end);
+    else pressure_permute_kernel<T, false><<<g, kThreads, 0, stream>>>(d, s, lay.m, H, begin, end);
+  };
+  if (prec == SMG_F64) go(static_cast<double*>(dst), static_cast<const double*>(src));
+  else go(static_cast<float*>(dst), static_cast<const float*>(src));
   ++c.launches;
   SMG_CUDA(cudaGetLastError());
 }
