@@ -101,6 +101,25 @@ int smg_slab_sizes(int degree, int level, int z0, int z1, int64_t sizes[5]);
 int smg_vmult_slab(smg_context* ctx, int level, int precision, void* y, const void* x, int z0, int z1);
 int smg_residual_slab(smg_context* ctx, int level, int precision, void* r, const void* b, const void* x, int z0,
                       int z1);
+/* ---- multigrid on z-slabs (general held ranges). A "held" vector holds the cells [zlo, zhi) of its
+ *      level in the slab layout above; each call computes only the rows named by its cell range:
+ *        residual_held       r = b - A x on the rows of cells [c0, c1) (held must cover c0-1 .. c1)
+ *        smooth_colour_held  the patches of one colour whose vertex z plane is in [vz0, vz1]
+ *        prolongate_add_held fine rows of fine cells [f0, f1) += P x_c
+ *        restrict_held       coarse rows of coarse cells [c0, c1) = P^T r_f (reads fine cells 2c0-2 .. 2c1)
+ *        dot_held            dot over the rows of cells [c0, c1) (fp64 accumulate; caller all-reduces) ---- */
+int smg_held_sizes(int degree, int level, int zlo, int zhi, int64_t sizes[5]);
+int smg_residual_held(smg_context* ctx, int level, int precision, void* r, const void* b, const void* x, int zlo,
+                      int zhi, int c0, int c1);
+int smg_smooth_colour_held(smg_context* ctx, int level, int precision, int colour, void* x, const void* r, int zlo,
+                           int zhi, int vz0, int vz1);
+int smg_prolongate_add_held(smg_context* ctx, int coarse_level, int precision, void* x_fine, const void* x_coarse,
+                            int fzlo, int fzhi, int czlo, int czhi, int f0, int f1);
+int smg_restrict_held(smg_context* ctx, int coarse_level, int precision, void* r_coarse, const void* r_fine, int fzlo,
+                      int fzhi, int czlo, int czhi, int c0, int c1);
+int smg_dot_held(smg_context* ctx, int level, int precision, const void* a, const void* b, int zlo, int zhi, int c0,
+                 int c1, double* out);
+
 /* dot over the owned rows of two slab vectors (fp64 accumulate); the caller all-reduces across ranks */
 int smg_dot_slab(smg_context* ctx, int level, int precision, const void* a, const void* b, int z0, int z1,
                  double* out);

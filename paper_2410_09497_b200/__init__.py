@@ -25,7 +25,8 @@ EXPORTED = [
     "smg_level_sizes", "smg_vec_alloc", "smg_vec_free", "smg_vmult", "smg_residual", "smg_smooth",
     "smg_prolongate_add", "smg_restrict", "smg_coarse_solve", "smg_vcycle", "smg_solve", "smg_dot", "smg_axpy",
     "smg_convert", "smg_vmult_host", "smg_vec_upload", "smg_vec_download", "smg_slab_sizes", "smg_vmult_slab",
-    "smg_residual_slab", "smg_dot_slab",
+    "smg_residual_slab", "smg_dot_slab", "smg_held_sizes", "smg_residual_held", "smg_smooth_colour_held",
+    "smg_prolongate_add_held", "smg_restrict_held", "smg_dot_held",
 ]
 
 
@@ -85,6 +86,12 @@ def lib():
         L.smg_vmult_slab.argtypes = [P, I, I, P, P, I, I]
         L.smg_residual_slab.argtypes = [P, I, I, P, P, P, I, I]
         L.smg_dot_slab.argtypes = [P, I, I, P, P, I, I, ctypes.POINTER(D)]
+        L.smg_held_sizes.argtypes = [I, I, I, I, P]
+        L.smg_residual_held.argtypes = [P, I, I, P, P, P, I, I, I, I]
+        L.smg_smooth_colour_held.argtypes = [P, I, I, I, P, P, I, I, I, I]
+        L.smg_prolongate_add_held.argtypes = [P, I, I, P, P, I, I, I, I, I, I]
+        L.smg_restrict_held.argtypes = [P, I, I, P, P, I, I, I, I, I, I]
+        L.smg_dot_held.argtypes = [P, I, I, P, P, I, I, I, I, ctypes.POINTER(D)]
         L.smg_vec_download.argtypes = [P, I, I, P, P, P]
         _LIB = L
     return _LIB

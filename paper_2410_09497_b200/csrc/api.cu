@@ -695,6 +695,86 @@ int smg_dot_slab(smg_context* h, int level, int precision, const void* a, const 
   });
 }
 
+int smg_held_sizes(int degree, int level, int zlo, int zhi, int64_t sizes[5]) {
+  try {
+    smg::LevelLayout l(degree, level, zlo, zhi);
+    for (int i = 0; i < 4; ++i) sizes[i] = l.size[i];
+    sizes[4] = l.total;
+    return SMG_OK;
+  } catch (...) {
+    return SMG_EINVAL;
+  }
+}
+
+int smg_residual_held(smg_context* h, int level, int precision, void* r, const void* b, const void* x, int zlo, int zhi,
+                      int c0, int c1) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!r || !x || r == x || r == b) throw std::invalid_argument("residual_held: r must differ from b and x");
+    smg::launch_vmult_args_public(c, level, precision, r, x, b, zlo, zhi, c0, c1);
+    return SMG_OK;
+  });
+}
+
+int smg_smooth_colour_held(smg_context* h, int level, int precision, int colour, void* x, const void* r, int zlo,
+                           int zhi, int vz0, int vz1) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (level < 1 || colour < 0 || colour > 7) throw std::invalid_argument("smooth_colour_held: bad level / colour");
+    smg::launch_smooth_colour_held(c, level, precision, colour, x, r, zlo, zhi, vz0, vz1);
+    return SMG_OK;
+  });
+}
+
+int smg_prolongate_add_held(smg_context* h, int coarse_level, int precision, void* xf, const void* xc, int fzlo,
+                            int fzhi, int czlo, int czhi, int f0, int f1) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, coarse_level + 1);
+    smg::check_prec(precision);
+    smg::launch_prolongate_add_held(c, coarse_level, precision, xf, xc, fzlo, fzhi, czlo, czhi, f0, f1);
+    return SMG_OK;
+  });
+}
+
+int smg_restrict_held(smg_context* h, int coarse_level, int precision, void* rc, const void* rf, int fzlo, int fzhi,
+                      int czlo, int czhi, int c0, int c1) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, coarse_level + 1);
+    smg::check_prec(precision);
+    smg::launch_restrict_held(c, coarse_level, precision, rc, rf, fzlo, fzhi, czlo, czhi, c0, c1);
+    return SMG_OK;
+  });
+}
+
+int smg_dot_held(smg_context* h, int level, int precision, const void* a, const void* b, int zlo, int zhi, int c0,
+                 int c1, double* out) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!out) throw std::invalid_argument("dot_held: null output");
+    const int m = c.dev[0][level].lay.m, H = c.cfg.degree + 1;
+    if (c0 < zlo || c1 > zhi || c0 >= c1) throw std::invalid_argument("dot_held: rows outside the held cells");
+    const smg::LevelLayout lay(c.cfg.degree, level, zlo, zhi);
+    int64_t beg[4], len[4];
+    for (int blk = 0; blk < 4; ++blk) {
+      const int64_t p0 = static_cast<int64_t>(c0 - zlo) * H;
+      int64_t p1 = static_cast<int64_t>(c1 - zlo) * H;
+      if (blk == 2 && c1 == m) p1 += 1;
+      beg[blk] = lay.off[blk] + p0 * lay.plane[blk];
+      len[blk] = (p1 - p0) * lay.plane[blk];
+    }
+    *out = smg::dot_ranges(c, precision, a, b, beg, len, 4);
+    return SMG_OK;
+  });
+}
+
 int smg_dot(smg_context* h, int level, int precision, const void* a, const void* b, double* out) {
   return smg::guarded(h, [&] {
     Context& c = smg::ctx_of(h);

@@ -82,14 +82,17 @@ struct DevLevel {
   void* pweights = nullptr; // pressure node weights (k+1)
 };
 
+// A tensor map depends on the vector's address AND its layout (level, precision, held cells): the
+// allocator may hand the same address to a vector of another layout, so all of them are in the key.
 struct TmapKey {
   const void* ptr;
-  int level, esize, zlo;
+  int level, esize, zlo, zhi;
   bool operator<(const TmapKey& o) const {
     if (ptr != o.ptr) return ptr < o.ptr;
     if (level != o.level) return level < o.level;
     if (esize != o.esize) return esize < o.esize;
-    return zlo < o.zlo;
+    if (zlo != o.zlo) return zlo < o.zlo;
+    return zhi < o.zhi;
   }
 };
 
@@ -137,11 +140,23 @@ void launch_vmult(Context& c, int level, int prec, void* y, const void* x, const
 // z-slab operator: x, y (, b) hold the cells [max(z0-1,0), min(z1+1,m)) in the slab layout; computes
 // the rows of the owned cells [z0, z1) (ghost layers must be current in x)
 void launch_vmult_slab(Context& c, int level, int prec, void* y, const void* x, const void* b, int z0, int z1);
+// operator (residual if b) rows of the cells [c0, c1) on vectors holding the cells [zlo, zhi)
+void launch_vmult_args_public(Context& c, int level, int prec, void* y, const void* x, const void* b, int zlo, int zhi,
+                              int c0, int c1);
 // operator rows of the cells [z0, z1) of a whole-level vector (bricks restricted to that z range)
 void launch_vmult_zrange(Context& c, int level, int prec, void* y, const void* x, const void* b, int z0, int z1);
 void launch_smooth_colour(Context& c, int level, int prec, int colour, void* x, const void* r);
+// one colour on vectors holding the cells [zlo, zhi): patches with vertex z planes in [vz0, vz1]
+void launch_smooth_colour_held(Context& c, int level, int prec, int colour, void* x, const void* r, int zlo, int zhi,
+                               int vz0, int vz1);
 void launch_prolongate_add(Context& c, int coarse_level, int prec, void* xf, const void* xc);
 void launch_restrict(Context& c, int coarse_level, int prec, void* rc, const void* rf);
+// z-slab transfers: fine vectors hold fine cells [fzlo, fzhi), coarse [czlo, czhi); prolongation adds
+// into the rows of fine cells [r0, r1), restriction writes the rows of coarse cells [r0, r1)
+void launch_prolongate_add_held(Context& c, int coarse_level, int prec, void* xf, const void* xc, int fzlo, int fzhi,
+                                int czlo, int czhi, int r0, int r1);
+void launch_restrict_held(Context& c, int coarse_level, int prec, void* rc, const void* rf, int fzlo, int fzhi, int czlo,
+                          int czhi, int r0, int r1);
 void launch_coarse_apply(Context& c, int prec, void* x, const void* b);
 double dot(Context& c, int64_t n, int prec, const void* a, const void* b);
 double dot_ranges(Context& c, int prec, const void* a, const void* b, const int64_t* begin, const int64_t* len,

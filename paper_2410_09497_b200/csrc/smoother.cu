@@ -254,11 +254,18 @@ struct Patch {
   }
 };
 
+// per-block base pointers of a level vector in the global index space (a z-slab vector passes bases
+// shifted back by its first plane)
+template <typename T>
+struct SBlocks {
+  T* c[4];
+};
+
 template <typename T, int K, int W, int MINB, int GS>
-__global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(T* __restrict__ x, const T* __restrict__ r,
+__global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlocks<T> x, const SBlocks<const T> r,
                                                               const T* __restrict__ ptab, int m, int colour,
-                                                              int cg_max_iter, T cg_tol, int cg_fixed,
-                                                              int cg_precond) {
+                                                              int vz_first, int cnt_z, int cg_max_iter, T cg_tol,
+                                                              int cg_fixed, int cg_precond) {
   using P = PD<K>;
   constexpr int H = K + 1, NO = P::NO;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -278,13 +285,13 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(T* __restric
     __syncthreads();
   }
   const int warp = threadIdx.x / GS, lane = threadIdx.x % GS;  // patch slot in the CTA, thread in its group
-  const int cnt[3] = {(colour & 1) ? m / 2 : m / 2 - 1, ((colour >> 1) & 1) ? m / 2 : m / 2 - 1,
-                      ((colour >> 2) & 1) ? m / 2 : m / 2 - 1};
+  // vertices of the colour: x / y over the whole level, z from vz_first (cnt_z planes, step 2)
+  const int cnt[3] = {(colour & 1) ? m / 2 : m / 2 - 1, ((colour >> 1) & 1) ? m / 2 : m / 2 - 1, cnt_z};
   const int npatch = cnt[0] * cnt[1] * cnt[2];
   const int pid = blockIdx.x * W + warp;
   if (pid >= npatch) return;
   const int v[3] = {((colour & 1) ? 1 : 2) + 2 * (pid % cnt[0]), (((colour >> 1) & 1) ? 1 : 2) + 2 * ((pid / cnt[0]) % cnt[1]),
-                    (((colour >> 2) & 1) ? 1 : 2) + 2 * (pid / (cnt[0] * cnt[1]))};
+                    vz_first + 2 * (pid / (cnt[0] * cnt[1]))};
   T* ws = tab + P::TABP + P::LINV + warp * P::WS;
   T* Fh = ws;                // 3 x NV eigen coefficients of F_c
   T* Pr = Fh + 3 * P::NV;    // CG residual
@@ -302,7 +309,6 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(T* __restric
   ps.linv = tab + P::TABP;  // CTA-shared table filled above
   ps.interior = ps.var[0] == 0 && ps.var[1] == 0 && ps.var[2] == 0;
   const int n = m * H;
-  const int64_t sizeV = static_cast<int64_t>(n + 1) * n * n;
 
   // ---- gather R_j r: velocity blocks -> T1 -> eigen coefficients Fh_c; pressure -> Pq (= G) ----
   auto vel_index = [&](int c, int o) {
@@ -312,20 +318,20 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(T* __restric
     if (c == 0) gd0 = n + 1;
     if (c == 1) gd1 = n + 1;
     const int b0 = (v[0] - 1) * H + (c == 0), b1 = (v[1] - 1) * H + (c == 1), b2 = (v[2] - 1) * H + (c == 2);
-    return c * sizeV + (static_cast<int64_t>(b2 + zz) * gd1 + b1 + yy) * gd0 + b0 + xx;
+    return (static_cast<int64_t>(b2 + zz) * gd1 + b1 + yy) * gd0 + b0 + xx;
   };
   auto pres_index = [&](int o) {
     const int xx = o % NO, yy = (o / NO) % NO, zz = o / (NO * NO);
-    return 3 * sizeV + (static_cast<int64_t>((v[2] - 1) * H + zz) * n + (v[1] - 1) * H + yy) * n + (v[0] - 1) * H + xx;
+    return (static_cast<int64_t>((v[2] - 1) * H + zz) * n + (v[1] - 1) * H + yy) * n + (v[0] - 1) * H + xx;
   };
 #define SMG_FOR_C(...) \
   { constexpr int C = 0; __VA_ARGS__ } { constexpr int C = 1; __VA_ARGS__ } { constexpr int C = 2; __VA_ARGS__ }
   SMG_FOR_C({
-    for (int o = lane; o < P::NV; o += GS) T1[o] = r[vel_index(C, o)];
+    for (int o = lane; o < P::NV; o += GS) T1[o] = r.c[C][vel_index(C, o)];
     gsync<GS>();
     ps.template s3<C, true>(T1, Fh + C * P::NV, T2);
   })
-  for (int o = lane; o < P::NPR; o += GS) Pq[o] = r[pres_index(o)];
+  for (int o = lane; o < P::NPR; o += GS) Pq[o] = r.c[3][pres_index(o)];
   // ---- rhs = sum_c G_c Lambda_c^-1 Fh_c - G  (projected) -> Pr ----
   for (int o = lane; o < P::NPR; o += GS) Pr[o] = -Pq[o];
   gsync<GS>();
@@ -396,10 +402,10 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(T* __restric
     gsync<GS>();
     ps.template lam_inv<C>(T1);
     ps.template s3<C, false>(T1, T2, Pz);
-    for (int o = lane; o < P::NV; o += GS) x[vel_index(C, o)] += T2[o];
+    for (int o = lane; o < P::NV; o += GS) x.c[C][vel_index(C, o)] += T2[o];
   })
 #undef SMG_FOR_C
-  for (int o = lane; o < P::NPR; o += GS) x[pres_index(o)] += Px[o];
+  for (int o = lane; o < P::NPR; o += GS) x.c[3][pres_index(o)] += Px[o];
 }
 
 template <typename T, int K>
@@ -410,8 +416,17 @@ constexpr int warps_per_cta() {
   return w >= 8 ? 8 : (w >= 4 ? 4 : (w >= 2 ? 2 : 1));
 }
 
+template <typename T>
+SBlocks<T> sblocks(const LevelLayout& lay, T* v) {
+  SBlocks<T> B;
+  const int H = lay.k + 1;
+  for (int c = 0; c < 4; ++c) B.c[c] = v + lay.off[c] - static_cast<int64_t>(lay.zlo) * H * lay.plane[c];
+  return B;
+}
+
 template <typename T, int K, int W, int GS>
-void launch_group(Context& ctx, const DevLevel& dl, int npatch, int colour, void* x, const void* r) {
+void launch_group(Context& ctx, const DevLevel& dl, const LevelLayout& lay, int npatch, int colour, int vz_first,
+                  int cnt_z, void* x, const void* r) {
   using P = PD<K>;
   const size_t smem = sizeof(T) * (P::TABP + P::LINV + W * P::WS);
   // as many resident CTAs as shared memory allows (up to 3): registers are capped accordingly
@@ -424,33 +439,44 @@ void launch_group(Context& ctx, const DevLevel& dl, int npatch, int colour, void
     attr = true;
   }
   kern<<<(npatch + W - 1) / W, GS * W, smem, ctx.stream>>>(
-      static_cast<T*>(x), static_cast<const T*>(r), static_cast<const T*>(dl.patch), dl.lay.m, colour,
-      ctx.cfg.cg_max_iter, static_cast<T>(ctx.cfg.cg_tol), ctx.cfg.cg_fixed, ctx.cfg.cg_precond);
+      sblocks(lay, static_cast<T*>(x)), sblocks(lay, static_cast<const T*>(r)), static_cast<const T*>(dl.patch),
+      dl.lay.m, colour, vz_first, cnt_z, ctx.cfg.cg_max_iter, static_cast<T>(ctx.cfg.cg_tol), ctx.cfg.cg_fixed,
+      ctx.cfg.cg_precond);
   SMG_CUDA(cudaGetLastError());
   ++ctx.launches;
 }
 
+// patches of one colour with vertex z planes in [vz0, vz1] (clipped to 1..m-1), on vectors holding the
+// cells [zlo, zhi) of the level
 template <typename T, int K>
-void launch_k(Context& ctx, int level, int colour, void* x, const void* r) {
+void launch_k(Context& ctx, int level, int colour, void* x, const void* r, int zlo, int zhi, int vz0, int vz1) {
   const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
   const int m = dl.lay.m;
+  const LevelLayout lay(K, level, zlo, zhi);
   auto cnt = [&](int bit) { return bit ? m / 2 : m / 2 - 1; };
-  const int npatch = cnt(colour & 1) * cnt((colour >> 1) & 1) * cnt((colour >> 2) & 1);
+  const int zbit = (colour >> 2) & 1;
+  int vf = std::max(vz0, 1);
+  if ((vf & 1) != zbit) ++vf;  // odd planes for bit 1, even for bit 0
+  const int vl = std::min(vz1, m - 1);
+  const int cnt_z = vl >= vf ? (vl - vf) / 2 + 1 : 0;
+  if (cnt_z > 0 && (vf - 1 < zlo || vl + 1 > zhi))
+    throw std::invalid_argument("smooth: patches need the cells on both sides of their vertex plane");
+  const int npatch = cnt(colour & 1) * cnt((colour >> 1) & 1) * cnt_z;
   if (npatch <= 0) return;
-  // few patches (coarse levels): a 4-warp CTA per patch cuts the per-patch latency; many patches: one
-  // warp per patch, several per CTA
-  if (npatch <= 148) launch_group<T, K, 1, 256>(ctx, dl, npatch, colour, x, r);
-  else if (npatch < 148 * 8) launch_group<T, K, 1, 128>(ctx, dl, npatch, colour, x, r);
-  else launch_group<T, K, warps_per_cta<T, K>(), 32>(ctx, dl, npatch, colour, x, r);
+  // few patches (coarse levels): a 4- or 8-warp CTA per patch cuts the per-patch latency; many
+  // patches: one warp per patch, several per CTA
+  if (npatch <= 148) launch_group<T, K, 1, 256>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
+  else if (npatch < 148 * 8) launch_group<T, K, 1, 128>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
+  else launch_group<T, K, warps_per_cta<T, K>(), 32>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
 }
 
 template <typename T>
-void launch_prec(Context& ctx, int level, int colour, void* x, const void* r) {
+void launch_prec(Context& ctx, int level, int colour, void* x, const void* r, int zlo, int zhi, int vz0, int vz1) {
   switch (ctx.cfg.degree) {
-    case 1: launch_k<T, 1>(ctx, level, colour, x, r); break;
-    case 2: launch_k<T, 2>(ctx, level, colour, x, r); break;
-    case 3: launch_k<T, 3>(ctx, level, colour, x, r); break;
-    case 4: launch_k<T, 4>(ctx, level, colour, x, r); break;
+    case 1: launch_k<T, 1>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1); break;
+    case 2: launch_k<T, 2>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1); break;
+    case 3: launch_k<T, 3>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1); break;
+    case 4: launch_k<T, 4>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1); break;
     default: throw std::invalid_argument("degree not supported by the patch smoother kernel (1..4)");
   }
 }
@@ -458,8 +484,15 @@ void launch_prec(Context& ctx, int level, int colour, void* x, const void* r) {
 }  // namespace
 
 void launch_smooth_colour(Context& ctx, int level, int prec, int colour, void* x, const void* r) {
-  if (prec == SMG_F64) launch_prec<double>(ctx, level, colour, x, r);
-  else launch_prec<float>(ctx, level, colour, x, r);
+  const int m = ctx.dev[0][level].lay.m;
+  if (prec == SMG_F64) launch_prec<double>(ctx, level, colour, x, r, 0, m, 1, m - 1);
+  else launch_prec<float>(ctx, level, colour, x, r, 0, m, 1, m - 1);
+}
+
+void launch_smooth_colour_held(Context& ctx, int level, int prec, int colour, void* x, const void* r, int zlo,
+                               int zhi, int vz0, int vz1) {
+  if (prec == SMG_F64) launch_prec<double>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1);
+  else launch_prec<float>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1);
 }
 
 // packed patch table (order of PD<K> offsets): every matrix as padded rows of M and of M^T

@@ -7,6 +7,8 @@
 // per output DoF, reading the (k+2)(k+1)^2 / 2(k+1)-stencil from L1/L2; HBM-bound by construction.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "smg_internal.cuh"
 
 namespace smg {
@@ -14,11 +16,27 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// per-block base pointers in the global index space (z-slab vectors: shifted back by their first plane)
+template <typename T>
+struct TBlocks {
+  T* c[4];
+};
+
+template <typename T>
+TBlocks<T> tblocks(const LevelLayout& lay, T* v) {
+  TBlocks<T> B;
+  const int H = lay.k + 1;
+  for (int c = 0; c < 4; ++c) B.c[c] = v + lay.off[c] - static_cast<int64_t>(lay.zlo) * H * lay.plane[c];
+  return B;
+}
+
 // 1D stencils. Continuous (par): fine node gf of a coarse mesh with mc cells, H = k+1:
 //   cell E = gf / 2H, row r = gf - 2HE (last node: E = mc-1, r = 2H); coarse nodes E*H + j, j<=H.
 // Discontinuous: E = gf / 2H, r = gf % 2H; coarse nodes E*H + j, j < H.
+// fine rows of the fine cells [f0, f1) (all rows: f0 = 0, f1 = 2 mc)
 template <typename T, int K>
-__global__ void prolongate_kernel(T* __restrict__ xf, const T* __restrict__ xc, const T* __restrict__ tab, int mc) {
+__global__ void prolongate_kernel(const TBlocks<T> xf, const TBlocks<const T> xc, const T* __restrict__ tab, int mc,
+                                  int f0, int f1) {
   constexpr int H = K + 1;
   constexpr int EC_R = 2 * H + 1, EC_C = H + 1, ED_R = 2 * H, ED_C = H;
   __shared__ T Ec[EC_R * EC_C], Ed[ED_R * ED_C];
@@ -29,11 +47,12 @@ __global__ void prolongate_kernel(T* __restrict__ xf, const T* __restrict__ xc, 
   const int nc = mc * H, nf = 2 * nc;
   int64_t fd[3] = {nf, nf, nf}, cd[3] = {nc, nc, nc};
   if (comp < 3) { fd[comp] = nf + 1; cd[comp] = nc + 1; }
-  const int64_t fsize = fd[0] * fd[1] * fd[2];
-  const int64_t vf = static_cast<int64_t>(nf + 1) * nf * nf, vc = static_cast<int64_t>(nc + 1) * nc * nc;
-  T* out = xf + comp * vf;
-  const T* in = xc + comp * vc;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < fsize;
+  const int64_t pl = fd[0] * fd[1];
+  const int64_t ibeg = static_cast<int64_t>(f0) * H * pl;
+  const int64_t iend = (static_cast<int64_t>(f1) * H + (comp == 2 && f1 == 2 * mc ? 1 : 0)) * pl;
+  T* out = xf.c[comp];
+  const T* in = xc.c[comp];
+  for (int64_t i = ibeg + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < iend;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int g[3] = {static_cast<int>(i % fd[0]), static_cast<int>((i / fd[0]) % fd[1]),
                       static_cast<int>(i / (fd[0] * fd[1]))};
@@ -74,8 +93,10 @@ __global__ void prolongate_kernel(T* __restrict__ xf, const T* __restrict__ xc, 
 
 // Restriction = P^T: coarse node gc collects fine rows r < 2H of every coarse cell containing it
 // (the fine vertex at r = 2H of cell E is row 0 of cell E+1, counted once).
+// coarse rows of the coarse cells [c0, c1) (all rows: c0 = 0, c1 = mc); reads fine cells [2 c0 - 1, 2 c1]
 template <typename T, int K>
-__global__ void restrict_kernel(T* __restrict__ rc, const T* __restrict__ rf, const T* __restrict__ tab, int mc) {
+__global__ void restrict_kernel(const TBlocks<T> rc, const TBlocks<const T> rf, const T* __restrict__ tab, int mc,
+                                int c0, int c1) {
   constexpr int H = K + 1;
   constexpr int EC_R = 2 * H + 1, EC_C = H + 1, ED_R = 2 * H, ED_C = H;
   __shared__ T Ec[EC_R * EC_C], Ed[ED_R * ED_C];
@@ -86,11 +107,12 @@ __global__ void restrict_kernel(T* __restrict__ rc, const T* __restrict__ rf, co
   const int nc = mc * H, nf = 2 * nc;
   int64_t fd[3] = {nf, nf, nf}, cd[3] = {nc, nc, nc};
   if (comp < 3) { fd[comp] = nf + 1; cd[comp] = nc + 1; }
-  const int64_t csize = cd[0] * cd[1] * cd[2];
-  const int64_t vf = static_cast<int64_t>(nf + 1) * nf * nf, vc = static_cast<int64_t>(nc + 1) * nc * nc;
-  T* out = rc + comp * vc;
-  const T* in = rf + comp * vf;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < csize;
+  const int64_t pl = cd[0] * cd[1];
+  const int64_t ibeg = static_cast<int64_t>(c0) * H * pl;
+  const int64_t iend = (static_cast<int64_t>(c1) * H + (comp == 2 && c1 == mc ? 1 : 0)) * pl;
+  T* out = rc.c[comp];
+  const T* in = rf.c[comp];
+  for (int64_t i = ibeg + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < iend;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int g[3] = {static_cast<int>(i % cd[0]), static_cast<int>((i / cd[0]) % cd[1]),
                       static_cast<int>(i / (cd[0] * cd[1]))};
@@ -153,35 +175,52 @@ int grid_for(int64_t n) {
   return static_cast<int>(g < 4 * kDotBlocks ? (g < 1 ? 1 : g) : 4 * kDotBlocks);
 }
 
+// held ranges: fine vectors hold fine cells [fzlo, fzhi), coarse ones [czlo, czhi); rows computed for
+// fine cells [r0, r1) (prolongation) or coarse cells [r0, r1) (restriction)
+struct TransferRange {
+  int fzlo, fzhi, czlo, czhi, r0, r1;
+};
+
 template <typename T, int K>
-void transfer_k(Context& ctx, int coarse_level, void* out, const void* in, bool prolong) {
+void transfer_k(Context& ctx, int coarse_level, void* out, const void* in, bool prolong, const TransferRange& t) {
   const int p = sizeof(T) == 8 ? 0 : 1;
   const DevLevel& fine = ctx.dev[p][coarse_level + 1];
   const DevLevel& coarse = ctx.dev[p][coarse_level];
   const int mc = coarse.lay.m;
+  const LevelLayout fl(K, coarse_level + 1, t.fzlo, t.fzhi), cl(K, coarse_level, t.czlo, t.czhi);
   if (prolong) {
-    dim3 grid(grid_for(fine.lay.size[0]), 4);
-    prolongate_kernel<T, K><<<grid, kThreads, 0, ctx.stream>>>(static_cast<T*>(out), static_cast<const T*>(in),
-                                                              static_cast<const T*>(fine.transfer), mc);
+    // fine cells [r0, r1) read coarse cells [r0 / 2, (r1 + 1) / 2)
+    if (t.r0 < t.fzlo || t.r1 > t.fzhi || t.r0 / 2 < t.czlo || (t.r1 + 1) / 2 > t.czhi)
+      throw std::invalid_argument("prolongate: held ranges do not cover the rows");
+    const int64_t rows = (static_cast<int64_t>(t.r1 - t.r0) * (K + 1) + 1) * fl.plane[0];
+    dim3 grid(grid_for(rows), 4);
+    prolongate_kernel<T, K><<<grid, kThreads, 0, ctx.stream>>>(tblocks(fl, static_cast<T*>(out)),
+                                                              tblocks(cl, static_cast<const T*>(in)),
+                                                              static_cast<const T*>(fine.transfer), mc, t.r0, t.r1);
   } else {
-    dim3 grid(grid_for(coarse.lay.size[0]), 4);
-    restrict_kernel<T, K><<<grid, kThreads, 0, ctx.stream>>>(static_cast<T*>(out), static_cast<const T*>(in),
-                                                            static_cast<const T*>(fine.transfer), mc);
+    // coarse cells [r0, r1) read fine cells [2 r0 - 1, 2 r1] (within the domain)
+    if (t.r0 < t.czlo || t.r1 > t.czhi || std::max(2 * t.r0 - 1, 0) < t.fzlo || std::min(2 * t.r1 + 1, 2 * mc) > t.fzhi)
+      throw std::invalid_argument("restrict: held ranges do not cover the rows");
+    const int64_t rows = (static_cast<int64_t>(t.r1 - t.r0) * (K + 1) + 1) * cl.plane[0];
+    dim3 grid(grid_for(rows), 4);
+    restrict_kernel<T, K><<<grid, kThreads, 0, ctx.stream>>>(tblocks(cl, static_cast<T*>(out)),
+                                                            tblocks(fl, static_cast<const T*>(in)),
+                                                            static_cast<const T*>(fine.transfer), mc, t.r0, t.r1);
   }
   SMG_CUDA(cudaGetLastError());
   ++ctx.launches;
 }
 
 template <typename T>
-void transfer_prec(Context& ctx, int coarse_level, void* out, const void* in, bool prolong) {
+void transfer_prec(Context& ctx, int coarse_level, void* out, const void* in, bool prolong, const TransferRange& t) {
   switch (ctx.cfg.degree) {
-    case 1: transfer_k<T, 1>(ctx, coarse_level, out, in, prolong); break;
-    case 2: transfer_k<T, 2>(ctx, coarse_level, out, in, prolong); break;
-    case 3: transfer_k<T, 3>(ctx, coarse_level, out, in, prolong); break;
-    case 4: transfer_k<T, 4>(ctx, coarse_level, out, in, prolong); break;
-    case 5: transfer_k<T, 5>(ctx, coarse_level, out, in, prolong); break;
-    case 6: transfer_k<T, 6>(ctx, coarse_level, out, in, prolong); break;
-    case 7: transfer_k<T, 7>(ctx, coarse_level, out, in, prolong); break;
+    case 1: transfer_k<T, 1>(ctx, coarse_level, out, in, prolong, t); break;
+    case 2: transfer_k<T, 2>(ctx, coarse_level, out, in, prolong, t); break;
+    case 3: transfer_k<T, 3>(ctx, coarse_level, out, in, prolong, t); break;
+    case 4: transfer_k<T, 4>(ctx, coarse_level, out, in, prolong, t); break;
+    case 5: transfer_k<T, 5>(ctx, coarse_level, out, in, prolong, t); break;
+    case 6: transfer_k<T, 6>(ctx, coarse_level, out, in, prolong, t); break;
+    case 7: transfer_k<T, 7>(ctx, coarse_level, out, in, prolong, t); break;
     default: throw std::invalid_argument("degree not supported by the transfer kernels (1..7)");
   }
 }
@@ -189,13 +228,31 @@ void transfer_prec(Context& ctx, int coarse_level, void* out, const void* in, bo
 }  // namespace
 
 void launch_prolongate_add(Context& ctx, int coarse_level, int prec, void* xf, const void* xc) {
-  if (prec == SMG_F64) transfer_prec<double>(ctx, coarse_level, xf, xc, true);
-  else transfer_prec<float>(ctx, coarse_level, xf, xc, true);
+  const int mc = ctx.dev[0][coarse_level].lay.m;
+  const TransferRange t{0, 2 * mc, 0, mc, 0, 2 * mc};
+  if (prec == SMG_F64) transfer_prec<double>(ctx, coarse_level, xf, xc, true, t);
+  else transfer_prec<float>(ctx, coarse_level, xf, xc, true, t);
 }
 
 void launch_restrict(Context& ctx, int coarse_level, int prec, void* rc, const void* rf) {
-  if (prec == SMG_F64) transfer_prec<double>(ctx, coarse_level, rc, rf, false);
-  else transfer_prec<float>(ctx, coarse_level, rc, rf, false);
+  const int mc = ctx.dev[0][coarse_level].lay.m;
+  const TransferRange t{0, 2 * mc, 0, mc, 0, mc};
+  if (prec == SMG_F64) transfer_prec<double>(ctx, coarse_level, rc, rf, false, t);
+  else transfer_prec<float>(ctx, coarse_level, rc, rf, false, t);
+}
+
+void launch_prolongate_add_held(Context& ctx, int coarse_level, int prec, void* xf, const void* xc, int fzlo, int fzhi,
+                                int czlo, int czhi, int f0, int f1) {
+  const TransferRange t{fzlo, fzhi, czlo, czhi, f0, f1};
+  if (prec == SMG_F64) transfer_prec<double>(ctx, coarse_level, xf, xc, true, t);
+  else transfer_prec<float>(ctx, coarse_level, xf, xc, true, t);
+}
+
+void launch_restrict_held(Context& ctx, int coarse_level, int prec, void* rc, const void* rf, int fzlo, int fzhi,
+                          int czlo, int czhi, int c0, int c1) {
+  const TransferRange t{fzlo, fzhi, czlo, czhi, c0, c1};
+  if (prec == SMG_F64) transfer_prec<double>(ctx, coarse_level, rc, rf, false, t);
+  else transfer_prec<float>(ctx, coarse_level, rc, rf, false, t);
 }
 
 void launch_coarse_apply(Context& ctx, int prec, void* x, const void* b) {

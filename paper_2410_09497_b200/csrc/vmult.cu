@@ -37,6 +37,11 @@ void launch_vmult(Context& ctx, int level, int prec, void* y, const void* x, con
   launch_vmult_args(ctx, level, prec, VmultArgs{y, x, b, false, 0, m, 0, m});
 }
 
+void launch_vmult_args_public(Context& ctx, int level, int prec, void* y, const void* x, const void* b, int zlo,
+                              int zhi, int c0, int c1) {
+  launch_vmult_args(ctx, level, prec, VmultArgs{y, x, b, true, zlo, zhi, c0, c1});
+}
+
 void launch_vmult_zrange(Context& ctx, int level, int prec, void* y, const void* x, const void* b, int z0, int z1) {
   const int m = ctx.dev[0][level].lay.m;
   launch_vmult_args(ctx, level, prec, VmultArgs{y, x, b, false, 0, m, z0, z1});

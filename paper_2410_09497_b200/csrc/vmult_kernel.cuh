@@ -168,6 +168,7 @@ struct Geo {
   int nlim[3];  // exclusive node limit of the outputs per axis (n, n, z_end * H)
   int mlim[3];  // exclusive cell limit per axis (m, m, z_end)
   int zoff;     // first z node plane the vector holds (0, or zlo * H for a slab): TMA maps are slab-local
+  int zend;     // one past the last z node plane of the held cells (u_z holds one more plane)
   int c0[3];  // brick cell origin
   int g0[3];  // brick node origin
 };
@@ -264,7 +265,7 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
         for (int r = tid; r < UY * UZ; r += NT) {
           const int y = y0 + r % UY, z = z0 + r / UY;
           T* dst = sU + r * UX;
-          if (y >= 0 && y < n && z >= 0 && z < n) {
+          if (y >= 0 && y < n && z >= G.zoff && z < G.zend) {
             const int64_t start = (static_cast<int64_t>(z) * n + y) * (n + 1) + G.g0[0] - H;
             const int64_t sal = start >= 0 ? start / BR::VEC * BR::VEC : -((-start + BR::VEC - 1) / BR::VEC) * BR::VEC;
             // rows at y = 0 must not reach back into plane z - 1 (for a slab, that plane may not be held)
@@ -301,7 +302,7 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
       const int l[3] = {i % XE - H, (i / XE) % UY - H, i / (XE * UY) - H};
       const int g[3] = {G.g0[0] + l[0], G.g0[1] + l[1], G.g0[2] + l[2]};
       bool ok = g[0] >= 0 && g[1] >= 0 && g[2] >= 0 && g[0] < gd[0] && g[1] < gd[1] && g[2] < gd[2];
-      ok = ok && g[C] != 0 && g[C] != n;
+      ok = ok && g[C] != 0 && g[C] != n && g[2] >= G.zoff && g[2] < G.zend + (C == 2);
       const T* src = ok ? xc + (static_cast<int64_t>(g[2]) * gd[1] + g[1]) * gd[0] + g[0] : xc;
       const int sh = C == 0 ? row_shift0<T>(G, H, g[1]) : brick_shift<T>(G, H);
       cp_async_elem(sU + (i / XE) * UX + sh + (l[0] + H), src, ok);
@@ -327,7 +328,7 @@ __device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const Blocks<const
     for (int i = threadIdx.x; i < E0 * E1 * E2; i += NT) {
       const int lx = i % E0, ly = (i / E0) % E1, lz = i / (E0 * E1);
       const int gx = G.g0[0] + lx - H, gy = G.g0[1] + ly - H, gz = G.g0[2] + lz - H;
-      const bool ok = gx >= 0 && gy >= 0 && gz >= 0 && gx < n && gy < n && gz < n;
+      const bool ok = gx >= 0 && gy >= 0 && gz >= G.zoff && gx < n && gy < n && gz < G.zend;
       const T* src = ok ? xp + (static_cast<int64_t>(gz) * n + gy) * n + gx : xp;
       cp_async_elem(sP + (lz * E1 + ly) * BR::PXT + sh + lx, src, ok);
     }
@@ -734,6 +735,7 @@ __device__ __forceinline__ void brick_geo(Geo& G, int brick, int lnbx, int lnby,
 template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, bool RESID, bool TMA>
 __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<const T> X, const Blocks<T> Y,
                                                              const Blocks<const T> B, int m, int zc0, int zc1, int zlo,
+                                                             int zhi,
                                                              T h,
                                                              const Maps* __restrict__ mapsp) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
@@ -753,6 +755,7 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
   G.mlim[0] = G.mlim[1] = m;
   G.mlim[2] = zc1;
   G.zoff = Gn.zoff = zlo * H;
+  G.zend = Gn.zend = zhi * H;
   for (int a = 0; a < 3; ++a) {
     Gn.nlim[a] = G.nlim[a];
     Gn.mlim[a] = G.mlim[a];
@@ -956,13 +959,12 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
   const int m = ctx.dev[0][level].lay.m, n = ctx.dev[0][level].lay.n;
   const LevelLayout lay = a.slab ? LevelLayout(K, level, a.zlo, a.zhi) : ctx.dev[0][level].lay;
   if (a.slab) {
-    // the owned range must be whole bricks unless it ends at the domain top (bricks never read past
-    // the planes a slab holds), and the slab must hold one ghost cell beyond each interior end
-    if (a.z0 < 0 || a.z1 > m || a.z0 >= a.z1 || a.zlo != std::max(a.z0 - 1, 0) || a.zhi != std::min(a.z1 + 1, m))
-      throw std::invalid_argument("slab: held cells must be the owned cells plus one ghost cell per interior side");
-    if (a.z1 < m && (a.z1 - a.z0) % BZ != 0)
-      throw std::invalid_argument("slab: owned cell range must be a multiple of the brick depth (" + std::to_string(BZ) +
-                                  ") unless it ends at the top of the domain");
+    // the vector must hold one cell beyond each end of the computed range (inside the domain); staging
+    // never reads planes outside the held range (bounds in the kernel, OOB fill of the slab-local maps),
+    // and rows of a partial last brick beyond z1 are masked
+    if (a.z0 < 0 || a.z1 > m || a.z0 >= a.z1 || a.zlo > std::max(a.z0 - 1, 0) || a.zhi < std::min(a.z1 + 1, m) ||
+        a.zlo < 0 || a.zhi > m)
+      throw std::invalid_argument("slab: the held cells must cover the computed cells plus one neighbour cell layer");
   }
   const Blocks<const T> X = block_bases(lay, static_cast<const T*>(a.x));
   const Blocks<T> Y = block_bases(lay, static_cast<T*>(a.y));
@@ -982,7 +984,7 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
   if (tma) {
     // tensor maps are cached per (input vector, slab, level, precision) in 64-B aligned global
     // slots, written stream-ordered before the launch
-    const TmapKey key{a.x, level, static_cast<int>(sizeof(T)), a.zlo};
+    const TmapKey key{a.x, level, static_cast<int>(sizeof(T)), a.zlo, a.zhi};
     auto it = ctx.tmap_slots.find(key);
     if (it == ctx.tmap_slots.end()) {
       const int slot = ctx.tmap_next++ % kTmapSlots;
@@ -1002,7 +1004,7 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
     static std::set<const void*> attr_set;  // kernels whose smem limit is raised already
     if (attr_set.insert(reinterpret_cast<const void*>(kern)).second)
       SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    kern<<<grid, NT, smem, ctx.stream>>>(X, Y, B, m, a.z0, a.z1, a.zlo, h, dmaps);
+    kern<<<grid, NT, smem, ctx.stream>>>(X, Y, B, m, a.z0, a.z1, a.zlo, a.zhi, h, dmaps);
   };
   if (a.b) {
     if (tma) go(stokes_vmult_kernel<T, K, BX, BY, BZ, OCC, NT, true, true>);

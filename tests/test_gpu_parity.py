@@ -231,8 +231,41 @@ def test_slab_vmult_matches_global(k, level, nslab):
 
 
 def test_slab_rejects_bad_ranges():
-    from paper_2410_09497_b200 import slab
-    ctx = smg.Context(1, 3)  # k = 1 bricks are 4 cells deep
-    op = slab.SlabOperator(ctx, 3, 0, 2)
-    with pytest.raises(ValueError):
-        op.vmult(op.new_vector(), op.new_vector())
+    import ctypes
+    ctx = smg.Context(1, 3)
+    x = torch.zeros(10 ** 6, dtype=torch.float64, device="cuda")
+    # rows of cells [4, 8) need the held range to cover cells 3 .. 8
+    rc = smg.lib().smg_residual_held(ctx._h, 3, smg.F64, ctypes.c_void_p(x.data_ptr()), None,
+                                     ctypes.c_void_p(x[10:].data_ptr()), 4, 8, 4, 8)
+    assert rc == smg.SMG_EINVAL
+
+
+@pytest.mark.parametrize("k,level,nparts", [(2, 4, 2), (1, 4, 2), (2, 4, 4), (3, 3, 2)])
+def test_slab_multigrid_matches_single_gpu(k, level, nparts):
+    # distributed V-cycle / FGMRES on virtual slabs (ghost exchange, face patches computed on both
+    # sides, restriction from the extended residual, agglomerated coarse levels) == single GPU
+    from paper_2410_09497_b200 import slab_mg
+    ctx = smg.Context(k, level, cg_max_iter=10, cg_fixed=True)
+    mg = slab_mg.virtual_partition(ctx, level, nparts)
+    assert mg.la < level
+    b = dev(rand_vec(k, level, 21))
+    for dt in (torch.float64, torch.float32):
+        bb = b.to(dt)
+        ref = ctx.vcycle(level, bb)
+        parts = {p: mg.slabs[p][level].extract(bb) for p in mg.parts}
+        xs = mg.vcycle(level, parts, dt)
+        got = torch.zeros_like(bb)
+        for p in mg.parts:
+            mg.slabs[p][level].add_owned_into(got, xs[p])
+        tol = 1e-12 if dt == torch.float64 else 1e-5
+        assert rel(got.double().cpu().numpy(), ref.double().cpu().numpy()) <= tol
+    rhs = ctx.apply_stokes(level, b)
+    x_ref, it_ref, _ = ctx.solve(level, rhs, 1e-8, 40, smg.F32)
+    parts = {p: mg.slabs[p][level].extract(rhs) for p in mg.parts}
+    xs, it, hist = mg.solve(parts, 1e-8, 40, smg.F32)
+    assert abs(it - it_ref) <= 1
+    got = torch.zeros_like(rhs)
+    for p in mg.parts:
+        mg.slabs[p][level].add_owned_into(got, xs[p])
+    res = float((rhs - ctx.apply_stokes(level, got)).norm() / rhs.norm())
+    assert res <= 2e-8
