@@ -10,7 +10,8 @@ Each step is one fp64 operator apply y = A x; x and y are 227 MB each (> 126 MB 
 is needed between steps. Under torchrun (N > 1) the SAME global problem is split into N z-slabs, one
 per GPU (strong scaling): each step is the ghost-layer exchange over NCCL (P2P send/recv of one cell
 layer per neighbour and block) followed by the slab operator; value = global DoF / max-over-ranks
-step time. The smoother and the MG solve are single-GPU in round 1 (reported at N = 1 only).
+step time. The MG solve runs on the same slabs (slab_mg: ghost exchange per smoothing colour, coarse
+levels agglomerated); the smoother DoF/s line is reported at N = 1 only.
 """
 import argparse
 import json
@@ -287,6 +288,23 @@ def main():
         op = slab.SlabOperator(ctx, level, z0, z1, rank, world)
         L = op.lay
         xsl = L.extract(x).contiguous()
+        if not args.no_solve:
+            # distributed MG-FGMRES: same global right-hand side, z-slab multigrid (slab_mg)
+            from paper_2410_09497_b200 import slab_mg
+            bglob = ctx.apply_stokes(level, x)
+            mg = slab_mg.SlabMG(ctx, level, slab.partition(level, world), [rank], world=world)
+            bparts = {rank: mg.slabs[rank][level].extract(bglob)}
+            del bglob
+            mg.solve(bparts, 1e-8, 30, smg.F32)  # warm-up
+            barrier()
+            t0 = time.perf_counter()
+            _, it, hist = mg.solve(bparts, 1e-8, 30, smg.F32)
+            torch.cuda.synchronize()
+            ts = max_over_ranks(time.perf_counter() - t0)
+            extra["solve"] = {"iterations": it, "rel_residual": float(hist[-1] / hist[0]), "time_s": ts,
+                              "ns_per_dof": ts / N * 1e9, "tol": 1e-8,
+                              "precision": "fp64 FGMRES + fp32 V-cycle, z-slab multigrid over the ranks "
+                                           f"(agglomerated below level {mg.la + 1})"}
         del x
         torch.cuda.empty_cache()
         ysl = op.new_vector()

@@ -127,6 +127,13 @@ class SlabMG:
                         S.block(vs[p], c)[sa:sb] = T.block(vs[q], c)[ta:tb]
             return
         import torch.distributed as dist
+        if dist.get_backend(self.group) == "gloo" and any(v.is_cuda for v in vs.values()):
+            # gloo has no CUDA P2P: stage through host memory (logic checks on single-GPU boxes)
+            hs = {p: v.cpu() for p, v in vs.items()}
+            self.exchange(l, hs)
+            for p in vs:
+                vs[p].copy_(hs[p])
+            return
         ops = []
         for p in self.parts:
             S = self.slabs[p][l]
@@ -154,6 +161,11 @@ class SlabMG:
         if self.virtual:
             return contrib
         import torch.distributed as dist
+        if dist.get_backend(self.group) == "gloo" and contrib.is_cuda:
+            h = contrib.cpu()
+            dist.all_reduce(h, group=self.group)
+            contrib.copy_(h)
+            return contrib
         dist.all_reduce(contrib, group=self.group)
         return contrib
 
@@ -169,7 +181,8 @@ class SlabMG:
         if not self.virtual and self.world > 1:
             import torch
             import torch.distributed as dist
-            t = torch.tensor([tot], dtype=torch.float64, device=f"cuda:{self.ctx.device}")
+            gloo = dist.get_backend(self.group) == "gloo"
+            t = torch.tensor([tot], dtype=torch.float64, device="cpu" if gloo else f"cuda:{self.ctx.device}")
             dist.all_reduce(t, group=self.group)
             tot = float(t.item())
         return tot
