@@ -634,6 +634,26 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       g[O2] = G.g0[O2] + oj;
       const bool inside = g[O1] < G.nlim[O1] && g[O2] < G.nlim[O2];
       T* yp = sYP + oi * YSO1 + oj * YSO2;
+      // residual: the b values of this item's rows are loaded up front so their HBM latency overlaps
+      // the contractions (loads inside the store path were exposed: residual 1.8x the plain apply)
+      constexpr bool DIRECT = !(C == 0 && (kStageUx || RESID));
+      T bvel[S3 * H], bpre[S3 * H];
+      if constexpr (RESID) {
+#pragma unroll
+        for (int j = 0; j < S3 * H; ++j) {
+          bvel[j] = T(0);
+          bpre[j] = T(0);
+          if (DIRECT) {
+            int gg[3] = {g[0], g[1], g[2]};
+            gg[C] = G.g0[C] + e0 * H + j;
+            if (inside && gg[C] < G.nlim[C]) bvel[j] = bc[gg[0] * st[0] + gg[1] * st[1] + gg[2] * st[2]];
+          }
+          if (C == 2) {
+            const int gz = G.g0[2] + e0 * H + j;
+            if (inside && gz < G.nlim[2]) bpre[j] = B.c[3][(static_cast<int64_t>(gz) * n + g[1]) * n + g[0]];
+          }
+        }
+      }
 #pragma unroll
       for (int ee = 0; ee < S3; ++ee) {
         const int e = e0 + ee;
@@ -652,7 +672,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
             if (a == 0) w += cref<T>(R::D + i * P + H) * q[ee * H + i];
           }
           const T val = h * v + h2 * w;
-          if (C == 0 && kStageUx) {
+          if (C == 0 && (kStageUx || RESID)) {
             sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
           } else {
             g[C] = G.g0[C] + e * H + a;
@@ -660,7 +680,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
               const int64_t gi = g[0] * st[0] + g[1] * st[1] + g[2] * st[2];
               T rr = val;
               if (g[C] == 0) rr = T(0);  // constrained boundary-normal row
-              else if (RESID) rr = bc[gi] - rr;
+              else if (RESID) rr = bvel[ee * H + a] - rr;
               yc[gi] = rr;
             }
           }
@@ -681,18 +701,18 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
             if (inside && gz < G.nlim[2]) {
               const int64_t gi = (static_cast<int64_t>(gz) * n + g[1]) * n + g[0];
               const T vp = yp[(e * H + i) * YSC] + h2 * z;
-              Y.c[3][gi] = RESID ? B.c[3][gi] - vp : vp;
+              Y.c[3][gi] = RESID ? bpre[ee * H + i] - vp : vp;
             }
           }
         }
       }
       // the constrained plane g_c = n belongs to the brick holding the last cell along c
-      if ((C != 0 || !kStageUx) && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
+      if ((C != 0 || !(kStageUx || RESID)) && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
         g[C] = n;
         yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
       }
     }
-    if (C == 0 && kStageUx) {
+    if (C == 0 && (kStageUx || RESID)) {
       __syncthreads();
       // coalesced write-out of the u_x rows (x = c fastest), plus the constrained plane x = n
       const bool last = G.c0[0] + NCc >= m;
