@@ -636,7 +636,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       T* yp = sYP + oi * YSO1 + oj * YSO2;
       // residual: the b values of this item's rows are loaded up front so their HBM latency overlaps
       // the contractions (loads inside the store path were exposed: residual 1.8x the plain apply)
-      constexpr bool DIRECT = !(C == 0 && (kStageUx || RESID));
+      constexpr bool DIRECT = !(C == 0 && kStageUx);
       T bvel[S3 * H], bpre[S3 * H];
       if constexpr (RESID) {
 #pragma unroll
@@ -672,7 +672,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
             if (a == 0) w += cref<T>(R::D + i * P + H) * q[ee * H + i];
           }
           const T val = h * v + h2 * w;
-          if (C == 0 && (kStageUx || RESID)) {
+          if (C == 0 && kStageUx) {
             sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
           } else {
             g[C] = G.g0[C] + e * H + a;
@@ -707,12 +707,12 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         }
       }
       // the constrained plane g_c = n belongs to the brick holding the last cell along c
-      if ((C != 0 || !(kStageUx || RESID)) && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
+      if ((C != 0 || !kStageUx) && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
         g[C] = n;
         yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
       }
     }
-    if (C == 0 && (kStageUx || RESID)) {
+    if (C == 0 && kStageUx) {
       __syncthreads();
       // coalesced write-out of the u_x rows (x = c fastest), plus the constrained plane x = n
       const bool last = G.c0[0] + NCc >= m;
