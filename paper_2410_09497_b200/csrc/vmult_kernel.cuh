@@ -222,7 +222,8 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                : "memory");
 }
 
-__device__ __forceinline__ int floor_to(int v, int q) { return (v >= 0 ? v / q : -((-v + q - 1) / q)) * q; }
+// floor to a multiple of the power of two q (two's complement: also right for negative v)
+__device__ __forceinline__ int floor_to(int v, int q) { return v & -q; }
 
 // smem origin offsets of the staged rows (element of x = g0x - H relative to the row start)
 // smem position of element x0 in a staged 3D box row: PADF + x0 - xs, xs = max(floor16B(x0), 0);
@@ -238,8 +239,7 @@ __device__ __forceinline__ int brick_shift(const Geo& G, int H) {
 template <typename T>
 __device__ __forceinline__ int row_shift0(const Geo& G, int H, int y) {
   constexpr int VEC = 16 / static_cast<int>(sizeof(T));
-  const int v = (y * (G.n + 1) + G.g0[0] - H) % VEC;
-  return v < 0 ? v + VEC : v;
+  return (y * (G.n + 1) + G.g0[0] - H) & (VEC - 1);  // non-negative residue (power-of-two VEC)
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -267,7 +267,7 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
           T* dst = sU + r * UX;
           if (y >= 0 && y < n && z >= G.zoff && z < G.zend) {
             const int64_t start = (static_cast<int64_t>(z) * n + y) * (n + 1) + G.g0[0] - H;
-            const int64_t sal = start >= 0 ? start / BR::VEC * BR::VEC : -((-start + BR::VEC - 1) / BR::VEC) * BR::VEC;
+            const int64_t sal = start & -static_cast<int64_t>(BR::VEC);  // floor to a 16-B boundary
             // rows at y = 0 must not reach back into plane z - 1 (for a slab, that plane may not be held)
             const int64_t row0 = static_cast<int64_t>(z) * n * (n + 1);
             const int64_t ss = (y == 0 && sal < row0) ? row0 : sal;
@@ -355,10 +355,15 @@ __device__ __forceinline__ void fix_columns(T* sU0, T* sU1, T* sU2, T* sP, const
   }
   if (x0 > 0 && x0 + BR::XEXT(0) <= G.n) return;
   if (sU0) {
+    // only the columns gx <= 0 (left end: x0 <= 0) or gx >= n (right end) of every row
     constexpr int XE = BR::XEXT(0), UY = BR::UY(0), ROWS = BR::UY(0) * BR::UZ(0);
-    for (int i = threadIdx.x; i < ROWS * XE; i += NT) {
-      const int r = i / XE, gx = x0 + i % XE;
-      if (gx <= 0 || gx >= G.n) sU0[r * BR::UX(0) + row_shift0<T>(G, H, G.g0[1] - H + r % UY) + i % XE] = T(0);
+    const int lo = x0 <= 0 ? 1 - x0 : 0;                  // columns [0, lo) have gx <= 0
+    const int hi = G.n - x0 < XE ? G.n - x0 : XE;          // columns [hi, XE) have gx >= n
+    const int nl = lo, nr = XE - hi, per = nl + nr;
+    for (int i = threadIdx.x; i < ROWS * per; i += NT) {
+      const int r = i / per, j = i - r * per;
+      const int col = j < nl ? j : hi + (j - nl);
+      sU0[r * BR::UX(0) + row_shift0<T>(G, H, G.g0[1] - H + r % UY) + col] = T(0);
     }
   }
   if (x0 >= 0) return;
@@ -637,21 +642,20 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       // residual: the b values of this item's rows are loaded up front so their HBM latency overlaps
       // the contractions (loads inside the store path were exposed: residual 1.8x the plain apply)
       constexpr bool DIRECT = !(C == 0 && kStageUx);
+      // global index of the item's first row (node G.g0[C] + e0 H along c); rows step by st[C]
+      const int gc0 = G.g0[C] + e0 * H;
+      const int64_t gbase = g[O1] * st[O1] + g[O2] * st[O2] + gc0 * st[C];
+      const int64_t pbase = C == 2 ? (static_cast<int64_t>(gc0) * n + g[1]) * n + g[0] : 0;  // pressure, C = 2
+      const int64_t pplane = static_cast<int64_t>(n) * n;
       T bvel[S3 * H], bpre[S3 * H];
       if constexpr (RESID) {
 #pragma unroll
         for (int j = 0; j < S3 * H; ++j) {
           bvel[j] = T(0);
           bpre[j] = T(0);
-          if (DIRECT) {
-            int gg[3] = {g[0], g[1], g[2]};
-            gg[C] = G.g0[C] + e0 * H + j;
-            if (inside && gg[C] < G.nlim[C]) bvel[j] = bc[gg[0] * st[0] + gg[1] * st[1] + gg[2] * st[2]];
-          }
-          if (C == 2) {
-            const int gz = G.g0[2] + e0 * H + j;
-            if (inside && gz < G.nlim[2]) bpre[j] = B.c[3][(static_cast<int64_t>(gz) * n + g[1]) * n + g[0]];
-          }
+          const bool ok = inside && gc0 + j < G.nlim[C];
+          if (DIRECT && ok) bvel[j] = bc[gbase + j * st[C]];
+          if (C == 2 && ok) bpre[j] = B.c[3][pbase + j * pplane];
         }
       }
 #pragma unroll
@@ -675,13 +679,12 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
           if (C == 0 && kStageUx) {
             sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
           } else {
-            g[C] = G.g0[C] + e * H + a;
-            if (inside && g[C] < G.nlim[C]) {
-              const int64_t gi = g[0] * st[0] + g[1] * st[1] + g[2] * st[2];
+            const int gc = gc0 + ee * H + a;
+            if (inside && gc < G.nlim[C]) {
               T rr = val;
-              if (g[C] == 0) rr = T(0);  // constrained boundary-normal row
+              if (gc == 0) rr = T(0);  // constrained boundary-normal row
               else if (RESID) rr = bvel[ee * H + a] - rr;
-              yc[gi] = rr;
+              yc[gbase + (ee * H + a) * st[C]] = rr;
             }
           }
         }
@@ -697,11 +700,9 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
           } else if (C == 1) {
             yp[(e * H + i) * YSC] += h2 * z;
           } else {
-            const int gz = G.g0[2] + e * H + i;
-            if (inside && gz < G.nlim[2]) {
-              const int64_t gi = (static_cast<int64_t>(gz) * n + g[1]) * n + g[0];
+            if (inside && gc0 + ee * H + i < G.nlim[2]) {
               const T vp = yp[(e * H + i) * YSC] + h2 * z;
-              Y.c[3][gi] = RESID ? bpre[ee * H + i] - vp : vp;
+              Y.c[3][pbase + (ee * H + i) * pplane] = RESID ? bpre[ee * H + i] - vp : vp;
             }
           }
         }
