@@ -28,6 +28,11 @@ DEGREE, LEVEL = 2, 5
 METRIC = "Stokes operator-apply DoF/s (fp64), RT_2 64^3 cells; + fp32 smoother DoF/s and MG-FGMRES solve time"
 
 
+# brick shapes of the operator kernel per degree (fp64), csrc/vmult_kernel.cuh BrickShape
+SHAPES = {1: "8x4x4-cell bricks, 2 CTAs/SM, 256 threads", 2: "4x4x2-cell bricks, 2 CTAs/SM, 256 threads",
+          3: "4x2x2-cell bricks, 1 CTA/SM, 256 threads", 4: "2x2x2-cell bricks, 384 threads"}
+
+
 def dofs(k, level):
     n = (2 << level) * (k + 1)
     return 3 * (n + 1) * n * n + n ** 3
@@ -357,7 +362,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "kernel": f"stokes_vmult_kernel<double,{k}> (k=2: 4x4x2-cell bricks, 2 CTAs/SM, 256 threads)"},
+                     "kernel": f"stokes_vmult_kernel<double,{k}> ({SHAPES.get(k, 'see DESIGN.md')})"},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
     }
     out.update(extra)
