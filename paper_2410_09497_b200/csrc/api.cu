@@ -324,9 +324,9 @@ void vmult_host_pipelined(Context& c, int level, int prec, void* const y_vel[3],
     SMG_CUDA(cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking));
     SMG_CUDA(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking));
   }
-  // chunks of 4k cells (every brick depth divides 4), at most 8
+  // chunks of 4k cells (every brick depth divides 4), at most 16
   const int m = lay.m;
-  int chunk = std::max(4, (m / 8) / 4 * 4);
+  int chunk = std::max(4, (m / 16) / 4 * 4);
   if (m < 8) chunk = m;
   const int nchunk = (m + chunk - 1) / chunk;
   std::vector<cudaEvent_t> ev_in(nchunk), ev_comp(nchunk);
