@@ -1085,11 +1085,11 @@ struct Variants<2> {
   template <typename T>
   static bool run(int v, Context& ctx, int level, const VmultArgs& a) {
     switch (v) {
-      case 1: launch_shape<T, 2, Shape<4, 4, 2, 384, 2>>(ctx, level, a); return true;
-      case 2: launch_shape<T, 2, Shape<4, 2, 2, 256, 2>>(ctx, level, a); return true;
-      case 3: launch_shape<T, 2, Shape<2, 2, 2, 128, 4>>(ctx, level, a); return true;
+      case 1: launch_shape<T, 2, Shape<4, 4, 2, 192, 2>>(ctx, level, a); return true;
+      case 2: launch_shape<T, 2, Shape<4, 4, 2, 160, 2>>(ctx, level, a); return true;
+      case 3: launch_shape<T, 2, Shape<4, 4, 2, 224, 2>>(ctx, level, a); return true;
       case 4: launch_shape<T, 2, Shape<4, 4, 4, 512, 1>>(ctx, level, a); return true;
-      case 5: launch_shape<T, 2, Shape<8, 2, 2, 256, 2>>(ctx, level, a); return true;
+      case 5: launch_shape<T, 2, Shape<4, 4, 4, 384, 1>>(ctx, level, a); return true;
       default: return false;
     }
   }
@@ -1103,6 +1103,19 @@ struct Variants<3> {
       case 2: launch_shape<T, 3, Shape<4, 2, 2, 256, 1>>(ctx, level, a); return true;
       case 3: launch_shape<T, 3, Shape<4, 2, 2, 384, 1>>(ctx, level, a); return true;
       case 4: launch_shape<T, 3, Shape<4, 2, 1, 256, 2>>(ctx, level, a); return true;
+      default: return false;
+    }
+  }
+};
+template <>
+struct Variants<4> {
+  template <typename T>
+  static bool run(int v, Context& ctx, int level, const VmultArgs& a) {
+    switch (v) {
+      case 1: launch_shape<T, 4, Shape<2, 2, 2, 256, 1>>(ctx, level, a); return true;
+      case 2: launch_shape<T, 4, Shape<2, 2, 1, 256, 2>>(ctx, level, a); return true;
+      case 3: launch_shape<T, 4, Shape<4, 2, 1, 256, 1>>(ctx, level, a); return true;
+      case 4: launch_shape<T, 4, Shape<2, 2, 2, 512, 1>>(ctx, level, a); return true;
       default: return false;
     }
   }
