@@ -65,7 +65,7 @@ def test_residual(k, level):
     assert rel(r, r_ref) <= 1e-12
 
 
-@pytest.mark.parametrize("k,level", [(1, 1), (1, 2), (2, 1), (3, 1)])
+@pytest.mark.parametrize("k,level", [(1, 1), (1, 2), (2, 1), (2, 2), (3, 1), (4, 1)])
 def test_smoother_fp64_fixed_cg_matches_oracle(k, level):
     # parity mode: a fixed number of inner CG iterations on both sides
     ctx = smg.Context(k, level, cg_max_iter=12, cg_fixed=True, cg_precond=1)
@@ -86,7 +86,7 @@ def test_smoother_fp32_matches_oracle(k, level):
     assert rel(x.double().cpu().numpy(), x_ref) <= 1e-4
 
 
-@pytest.mark.parametrize("k,level", [(1, 1), (2, 1), (2, 2), (3, 1)])
+@pytest.mark.parametrize("k,level", [(1, 1), (2, 1), (2, 2), (3, 1), (4, 1), (5, 1), (7, 1)])
 def test_transfer_matches_oracle(k, level):
     ctx = smg.Context(k, level)
     xc = rand_vec(k, level - 1, 9)
