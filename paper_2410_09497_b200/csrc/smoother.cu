@@ -1,482 +1,23 @@
-// K3: vertex-patch multiplicative Schwarz smoother, one colour per launch (smooth SPEC.md:400-408,
-// Alg. 2), local solver = Schur complement + fast diagonalisation
-// (schur_solve SPEC.md:356-364, Eq. 9):
-//   S P = B A^-1 F - G,   S = B A^-1 B^T,   U = A^-1 (F - B^T P),
-// with projected, pressure-mass-preconditioned CG on the patch pressure.
-//
-// B200 design: ONE WARP PER PATCH. All patch vectors live in the warp's slice of shared memory;
-// every step is a warp-synchronous pencil contraction with compile-time shapes (no CTA barriers).
-// Per component c and axis a, the fast-diagonalisation eigenvectors S_a are pre-multiplied with
-// the divergence factor of that axis at setup (G_a = D S_par along c, G_a = M' S_orth otherwise),
-// so B_c A_c^-1 B_c^T = (G (x) G (x) G) Lambda_c^-1 (G (x) G (x) G)^T costs 6 contractions instead of
-// 12, and the final velocity is U_c = (S (x) S (x) S) Lambda_c^-1 [S^T F_c - G^T P] re-using the
-// eigen-coefficients of F computed once. Same-colour patches write disjoint DoFs, so
-// the scatter is race-free and order-independent. The residual r = b - A x is refreshed per colour by
-// the vmult kernel in residual mode.
+// K3 dispatch (kernel in smoother_kernel.cuh, one TU per degree smoother_k<K>.cu) and the packed patch
+// tables uploaded at context creation.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 
-#include "smg_internal.cuh"
+#include "smoother.cuh"
 
 namespace smg {
 namespace {
 
-// Packed patch tables (pack_patch_tables; sizes in elements of T). Every matrix is stored twice, as
-// rows of M and rows of M^T, each row padded to a multiple of 4 elements (R4), so that a contraction
-// reads the coefficients of one output as 16-byte vectors (LDS.128) -- the coefficient broadcasts
-// were the largest instruction class after FFMA (profiles/r01 ncu_smoother_v6).
 constexpr int R4(int v) { return (v + 3) / 4 * 4; }
-template <int K>
-struct PD {
-  static constexpr int NP = 2 * K + 1;  // parallel (C0 interior nodes of the 2-cell patch)
-  static constexpr int NO = 2 * K + 2;  // orthogonal (DG) / pressure
-  static constexpr int NV = NP * NO * NO;
-  static constexpr int NPR = NO * NO * NO;
-  static constexpr int BIG = NV > NPR ? NV : NPR;
-  static constexpr int SQP = NP * R4(NP), SQO = NO * R4(NO);
-  static constexpr int PAR_S = 0;                        // S_par rows          NP x R4(NP)
-  static constexpr int PAR_ST = PAR_S + SQP;             // S_par^T rows        NP x R4(NP)
-  static constexpr int PAR_L = PAR_ST + SQP;             // eigenvalues         R4(NP)
-  static constexpr int ORTH_S = PAR_L + R4(NP);          // 4 x S_orth rows     NO x R4(NO)
-  static constexpr int ORTH_ST = ORTH_S + 4 * SQO;       // 4 x S_orth^T rows
-  static constexpr int ORTH_L = ORTH_ST + 4 * SQO;       // 4 x R4(NO)
-  static constexpr int G_PAR = ORTH_L + 4 * R4(NO);      // (D S_par) rows      NO x R4(NP)
-  static constexpr int G_PART = G_PAR + NO * R4(NP);     // (D S_par)^T rows    NP x R4(NO)
-  static constexpr int G_ORTH = G_PART + NP * R4(NO);    // 4 x (M' S_orth) rows
-  static constexpr int G_ORTHT = G_ORTH + 4 * SQO;       // 4 x transposed
-  static constexpr int MPI = G_ORTHT + 4 * SQO;          // M'^-1 rows          NO x R4(NO)
-  static constexpr int TAB = MPI + SQO;
-  static constexpr int TABP = (TAB + 3) / 4 * 4;
-  static constexpr int LINV = (3 * NV + 3) / 4 * 4;  // CTA-shared reciprocal eigenvalue sums (interior)
-  // per-patch workspace: Fh (3 NV) | r z d q x (5 NPR) | T1 T2 (2 BIG)
-  static constexpr int WS = 3 * NV + 5 * NPR + 2 * BIG;
-  static constexpr int dv(int c, int a) { return a == c ? NP : NO; }
-};
 
-template <typename T>
-struct Vec16;
-template <>
-struct Vec16<float> {
-  using type = float4;
-  static constexpr int N = 4;
-};
-template <>
-struct Vec16<double> {
-  using type = double2;
-  static constexpr int N = 2;
-};
-
-// out = (M applied along axis AX) in;  in dims (D0,D1,D2), out extent along AX = R.
-// M(i,j) = A[i * R4(C) + j] (rows padded to 16 B). One pencil per lane; the coefficients of output i
-// are read as 16-byte vectors (broadcast LDS.128).
-template <typename T, int D0, int D1, int D2, int AX, int R, int GS, bool ACC = false>
-__device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __restrict__ A, T* __restrict__ out,
-                                          int lane) {
-  constexpr int DI[3] = {D0, D1, D2};
-  constexpr int C = DI[AX];
-  constexpr int DO0 = AX == 0 ? R : D0, DO1 = AX == 1 ? R : D1;
-  constexpr int SI = AX == 0 ? 1 : (AX == 1 ? D0 : D0 * D1);
-  constexpr int SO = AX == 0 ? 1 : (AX == 1 ? DO0 : DO0 * DO1);
-  constexpr int QA = AX == 0 ? D1 : D0;  // the two other axes, in order
-  constexpr int NPEN = D0 * D1 * D2 / C;
-  for (int p = lane; p < NPEN; p += GS) {
-    const int u = p % QA, v = p / QA;
-    int bi, bo;
-    if (AX == 0) {
-      bi = (v * D1 + u) * D0;
-      bo = (v * DO1 + u) * DO0;
-    } else if (AX == 1) {
-      bi = v * D0 * D1 + u;
-      bo = v * DO0 * DO1 + u;
-    } else {
-      bi = v * D0 + u;
-      bo = v * DO0 + u;
-    }
-    using V = typename Vec16<T>::type;
-    constexpr int NV = Vec16<T>::N, LD = R4(C), NVR = (C + NV - 1) / NV;
-    T x[NVR * NV];
-#pragma unroll
-    for (int j = 0; j < NVR * NV; ++j) x[j] = j < C ? in[bi + j * SI] : T(0);
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const V* Ai = reinterpret_cast<const V*>(A + i * LD);
-      T s = T(0);
-#pragma unroll
-      for (int q = 0; q < NVR; ++q) {
-        const V a = Ai[q];
-        if constexpr (Vec16<T>::N == 4) {
-          s += a.x * x[4 * q];
-          if (4 * q + 1 < C) s += a.y * x[4 * q + 1];
-          if (4 * q + 2 < C) s += a.z * x[4 * q + 2];
-          if (4 * q + 3 < C) s += a.w * x[4 * q + 3];
-        } else {
-          s += a.x * x[2 * q];
-          if (2 * q + 1 < C) s += a.y * x[2 * q + 1];
-        }
-      }
-      if (ACC) out[bo + i * SO] += s;
-      else out[bo + i * SO] = s;
-    }
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// a patch is solved by a group of GS threads: one warp (GS = 32, many patches per CTA, warp-synchronous)
-// or a whole CTA (GS > 32, coarse levels where there are too few patches to fill the GPU and the
-// per-patch latency dominates)
-template <int GS>
-__device__ __forceinline__ void gsync() {
-  if constexpr (GS == 32) gsync<GS>();
-  else __syncthreads();
-}
-template <int GS, typename T>
-__device__ __forceinline__ T group_sum(T v) {
-  v = warp_sum(v);
-  if constexpr (GS == 32) {
-    return v;
-  } else {
-    __shared__ T red[GS / 32];
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    T s = T(0);
-#pragma unroll
-    for (int w = 0; w < GS / 32; ++w) s += red[w];
-    return s;
-  }
-}
-
-template <typename T, int K, int GS>
-struct Patch {
-  using P = PD<K>;
-  const T* tab;
-  const T* linv;  // 3 x NV reciprocal eigenvalue sums of the interior variant (CTA-shared)
-  bool interior;
-  int var[3];
-  int lane;
-
-  // rows of S (TR = false) or of S^T (TR = true) along axis a of component c
-  __device__ const T* S(int c, int a, bool tr) const {
-    return a == c ? tab + (tr ? P::PAR_ST : P::PAR_S) : tab + (tr ? P::ORTH_ST : P::ORTH_S) + var[a] * P::SQO;
-  }
-  __device__ const T* L(int c, int a) const { return a == c ? tab + P::PAR_L : tab + P::ORTH_L + var[a] * R4(P::NO); }
-  __device__ const T* G(int c, int a, bool tr) const {
-    return a == c ? tab + (tr ? P::G_PART : P::G_PAR) : tab + (tr ? P::G_ORTHT : P::G_ORTH) + var[a] * P::SQO;
-  }
-
-  // eigen-space transforms of a velocity-shaped array of component C (S square per axis):
-  // out = (S0 (x) S1 (x) S2)^T in (TR = true) or (S0 (x) S1 (x) S2) in; uses tmp; out != in.
-  template <int C, bool TR>
-  __device__ void s3(const T* in, T* out, T* tmp) const {
-    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, A0, A1, A2, 0, A0, GS>(in, S(C, 0, TR), out, lane);
-    gsync<GS>();
-    warp_axis<T, A0, A1, A2, 1, A1, GS>(out, S(C, 1, TR), tmp, lane);
-    gsync<GS>();
-    warp_axis<T, A0, A1, A2, 2, A2, GS>(tmp, S(C, 2, TR), out, lane);
-    gsync<GS>();
-  }
-  // pressure (NO^3) -> eigen space of component C: out = (G0 (x) G1 (x) G2)^T in
-  template <int C>
-  __device__ void gt3(const T* in, T* out, T* tmp) const {
-    constexpr int NO = P::NO;
-    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, NO, NO, NO, 0, A0, GS>(in, G(C, 0, true), out, lane);
-    gsync<GS>();
-    warp_axis<T, A0, NO, NO, 1, A1, GS>(out, G(C, 1, true), tmp, lane);
-    gsync<GS>();
-    warp_axis<T, A0, A1, NO, 2, A2, GS>(tmp, G(C, 2, true), out, lane);
-    gsync<GS>();
-  }
-  // eigen space of component C -> pressure: out = (G0 (x) G1 (x) G2) in
-  // acc (=|+=) (G0 (x) G1 (x) G2) in; s1, s2 scratch
-  template <int C, bool ACC>
-  __device__ void g3acc(const T* in, T* acc, T* s1, T* s2) const {
-    constexpr int NO = P::NO;
-    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, A0, A1, A2, 0, NO, GS>(in, G(C, 0, false), s1, lane);
-    gsync<GS>();
-    warp_axis<T, NO, A1, A2, 1, NO, GS>(s1, G(C, 1, false), s2, lane);
-    gsync<GS>();
-    warp_axis<T, NO, NO, A2, 2, NO, GS, ACC>(s2, G(C, 2, false), acc, lane);
-    gsync<GS>();
-  }
-  template <int C>
-  __device__ void g3(const T* in, T* out, T* tmp) const {
-    constexpr int NO = P::NO;
-    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, A0, A1, A2, 0, NO, GS>(in, G(C, 0, false), out, lane);
-    gsync<GS>();
-    warp_axis<T, NO, A1, A2, 1, NO, GS>(out, G(C, 1, false), tmp, lane);
-    gsync<GS>();
-    warp_axis<T, NO, NO, A2, 2, NO, GS>(tmp, G(C, 2, false), out, lane);
-    gsync<GS>();
-  }
-  // t *= Lambda_C^-1 (eigen space of component C). Interior patches (all end variants 0, the vast
-  // majority) multiply by the reciprocal eigenvalue sums tabulated once per CTA (linv); patches at the
-  // domain boundary divide (the division inside the CG loop was 11 % of the smoother's instructions)
-  template <int C>
-  __device__ void lam_inv(T* t) const {
-    if (interior) {
-      const T* li = linv + C * P::NV;
-      for (int o = lane; o < P::NV; o += GS) t[o] *= li[o];
-    } else {
-      constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1);
-      const T* l0 = L(C, 0);
-      const T* l1 = L(C, 1);
-      const T* l2 = L(C, 2);
-      for (int o = lane; o < P::NV; o += GS) {
-        const int x = o % A0, y = (o / A0) % A1, z = o / (A0 * A1);
-        t[o] = t[o] / (l0[x] + l1[y] + l2[z]);
-      }
-    }
-    gsync<GS>();
-  }
-  __device__ void project(T* p) const {
-    T s = T(0);
-    for (int o = lane; o < P::NPR; o += GS) s += p[o];
-    s = group_sum<GS>(s) / T(P::NPR);
-    gsync<GS>();
-    for (int o = lane; o < P::NPR; o += GS) p[o] -= s;
-    gsync<GS>();
-  }
-  __device__ T dot(const T* a, const T* b) const {
-    T s = T(0);
-    for (int o = lane; o < P::NPR; o += GS) s += a[o] * b[o];
-    return group_sum<GS>(s);
-  }
-};
-
-// per-block base pointers of a level vector in the global index space (a z-slab vector passes bases
-// shifted back by its first plane)
-template <typename T>
-struct SBlocks {
-  T* c[4];
-};
-
-template <typename T, int K, int W, int MINB, int GS>
-__global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlocks<T> x, const SBlocks<const T> r,
-                                                              const T* __restrict__ ptab, int m, int colour,
-                                                              int vz_first, int cnt_z, int cg_max_iter, T cg_tol,
-                                                              int cg_fixed, int cg_precond) {
-  using P = PD<K>;
-  constexpr int H = K + 1, NO = P::NO;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* tab = reinterpret_cast<T*>(smem_raw);
-  for (int i = threadIdx.x; i < P::TAB; i += blockDim.x) tab[i] = ptab[i];
-  __syncthreads();
-  {  // reciprocal eigenvalue sums of interior patches (end variant 0 on every axis), per component
-    T* li = tab + P::TABP;
-    for (int i = threadIdx.x; i < 3 * P::NV; i += blockDim.x) {
-      const int c = i / P::NV, o = i % P::NV;
-      const int A0 = P::dv(c, 0), A1 = P::dv(c, 1);
-      const int xyz[3] = {o % A0, (o / A0) % A1, o / (A0 * A1)};
-      T sum = T(0);
-      for (int a = 0; a < 3; ++a) sum += a == c ? tab[P::PAR_L + xyz[a]] : tab[P::ORTH_L + xyz[a]];
-      li[i] = T(1) / sum;
-    }
-    __syncthreads();
-  }
-  const int warp = threadIdx.x / GS, lane = threadIdx.x % GS;  // patch slot in the CTA, thread in its group
-  // vertices of the colour: x / y over the whole level, z from vz_first (cnt_z planes, step 2)
-  const int cnt[3] = {(colour & 1) ? m / 2 : m / 2 - 1, ((colour >> 1) & 1) ? m / 2 : m / 2 - 1, cnt_z};
-  const int npatch = cnt[0] * cnt[1] * cnt[2];
-  const int pid = blockIdx.x * W + warp;
-  if (pid >= npatch) return;
-  const int v[3] = {((colour & 1) ? 1 : 2) + 2 * (pid % cnt[0]), (((colour >> 1) & 1) ? 1 : 2) + 2 * ((pid / cnt[0]) % cnt[1]),
-                    vz_first + 2 * (pid / (cnt[0] * cnt[1]))};
-  T* ws = tab + P::TABP + P::LINV + warp * P::WS;
-  T* Fh = ws;                // 3 x NV eigen coefficients of F_c
-  T* Pr = Fh + 3 * P::NV;    // CG residual
-  T* Pz = Pr + P::NPR;       // preconditioned residual
-  T* Pd = Pz + P::NPR;       // search direction
-  T* Pq = Pd + P::NPR;       // S d
-  T* Px = Pq + P::NPR;       // pressure iterate
-  T* T1 = Px + P::NPR;       // scratch (BIG)
-  T* T2 = T1 + P::BIG;       // scratch (BIG)
-
-  Patch<T, K, GS> ps;
-  ps.tab = tab;
-  ps.lane = lane;
-  for (int a = 0; a < 3; ++a) ps.var[a] = 2 * (v[a] == 1) + (v[a] == m - 1);
-  ps.linv = tab + P::TABP;  // CTA-shared table filled above
-  ps.interior = ps.var[0] == 0 && ps.var[1] == 0 && ps.var[2] == 0;
-  const int n = m * H;
-
-  // ---- gather R_j r: velocity blocks -> T1 -> eigen coefficients Fh_c; pressure -> Pq (= G) ----
-  auto vel_index = [&](int c, int o) {
-    const int d0 = P::dv(c, 0), d1 = P::dv(c, 1);
-    const int xx = o % d0, yy = (o / d0) % d1, zz = o / (d0 * d1);
-    int64_t gd0 = n, gd1 = n;
-    if (c == 0) gd0 = n + 1;
-    if (c == 1) gd1 = n + 1;
-    const int b0 = (v[0] - 1) * H + (c == 0), b1 = (v[1] - 1) * H + (c == 1), b2 = (v[2] - 1) * H + (c == 2);
-    return (static_cast<int64_t>(b2 + zz) * gd1 + b1 + yy) * gd0 + b0 + xx;
-  };
-  auto pres_index = [&](int o) {
-    const int xx = o % NO, yy = (o / NO) % NO, zz = o / (NO * NO);
-    return (static_cast<int64_t>((v[2] - 1) * H + zz) * n + (v[1] - 1) * H + yy) * n + (v[0] - 1) * H + xx;
-  };
-#define SMG_FOR_C(...) \
-  { constexpr int C = 0; __VA_ARGS__ } { constexpr int C = 1; __VA_ARGS__ } { constexpr int C = 2; __VA_ARGS__ }
-  SMG_FOR_C({
-    for (int o = lane; o < P::NV; o += GS) T1[o] = r.c[C][vel_index(C, o)];
-    gsync<GS>();
-    ps.template s3<C, true>(T1, Fh + C * P::NV, T2);
-  })
-  for (int o = lane; o < P::NPR; o += GS) Pq[o] = r.c[3][pres_index(o)];
-  // ---- rhs = sum_c G_c Lambda_c^-1 Fh_c - G  (projected) -> Pr ----
-  for (int o = lane; o < P::NPR; o += GS) Pr[o] = -Pq[o];
-  gsync<GS>();
-  SMG_FOR_C({
-    for (int o = lane; o < P::NV; o += GS) T1[o] = Fh[C * P::NV + o];
-    gsync<GS>();
-    ps.template lam_inv<C>(T1);
-    ps.template g3<C>(T1, T2, Pq);  // result in T2 (Pq used as scratch)
-    for (int o = lane; o < P::NPR; o += GS) Pr[o] += T2[o];
-    gsync<GS>();
-  })
-  ps.project(Pr);
-  auto precond = [&](const T* rr, T* zz) {
-    if (cg_precond) {
-      const T* Mi = tab + P::MPI;
-      warp_axis<T, NO, NO, NO, 0, NO, GS>(rr, Mi, zz, lane);
-      gsync<GS>();
-      warp_axis<T, NO, NO, NO, 1, NO, GS>(zz, Mi, T1, lane);
-      gsync<GS>();
-      warp_axis<T, NO, NO, NO, 2, NO, GS>(T1, Mi, zz, lane);
-      gsync<GS>();
-    } else {
-      for (int o = lane; o < P::NPR; o += GS) zz[o] = rr[o];
-      gsync<GS>();
-    }
-    ps.project(zz);
-  };
-  precond(Pr, Pz);
-  for (int o = lane; o < P::NPR; o += GS) {
-    Pd[o] = Pz[o];
-    Px[o] = T(0);
-  }
-  gsync<GS>();
-  T rz = ps.dot(Pr, Pz);
-  const T r0 = sqrt(ps.dot(Pr, Pr));
-  for (int it = 0; it < cg_max_iter; ++it) {
-    if (!cg_fixed) {
-      if (sqrt(ps.dot(Pr, Pr)) <= cg_tol * r0) break;
-    }
-    // Pq = S Pd = sum_c G_c Lambda_c^-1 G_c^T Pd
-
-    SMG_FOR_C({
-      ps.template gt3<C>(Pd, T1, T2);
-      ps.template lam_inv<C>(T1);
-      ps.template g3acc<C, C != 0>(T1, Pq, T2, Pz);  // Pz is free scratch here (recomputed below)
-    })
-    const T dq = ps.dot(Pd, Pq);
-    if (!(dq > T(0)) || rz == T(0)) break;
-    const T alpha = rz / dq;
-    for (int o = lane; o < P::NPR; o += GS) {
-      Px[o] += alpha * Pd[o];
-      Pr[o] -= alpha * Pq[o];
-    }
-    gsync<GS>();
-    ps.project(Pr);
-    precond(Pr, Pz);
-    const T rzn = ps.dot(Pr, Pz);
-    const T beta = rzn / rz;
-    rz = rzn;
-    for (int o = lane; o < P::NPR; o += GS) Pd[o] = Pz[o] + beta * Pd[o];
-    gsync<GS>();
-  }
-  ps.project(Px);
-  // ---- U_c = (S (x) S (x) S) Lambda_c^-1 [Fh_c - G_c^T P];  x += R^T (U, P) ----
-  SMG_FOR_C({
-    ps.template gt3<C>(Px, T1, T2);
-    for (int o = lane; o < P::NV; o += GS) T1[o] = Fh[C * P::NV + o] - T1[o];
-    gsync<GS>();
-    ps.template lam_inv<C>(T1);
-    ps.template s3<C, false>(T1, T2, Pz);
-    for (int o = lane; o < P::NV; o += GS) x.c[C][vel_index(C, o)] += T2[o];
-  })
-#undef SMG_FOR_C
-  for (int o = lane; o < P::NPR; o += GS) x.c[3][pres_index(o)] += Px[o];
-}
-
-template <typename T, int K>
-constexpr int warps_per_cta() {
-  // keep a CTA at <= ~100 KB so that two fit on an SM
-  constexpr int ws = PD<K>::WS * static_cast<int>(sizeof(T));
-  constexpr int w = 100 * 1024 / ws;
-  return w >= 8 ? 8 : (w >= 4 ? 4 : (w >= 2 ? 2 : 1));
-}
-
-template <typename T>
-SBlocks<T> sblocks(const LevelLayout& lay, T* v) {
-  SBlocks<T> B;
-  const int H = lay.k + 1;
-  for (int c = 0; c < 4; ++c) B.c[c] = v + lay.off[c] - static_cast<int64_t>(lay.zlo) * H * lay.plane[c];
-  return B;
-}
-
-template <typename T, int K, int W, int GS>
-void launch_group(Context& ctx, const DevLevel& dl, const LevelLayout& lay, int npatch, int colour, int vz_first,
-                  int cnt_z, void* x, const void* r) {
-  using P = PD<K>;
-  const size_t smem = sizeof(T) * (P::TABP + P::LINV + W * P::WS);
-  // as many resident CTAs as shared memory allows (up to 3): registers are capped accordingly
-  constexpr size_t smem_c = sizeof(T) * (P::TABP + P::LINV + W * P::WS) + 1024;
-  constexpr int MINB = smem_c * 3 <= 233472 ? 3 : (smem_c * 2 <= 233472 ? 2 : 1);
-  auto kern = patch_smooth_kernel<T, K, W, MINB, GS>;
-  static bool attr = false;
-  if (!attr) {
-    SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = true;
-  }
-  kern<<<(npatch + W - 1) / W, GS * W, smem, ctx.stream>>>(
-      sblocks(lay, static_cast<T*>(x)), sblocks(lay, static_cast<const T*>(r)), static_cast<const T*>(dl.patch),
-      dl.lay.m, colour, vz_first, cnt_z, ctx.cfg.cg_max_iter, static_cast<T>(ctx.cfg.cg_tol), ctx.cfg.cg_fixed,
-      ctx.cfg.cg_precond);
-  SMG_CUDA(cudaGetLastError());
-  ++ctx.launches;
-}
-
-// patches of one colour with vertex z planes in [vz0, vz1] (clipped to 1..m-1), on vectors holding the
-// cells [zlo, zhi) of the level
-template <typename T, int K>
-void launch_k(Context& ctx, int level, int colour, void* x, const void* r, int zlo, int zhi, int vz0, int vz1) {
-  const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
-  const int m = dl.lay.m;
-  const LevelLayout lay(K, level, zlo, zhi);
-  auto cnt = [&](int bit) { return bit ? m / 2 : m / 2 - 1; };
-  const int zbit = (colour >> 2) & 1;
-  int vf = std::max(vz0, 1);
-  if ((vf & 1) != zbit) ++vf;  // odd planes for bit 1, even for bit 0
-  const int vl = std::min(vz1, m - 1);
-  const int cnt_z = vl >= vf ? (vl - vf) / 2 + 1 : 0;
-  if (cnt_z > 0 && (vf - 1 < zlo || vl + 1 > zhi))
-    throw std::invalid_argument("smooth: patches need the cells on both sides of their vertex plane");
-  const int npatch = cnt(colour & 1) * cnt((colour >> 1) & 1) * cnt_z;
-  if (npatch <= 0) return;
-  // few patches (coarse levels): a 4- or 8-warp CTA per patch cuts the per-patch latency; many
-  // patches: one warp per patch, several per CTA
-  if (npatch <= 148) launch_group<T, K, 1, 256>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
-  else if (npatch < 148 * 8) launch_group<T, K, 1, 128>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
-  else launch_group<T, K, warps_per_cta<T, K>(), 32>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
-}
-
-template <typename T>
-void launch_prec(Context& ctx, int level, int colour, void* x, const void* r, int zlo, int zhi, int vz0, int vz1) {
+void dispatch(Context& ctx, int level, int prec, int colour, void* x, const void* r, int zlo, int zhi, int vz0, int vz1) {
   switch (ctx.cfg.degree) {
-    case 1: launch_k<T, 1>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1); break;
-    case 2: launch_k<T, 2>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1); break;
-    case 3: launch_k<T, 3>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1); break;
-    case 4: launch_k<T, 4>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1); break;
+    case 1: smooth_launch_k<1>(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1); break;
+    case 2: smooth_launch_k<2>(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1); break;
+    case 3: smooth_launch_k<3>(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1); break;
+    case 4: smooth_launch_k<4>(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1); break;
     default: throw std::invalid_argument("degree not supported by the patch smoother kernel (1..4)");
   }
 }
@@ -485,14 +26,12 @@ void launch_prec(Context& ctx, int level, int colour, void* x, const void* r, in
 
 void launch_smooth_colour(Context& ctx, int level, int prec, int colour, void* x, const void* r) {
   const int m = ctx.dev[0][level].lay.m;
-  if (prec == SMG_F64) launch_prec<double>(ctx, level, colour, x, r, 0, m, 1, m - 1);
-  else launch_prec<float>(ctx, level, colour, x, r, 0, m, 1, m - 1);
+  dispatch(ctx, level, prec, colour, x, r, 0, m, 1, m - 1);
 }
 
 void launch_smooth_colour_held(Context& ctx, int level, int prec, int colour, void* x, const void* r, int zlo,
                                int zhi, int vz0, int vz1) {
-  if (prec == SMG_F64) launch_prec<double>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1);
-  else launch_prec<float>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1);
+  dispatch(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1);
 }
 
 // packed patch table (order of PD<K> offsets): every matrix as padded rows of M and of M^T
