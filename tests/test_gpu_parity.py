@@ -269,3 +269,37 @@ def test_slab_multigrid_matches_single_gpu(k, level, nparts):
         mg.slabs[p][level].add_owned_into(got, xs[p])
     res = float((rhs - ctx.apply_stokes(level, got)).norm() / rhs.norm())
     assert res <= 2e-8
+
+
+def test_cp_async_staging_path_matches_oracle():
+    # the cp.async (LDGSTS) staging fallback (SMG_NO_TMA, read once per process) against the oracle,
+    # whole-level and slab operator, in a fresh interpreter
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle
+import paper_2410_09497_b200 as smg
+from paper_2410_09497_b200 import slab
+worst = 0.0
+for k, level in ((1, 3), (2, 3), (3, 2)):
+    ctx = smg.Context(k, level)
+    x = np.random.default_rng(3).uniform(-1, 1, oracle.sizes(k, level)[4])
+    ref = oracle.apply_stokes(k, level, x)
+    xd = torch.from_numpy(x).cuda()
+    y = ctx.apply_stokes(level, xd).cpu().numpy()
+    worst = max(worst, np.abs(y - ref).max() / np.abs(ref).max())
+    got = torch.zeros_like(xd)
+    for z0, z1 in slab.partition(level, 2):
+        op = slab.SlabOperator(ctx, level, z0, z1)
+        yv = op.new_vector()
+        op.vmult(yv, op.lay.extract(xd), exchange=False)
+        op.lay.insert_owned(got, yv)
+    worst = max(worst, np.abs(got.cpu().numpy() - ref).max() / np.abs(ref).max())
+print(worst)
+'''
+    env = dict(os.environ, SMG_NO_TMA="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root, timeout=600)
+    assert out.returncode == 0, out.stderr
+    assert float(out.stdout.strip().splitlines()[-1]) <= 1e-12
