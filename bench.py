@@ -157,7 +157,7 @@ def run_reference(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"C2 sample: RT_{k} {2 << sample_level}^3 cells (1/8 of the 64^3 workload)",
                    "degree": k, "level": sample_level, "dofs": n},
         "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": os.cpu_count(), "kind": "port", "sample": sample},

@@ -1066,7 +1066,10 @@ void launch_shape(Context& ctx, int level, const VmultArgs& a) {
 template <int X_, int Y_, int Z_, int NT_, int OCC_>
 struct Shape { static constexpr int X = X_, Y = Y_, Z = Z_, NT = NT_, OCC = OCC_; };
 template <int K>
-struct Variants;
+struct Variants {  // degrees without alternative shapes
+  template <typename T>
+  static bool run(int, Context&, int, const VmultArgs&) { return false; }
+};
 template <>
 struct Variants<1> {
   template <typename T>
@@ -1085,11 +1088,11 @@ struct Variants<2> {
   template <typename T>
   static bool run(int v, Context& ctx, int level, const VmultArgs& a) {
     switch (v) {
-      case 1: launch_shape<T, 2, Shape<4, 4, 2, 192, 2>>(ctx, level, a); return true;
-      case 2: launch_shape<T, 2, Shape<4, 4, 2, 160, 2>>(ctx, level, a); return true;
-      case 3: launch_shape<T, 2, Shape<4, 4, 2, 224, 2>>(ctx, level, a); return true;
+      case 1: launch_shape<T, 2, Shape<4, 2, 2, 192, 3>>(ctx, level, a); return true;
+      case 2: launch_shape<T, 2, Shape<4, 2, 2, 256, 3>>(ctx, level, a); return true;
+      case 3: launch_shape<T, 2, Shape<4, 4, 1, 192, 3>>(ctx, level, a); return true;
       case 4: launch_shape<T, 2, Shape<4, 4, 4, 512, 1>>(ctx, level, a); return true;
-      case 5: launch_shape<T, 2, Shape<4, 4, 4, 384, 1>>(ctx, level, a); return true;
+      case 5: launch_shape<T, 2, Shape<8, 2, 1, 192, 3>>(ctx, level, a); return true;
       default: return false;
     }
   }
