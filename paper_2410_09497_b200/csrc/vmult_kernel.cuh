@@ -439,6 +439,17 @@ constexpr bool kStageUx = SMG_STAGE_UX;
 // cells per work item along a brick axis of nc cells: segments of 2 cells for low degrees (shared
 // neighbour loads, fewer index computations), single cells otherwise
 constexpr int seg_cells(int nc, int k) { return (nc % 2 == 0 && k <= 3) ? 2 : 1; }
+// row groups of the pass-3 items: the smallest divisor d of H with items * d >= threads, for k >= 7
+// (few, heavy items); 1 otherwise
+constexpr int pass3_groups(int items, int nt, int h, int k) {
+  if (k < 7) return 1;  // measured: helps k = 7 (33.3 -> 30.9 ms at level 5), hurts k = 4..6
+  for (int d = 1; d <= h && d <= 8; ++d)
+    if (h % d == 0 && items * d >= nt) return d;
+  int best = 1;
+  for (int d = 1; d <= h && d <= 8; ++d)
+    if (h % d == 0) best = d;
+  return best;
+}
 
 // ---------------------------------------------------------------------------------------------
 // one velocity component (U already staged in sU); if C == 2 and Gn != nullptr, the next brick's
@@ -622,8 +633,14 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
                   YSO2 = BR::stride(O2, BR::YX, BR::N(1));
     constexpr int NL = No1 * No2;
     constexpr int W = (S3 + 1) * H;  // window length of q; s and t have one more node
-    for (int it = tid; it < NL * (NCc / S3); it += NT) {
-      const int e0 = (it / NL) * S3, r = it % NL;
+    // high degrees: few (cell, line) items and many rows per item -> the H rows of an item are split
+    // into RG compile-time row groups (group slowest, so stores stay coalesced)
+    constexpr int ITEMS = NL * (NCc / S3);
+    constexpr int RG = pass3_groups(ITEMS, NT, H, K);
+    constexpr int RPG = H / RG;
+    for (int it = tid; it < ITEMS * RG; it += NT) {
+      const int grp = it / ITEMS, it0 = it - grp * ITEMS;
+      const int e0 = (it0 / NL) * S3, r = it0 % NL;
       const int oi = r % No1, oj = r / No1;
       const int base = (oj * No1 + oi) * PC + e0 * H;
       T s[W + 1], t[W + 1], q[W];
@@ -639,76 +656,98 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       g[O2] = G.g0[O2] + oj;
       const bool inside = g[O1] < G.nlim[O1] && g[O2] < G.nlim[O2];
       T* yp = sYP + oi * YSO1 + oj * YSO2;
-      // residual: the b values of this item's rows are loaded up front so their HBM latency overlaps
-      // the contractions (loads inside the store path were exposed: residual 1.8x the plain apply)
       constexpr bool DIRECT = !(C == 0 && kStageUx);
       // global index of the item's first row (node G.g0[C] + e0 H along c); rows step by st[C]
       const int gc0 = G.g0[C] + e0 * H;
       const int64_t gbase = g[O1] * st[O1] + g[O2] * st[O2] + gc0 * st[C];
       const int64_t pbase = C == 2 ? (static_cast<int64_t>(gc0) * n + g[1]) * n + g[0] : 0;  // pressure, C = 2
       const int64_t pplane = static_cast<int64_t>(n) * n;
-      T bvel[S3 * H], bpre[S3 * H];
-      if constexpr (RESID) {
+      auto rows = [&](auto gtag) {
+        constexpr int A0 = decltype(gtag)::value * RPG, A1 = A0 + RPG;  // rows [A0, A1) of each cell
+        // residual: the b values of this group's rows are loaded up front so their HBM latency overlaps
+        // the contractions (loads inside the store path were exposed: residual 1.8x the plain apply)
+        T bvel[S3 * RPG], bpre[S3 * RPG];
+        if constexpr (RESID) {
 #pragma unroll
-        for (int j = 0; j < S3 * H; ++j) {
-          bvel[j] = T(0);
-          bpre[j] = T(0);
-          const bool ok = inside && gc0 + j < G.nlim[C];
-          if (DIRECT && ok) bvel[j] = bc[gbase + j * st[C]];
-          if (C == 2 && ok) bpre[j] = B.c[3][pbase + j * pplane];
+          for (int ee = 0; ee < S3; ++ee)
+#pragma unroll
+            for (int j = 0; j < RPG; ++j) {
+              const int row = ee * H + A0 + j;
+              bvel[ee * RPG + j] = T(0);
+              bpre[ee * RPG + j] = T(0);
+              const bool ok = inside && gc0 + row < G.nlim[C];
+              if (DIRECT && ok) bvel[ee * RPG + j] = bc[gbase + row * st[C]];
+              if (C == 2 && ok) bpre[ee * RPG + j] = B.c[3][pbase + row * pplane];
+            }
         }
-      }
 #pragma unroll
-      for (int ee = 0; ee < S3; ++ee) {
-        const int e = e0 + ee;
+        for (int ee = 0; ee < S3; ++ee) {
+          const int e = e0 + ee;
 #pragma unroll
-        for (int a = 0; a < H; ++a) {
-          T v = T(0), w = T(0);
+          for (int a = A0; a < A1; ++a) {
+            T v = T(0), w = T(0);
 #pragma unroll
-          for (int bq = 0; bq < P; ++bq) {
-            v += cref<T>(R::LP + a * P + bq) * s[ee * H + H + bq] + cref<T>(R::MP + a * P + bq) * t[ee * H + H + bq];
-            if (a == 0)
-              v += cref<T>(R::LP + (K + 1) * P + bq) * s[ee * H + bq] + cref<T>(R::MP + (K + 1) * P + bq) * t[ee * H + bq];
+            for (int bq = 0; bq < P; ++bq) {
+              v += cref<T>(R::LP + a * P + bq) * s[ee * H + H + bq] + cref<T>(R::MP + a * P + bq) * t[ee * H + H + bq];
+              if (a == 0)
+                v += cref<T>(R::LP + (K + 1) * P + bq) * s[ee * H + bq] +
+                     cref<T>(R::MP + (K + 1) * P + bq) * t[ee * H + bq];
+            }
+#pragma unroll
+            for (int i = 0; i < H; ++i) {
+              w += cref<T>(R::D + i * P + a) * q[ee * H + H + i];
+              if (a == 0) w += cref<T>(R::D + i * P + H) * q[ee * H + i];
+            }
+            const T val = h * v + h2 * w;
+            if (C == 0 && kStageUx) {
+              sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
+            } else {
+              const int gc = gc0 + ee * H + a;
+              if (inside && gc < G.nlim[C]) {
+                T rr = val;
+                if (gc == 0) rr = T(0);  // constrained boundary-normal row
+                else if (RESID) rr = bvel[ee * RPG + a - A0] - rr;
+                yc[gbase + (ee * H + a) * st[C]] = rr;
+              }
+            }
           }
+          // pressure rows of cell e: y_p += h^2 D S
 #pragma unroll
-          for (int i = 0; i < H; ++i) {
-            w += cref<T>(R::D + i * P + a) * q[ee * H + H + i];
-            if (a == 0) w += cref<T>(R::D + i * P + H) * q[ee * H + i];
-          }
-          const T val = h * v + h2 * w;
-          if (C == 0 && kStageUx) {
-            sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
-          } else {
-            const int gc = gc0 + ee * H + a;
-            if (inside && gc < G.nlim[C]) {
-              T rr = val;
-              if (gc == 0) rr = T(0);  // constrained boundary-normal row
-              else if (RESID) rr = bvel[ee * H + a] - rr;
-              yc[gbase + (ee * H + a) * st[C]] = rr;
+          for (int i = A0; i < A1; ++i) {
+            T z = T(0);
+#pragma unroll
+            for (int bq = 0; bq < P; ++bq) z += cref<T>(R::D + i * P + bq) * s[ee * H + H + bq];
+            // y_p = h^2 (D_x S_x + D_y S_y + D_z S_z): component 0 stores, 1 accumulates, 2 writes HBM
+            if (C == 0) {
+              yp[(e * H + i) * YSC] = h2 * z;
+            } else if (C == 1) {
+              yp[(e * H + i) * YSC] += h2 * z;
+            } else {
+              if (inside && gc0 + ee * H + i < G.nlim[2]) {
+                const T vp = yp[(e * H + i) * YSC] + h2 * z;
+                Y.c[3][pbase + (ee * H + i) * pplane] = RESID ? bpre[ee * RPG + i - A0] - vp : vp;
+              }
             }
           }
         }
-        // pressure rows of cell e: y_p += h^2 D S
-#pragma unroll
-        for (int i = 0; i < H; ++i) {
-          T z = T(0);
-#pragma unroll
-          for (int bq = 0; bq < P; ++bq) z += cref<T>(R::D + i * P + bq) * s[ee * H + H + bq];
-          // y_p = h^2 (D_x S_x + D_y S_y + D_z S_z): component 0 stores, 1 accumulates, 2 writes HBM
-          if (C == 0) {
-            yp[(e * H + i) * YSC] = h2 * z;
-          } else if (C == 1) {
-            yp[(e * H + i) * YSC] += h2 * z;
-          } else {
-            if (inside && gc0 + ee * H + i < G.nlim[2]) {
-              const T vp = yp[(e * H + i) * YSC] + h2 * z;
-              Y.c[3][pbase + (ee * H + i) * pplane] = RESID ? bpre[ee * H + i] - vp : vp;
-            }
-          }
+      };
+      if constexpr (RG == 1) {
+        rows(std::integral_constant<int, 0>());
+      } else {
+        switch (grp) {
+          case 0: rows(std::integral_constant<int, 0>()); break;
+          case 1: rows(std::integral_constant<int, (RG > 1 ? 1 : 0)>()); break;
+          case 2: if constexpr (RG > 2) rows(std::integral_constant<int, (RG > 2 ? 2 : 0)>()); break;
+          case 3: if constexpr (RG > 3) rows(std::integral_constant<int, (RG > 3 ? 3 : 0)>()); break;
+          case 4: if constexpr (RG > 4) rows(std::integral_constant<int, (RG > 4 ? 4 : 0)>()); break;
+          case 5: if constexpr (RG > 5) rows(std::integral_constant<int, (RG > 5 ? 5 : 0)>()); break;
+          case 6: if constexpr (RG > 6) rows(std::integral_constant<int, (RG > 6 ? 6 : 0)>()); break;
+          default: if constexpr (RG > 7) rows(std::integral_constant<int, (RG > 7 ? 7 : 0)>()); break;
         }
       }
       // the constrained plane g_c = n belongs to the brick holding the last cell along c
-      if ((C != 0 || !kStageUx) && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
+      if (grp == 0 && (C != 0 || !kStageUx) && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] &&
+          G.mlim[C] == m) {
         g[C] = n;
         yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
       }
