@@ -1,4 +1,5 @@
 #!/bin/bash
+# brick-shape variants (build with `make -C paper_2410_09497_b200 TUNE=1` first): KS="2 3" bash tools/tune4.sh
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 : > gpurun_out/tune4.txt
