@@ -25,6 +25,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 DEGREE, LEVEL = 2, 5
+FP64_PEAK_TFLOPS = 33.3  # tools/fma_peak.cu on this pool's B200 (profiles/r01/fma_peaks.txt)
 METRIC = "Stokes operator-apply DoF/s (fp64), RT_2 64^3 cells; + fp32 smoother DoF/s and MG-FGMRES solve time"
 
 
@@ -374,6 +375,13 @@ def main():
                      "kernel": f"stokes_vmult_kernel<double,{k}> ({SHAPES.get(k, 'see DESIGN.md')})"},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
     }
+    # compute side of the roofline: algorithmic flops of the Kronecker-form operator (SURVEY.md §8(d):
+    # 19.5 k + 33 per DoF) against the FP64 FMA peak measured with tools/fma_peak.cu
+    flops = (19.5 * k + 33) * owned
+    tflops = flops / (ms_kernel * 1e-3) / 1e12
+    out["roofline"]["compute"] = {"algorithmic_flops_per_launch": flops, "achieved_tflops": tflops,
+                                  "fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac": tflops / FP64_PEAK_TFLOPS,
+                                  "peak_source": "measured, profiles/r01/fma_peaks.txt (tools/fma_peak.cu)"}
     out.update(extra)
     print(json.dumps(out))
     if dist:
