@@ -197,6 +197,23 @@ struct Patch {
     warp_axis<T, A0, A1, NO, 2, A2, GS>(tmp, G(C, 2, true), out, lane);
     gsync<GS>();
   }
+  // the first contraction of gt3 (axis 0), shared by components 1 and 2 (both orthogonal to x: same
+  // matrix G_orth(var0)^T): out = (G0^T (x) I (x) I) in
+  __device__ void gt3_axis0_orth(const T* in, T* out) const {
+    constexpr int NO = P::NO;
+    warp_axis<T, NO, NO, NO, 0, NO, GS>(in, G(1, 0, true), out, lane);
+    gsync<GS>();
+  }
+  // the last two contractions of gt3 from the axis-0 result x0: out = (I (x) G1^T (x) G2^T) x0
+  template <int C>
+  __device__ void gt3_from_axis0(const T* x0, T* out, T* tmp) const {
+    constexpr int NO = P::NO;
+    constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
+    warp_axis<T, A0, NO, NO, 1, A1, GS>(x0, G(C, 1, true), tmp, lane);
+    gsync<GS>();
+    warp_axis<T, A0, A1, NO, 2, A2, GS>(tmp, G(C, 2, true), out, lane);
+    gsync<GS>();
+  }
   // eigen space of component C -> pressure: out = (G0 (x) G1 (x) G2) in
   // acc (=|+=) (G0 (x) G1 (x) G2) in; s1, s2 scratch
   template <int C, bool ACC>
@@ -375,11 +392,18 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
     }
     // Pq = S Pd = sum_c G_c Lambda_c^-1 G_c^T Pd
 
-    SMG_FOR_C({
-      ps.template gt3<C>(Pd, T1, T2);
-      ps.template lam_inv<C>(T1);
-      ps.template g3acc<C, C != 0>(T1, Pq, T2, Pz);  // Pz is free scratch here (recomputed below)
-    })
+    // component 0, then 1 and 2 sharing their first contraction (x0 kept in Pz, which is free here:
+    // it is recomputed by the preconditioner below)
+    ps.template gt3<0>(Pd, T1, T2);
+    ps.template lam_inv<0>(T1);
+    ps.template g3acc<0, false>(T1, Pq, T2, T1);
+    ps.gt3_axis0_orth(Pd, Pz);
+    ps.template gt3_from_axis0<1>(Pz, T1, T2);
+    ps.template lam_inv<1>(T1);
+    ps.template g3acc<1, true>(T1, Pq, T2, T1);
+    ps.template gt3_from_axis0<2>(Pz, T1, T2);
+    ps.template lam_inv<2>(T1);
+    ps.template g3acc<2, true>(T1, Pq, T2, T1);
     const T dq = ps.dot(Pd, Pq);
     if (!(dq > T(0)) || rz == T(0)) break;
     const T alpha = rz / dq;
