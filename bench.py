@@ -303,6 +303,17 @@ def main():
         op = slab.SlabOperator(ctx, level, z0, z1, rank, world)
         L = op.lay
         xsl = L.extract(x).contiguous()
+        # correctness of the partitioned operator (exchange overlapped with the interior rows) against
+        # the whole-level operator on this rank's owned rows
+        yref = L.extract(ctx.apply_stokes(level, x))
+        ychk = op.vmult(op.new_vector(), xsl.clone())
+        err = 0.0
+        for c in range(4):
+            a_, b_ = L.owned_planes(c)
+            d = (L.block(ychk, c)[a_:b_] - L.block(yref, c)[a_:b_]).abs().max()
+            err = max(err, float(d) / max(float(yref.abs().max()), 1e-300))
+        extra["slab_check_rel_err"] = max_over_ranks(err)
+        del yref, ychk
         if not args.no_solve:
             # distributed MG-FGMRES: same global right-hand side, z-slab multigrid (slab_mg)
             from paper_2410_09497_b200 import slab_mg

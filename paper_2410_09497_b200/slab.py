@@ -127,6 +127,21 @@ class HaloExchange:
                 w.wait()
         return v
 
+    def start(self, v):
+        """post the exchange and return its work handles (NCCL runs it on its own stream); None when the
+        backend cannot overlap (gloo: done synchronously here)."""
+        import torch.distributed as dist
+        if dist.get_backend(self.group) == "gloo":
+            self.exchange(v)
+            return None
+        ops = self._ops(v)
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    @staticmethod
+    def finish(works):
+        for w in works or []:
+            w.wait()  # the current stream waits for the exchange
+
 
 def exchange_local(layouts, vecs):
     """single-process ghost exchange between slab vectors of one device (tests, virtual slabs)."""
@@ -169,12 +184,31 @@ class SlabOperator:
             self.halo.exchange(x)
         return x
 
-    def vmult(self, y, x, exchange=True):
-        if exchange:
-            self.exchange(x)
+    def _rows(self, y, x, c0, c1, b=None):
+        L = self.lay
+        if c0 >= c1:
+            return
+        self.ctx._check(lib().smg_residual_held(self.ctx._h, self.level, self.ctx._prec(x), _ptr(y),
+                                                None if b is None else _ptr(b), _ptr(x), L.zlo, L.zhi, c0, c1))
+
+    def vmult(self, y, x, exchange=True, overlap=True):
+        """y = A x on the owned rows. With an exchange, the rows that do not touch a ghost cell are
+        computed while NCCL moves the ghost layers (interior first, then the two boundary cell layers)."""
         p = self.ctx._prec(x)
         self.ctx._sync_stream()
-        self.ctx._check(lib().smg_vmult_slab(self.ctx._h, self.level, p, _ptr(y), _ptr(x), self.lay.z0, self.lay.z1))
+        L = self.lay
+        if not exchange or self.halo is None or not overlap or L.z1 - L.z0 < 3:
+            if exchange:
+                self.exchange(x)
+            self.ctx._check(lib().smg_vmult_slab(self.ctx._h, self.level, p, _ptr(y), _ptr(x), L.z0, L.z1))
+            return y
+        works = self.halo.start(x)
+        lo = L.z0 + (1 if L.zlo < L.z0 else 0)   # first cell whose rows need no ghost below
+        hi = L.z1 - (1 if L.zhi > L.z1 else 0)   # one past the last cell needing no ghost above
+        self._rows(y, x, lo, hi)
+        self.halo.finish(works)
+        self._rows(y, x, L.z0, lo)
+        self._rows(y, x, hi, L.z1)
         return y
 
     def residual(self, r, b, x, exchange=True):
