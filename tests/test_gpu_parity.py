@@ -154,6 +154,47 @@ def test_vec_upload_download_roundtrip():
         assert np.array_equal(a, b)
 
 
+def _zero_constrained_(v, k, level):
+    """zero the constrained boundary-normal planes of a device level vector in place."""
+    n = (2 << level) * (k + 1)
+    off = 0
+    for c in range(3):
+        d = [n, n, n]
+        d[c] = n + 1
+        blk = v[off:off + d[0] * d[1] * d[2]].view(d[2], d[1], d[0])
+        idx = [slice(None)] * 3
+        for pl in (0, n):
+            idx[2 - c] = pl
+            blk[tuple(idx)] = 0
+        off += d[0] * d[1] * d[2]
+
+
+@pytest.mark.parametrize("k,level", [(3, 6), (1, 6)])
+def test_c3_size_properties(k, level):
+    # C3 (k=3, 128^3, 538 M DoF): symmetry <Ax, y> = <x, Ay>, linearity and zero constrained rows at
+    # full size, where the oracle is too slow (SURVEY.md §8(c) size-independent properties)
+    ctx = smg.Context(k, level)
+    n_ = ctx.sizes(level)[4]
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.rand(n_, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    y = torch.rand(n_, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    _zero_constrained_(x, k, level)
+    _zero_constrained_(y, k, level)
+    Ax = ctx.apply_stokes(level, x)
+    a = float(torch.dot(Ax, y))
+    Ay = ctx.apply_stokes(level, y)
+    b = float(torch.dot(x, Ay))
+    assert abs(a - b) <= 1e-10 * max(abs(a), 1.0)
+    del Ay
+    A2 = ctx.apply_stokes(level, 0.5 * x + y)
+    A2 -= 0.5 * Ax
+    A2 -= ctx.apply_stokes(level, y)
+    assert float(A2.abs().max()) <= 1e-11 * float(Ax.abs().max())
+    mask = torch.ones_like(x)
+    _zero_constrained_(mask, k, level)
+    assert bool((Ax[mask == 0] == 0).all())  # constrained boundary-normal rows are zero
+
+
 def test_large_level_properties_symmetry_linearity():
     # full-size properties where the oracle is too slow: <A x, y> = <x, A y>, A(ax + y) = aAx + Ay
     k, level = 2, 5
