@@ -434,12 +434,25 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
   for (int o = lane; o < P::NPR; o += GS) x.c[3][pres_index(o)] += Px[o];
 }
 
+// CTAs per SM that shared memory allows for W warp-patches per CTA (1 KB reserved per CTA)
+template <typename T, int K>
+constexpr int ctas_per_sm(int w) {
+  const int bytes = static_cast<int>(sizeof(T)) * (PD<K>::TABP + PD<K>::LINV + w * PD<K>::WS) + 1024;
+  const int c = 233472 / bytes;
+  return c > 3 ? 3 : c;  // at most 3 CTAs (the register budget caps resident warps near 24)
+}
+// warp-patches per CTA maximising the patches resident per SM (ties: fewer per CTA)
 template <typename T, int K>
 constexpr int warps_per_cta() {
-  // keep a CTA at <= ~100 KB so that two fit on an SM
-  constexpr int ws = PD<K>::WS * static_cast<int>(sizeof(T));
-  constexpr int w = 100 * 1024 / ws;
-  return w >= 8 ? 8 : (w >= 4 ? 4 : (w >= 2 ? 2 : 1));
+  int best = 1, best_p = 0;
+  for (int w = 1; w <= 8; ++w) {
+    const int p = w * ctas_per_sm<T, K>(w);
+    if (p > best_p) {
+      best = w;
+      best_p = p;
+    }
+  }
+  return best;
 }
 
 template <typename T>
@@ -458,6 +471,7 @@ void launch_group(Context& ctx, const DevLevel& dl, const LevelLayout& lay, int 
   // as many resident CTAs as shared memory allows (up to 3): registers are capped accordingly
   constexpr size_t smem_c = sizeof(T) * (P::TABP + P::LINV + W * P::WS) + 1024;
   constexpr int MINB = smem_c * 3 <= 233472 ? 3 : (smem_c * 2 <= 233472 ? 2 : 1);
+  static_assert(smem_c <= 233472, "patch workspace exceeds shared memory");
   auto kern = patch_smooth_kernel<T, K, W, MINB, GS>;
   static bool attr = false;
   if (!attr) {
