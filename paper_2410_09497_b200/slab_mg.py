@@ -111,6 +111,15 @@ class SlabMG:
     # ---- communication ----
     def exchange(self, l, vs):
         """refresh GHOST cell layers of the part vectors vs[p] from the neighbours' owned cells."""
+        self.exchange_finish(self.exchange_start(l, vs))
+
+    @staticmethod
+    def exchange_finish(works):
+        for w in works or []:
+            w.wait()  # the current stream waits for the NCCL transfers
+
+    def exchange_start(self, l, vs):
+        """post the ghost exchange; returns NCCL work handles to finish later (None: already done)."""
         if self.virtual:
             for p in self.parts:
                 S = self.slabs[p][l]
@@ -125,7 +134,7 @@ class SlabMG:
                         sa, sb = S.cells(a, b)
                         ta, tb = T.cells(a, b)
                         S.block(vs[p], c)[sa:sb] = T.block(vs[q], c)[ta:tb]
-            return
+            return None
         import torch.distributed as dist
         if dist.get_backend(self.group) == "gloo" and any(v.is_cuda for v in vs.values()):
             # gloo has no CUDA P2P: stage through host memory (logic checks on single-GPU boxes)
@@ -133,7 +142,7 @@ class SlabMG:
             self.exchange(l, hs)
             for p in vs:
                 vs[p].copy_(hs[p])
-            return
+            return None
         ops = []
         for p in self.parts:
             S = self.slabs[p][l]
@@ -152,9 +161,7 @@ class SlabMG:
                     if ra < rb:
                         a, b = S.cells(ra, rb)
                         ops.append(dist.P2POp(dist.irecv, S.block(v, c)[a:b], q, self.group))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
 
     def allreduce_full(self, l, contrib):
         """sum over ranks of full-level vectors (agglomeration)."""
@@ -188,12 +195,21 @@ class SlabMG:
         return tot
 
     # ---- operators ----
-    def residual(self, l, r, b, x, c0, c1):
+    def residual(self, l, r, b, x, c0, c1, skip=None):
+        """r = b - A x on the rows of cells [z0 + c0, z1 + c1) (clipped to the level); skip = (s0, s1)
+        leaves out the rows [z0 + s0, z1 + s1) (computed earlier)."""
         for p in self.parts:
             S = self.slabs[p][l]
             a0, a1 = max(S.z0 + c0, 0), min(S.z1 + c1, S.m)
-            self.ctx._check(lib().smg_residual_held(self.ctx._h, l, self.ctx._prec(x[p]), _ptr(r[p]), _ptr(b[p]),
-                                                    _ptr(x[p]), S.zlo, S.zhi, a0, a1))
+            spans = [(a0, a1)]
+            if skip is not None:
+                s0, s1 = max(S.z0 + skip[0], a0), min(S.z1 + skip[1], a1)
+                if s0 < s1:
+                    spans = [(a0, s0), (s1, a1)]
+            for u0, u1 in spans:
+                if u0 < u1:
+                    self.ctx._check(lib().smg_residual_held(self.ctx._h, l, self.ctx._prec(x[p]), _ptr(r[p]),
+                                                            _ptr(b[p]), _ptr(x[p]), S.zlo, S.zhi, u0, u1))
 
     def vmult(self, l, y, x):
         """y = A x on the owned rows (x ghosts must be current)."""
@@ -204,8 +220,11 @@ class SlabMG:
 
     def smooth(self, l, x, b, r):
         for col in range(8):
-            self.exchange(l, x)
-            self.residual(l, r, b, x, -2, 1)
+            # the residual rows that need no ghost cell are computed while the exchange runs
+            works = self.exchange_start(l, x)
+            self.residual(l, r, b, x, 1, -1)
+            self.exchange_finish(works)
+            self.residual(l, r, b, x, -2, 1, skip=(1, -1))
             for p in self.parts:
                 S = self.slabs[p][l]
                 self.ctx._check(lib().smg_smooth_colour_held(self.ctx._h, l, self.ctx._prec(x[p]), col, _ptr(x[p]),
