@@ -9,6 +9,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
 #include "smg_internal.cuh"
@@ -326,7 +327,9 @@ void vmult_host_pipelined(Context& c, int level, int prec, void* const y_vel[3],
   }
   // chunks of 4k cells (every brick depth divides 4), at most 16
   const int m = lay.m;
-  int chunk = std::max(4, (m / 16) / 4 * 4);
+  int nch_target = 16;
+  if (const char* e = std::getenv("SMG_HOST_CHUNKS")) nch_target = std::max(1, std::atoi(e));
+  int chunk = std::max(4, (m / nch_target) / 4 * 4);
   if (m < 8) chunk = m;
   const int nchunk = (m + chunk - 1) / chunk;
   std::vector<cudaEvent_t> ev_in(nchunk), ev_comp(nchunk);
@@ -364,17 +367,23 @@ void vmult_host_pipelined(Context& c, int level, int prec, void* const y_vel[3],
       char* dst = (blk < 3 ? dx + lay.off[blk] * es : pin) + off * es;
       SMG_CUDA(cudaMemcpyAsync(dst, src, len * es, cudaMemcpyHostToDevice, c.s_in));
     }
-    launch_pressure_permute(c, level, prec, dx + lay.off[3] * es, pin, false, z0, z1, c.s_in);
     SMG_CUDA(cudaEventRecord(ev_in[k], c.s_in));
   }
-  for (int k = 0; k < nchunk; ++k) {
+  // the copy streams carry copies only (a kernel between two copies of one stream leaves the copy
+  // engine idle); the pressure permutations run on the compute stream, one chunk ahead of the vmult
+  auto permute_in = [&](int k) {
     const int z0 = k * chunk, z1 = std::min(m, z0 + chunk);
     SMG_CUDA(cudaStreamWaitEvent(c.stream, ev_in[k], 0));
-    if (k + 1 < nchunk) SMG_CUDA(cudaStreamWaitEvent(c.stream, ev_in[k + 1], 0));
+    launch_pressure_permute(c, level, prec, dx + lay.off[3] * es, pin, false, z0, z1, c.stream);
+  };
+  permute_in(0);
+  for (int k = 0; k < nchunk; ++k) {
+    const int z0 = k * chunk, z1 = std::min(m, z0 + chunk);
+    if (k + 1 < nchunk) permute_in(k + 1);
     launch_vmult_zrange(c, level, prec, dy, dx, nullptr, z0, z1);
+    launch_pressure_permute(c, level, prec, pout, dy + lay.off[3] * es, true, z0, z1, c.stream);
     SMG_CUDA(cudaEventRecord(ev_comp[k], c.stream));
     SMG_CUDA(cudaStreamWaitEvent(c.s_out, ev_comp[k], 0));
-    launch_pressure_permute(c, level, prec, pout, dy + lay.off[3] * es, true, z0, z1, c.s_out);
     for (int blk = 0; blk < 4; ++blk) {
       int64_t off, len;
       span(blk, z0, z1, off, len);
