@@ -1132,6 +1132,10 @@ struct Variants<2> {
       case 3: launch_shape<T, 2, Shape<4, 4, 1, 192, 3>>(ctx, level, a); return true;
       case 4: launch_shape<T, 2, Shape<4, 4, 4, 512, 1>>(ctx, level, a); return true;
       case 5: launch_shape<T, 2, Shape<8, 2, 1, 192, 3>>(ctx, level, a); return true;
+      case 6: launch_shape<T, 2, Shape<4, 4, 2, 192, 2>>(ctx, level, a); return true;
+      case 7: launch_shape<T, 2, Shape<8, 4, 2, 384, 1>>(ctx, level, a); return true;
+      case 8: launch_shape<T, 2, Shape<4, 4, 4, 384, 1>>(ctx, level, a); return true;
+      case 9: launch_shape<T, 2, Shape<4, 4, 2, 320, 2>>(ctx, level, a); return true;
       default: return false;
     }
   }
