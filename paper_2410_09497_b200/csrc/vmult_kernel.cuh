@@ -548,7 +548,10 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         seg_sipg<T, K, S1, BND>(in, out, eg == 0 ? 0 : -1, (m - 1 - eg < S1) ? m - 1 - eg : -1);
 #pragma unroll
         for (int a = 0; a < S1 * H; ++a) sB1[((e2 * H + a) * No1 + o) * PC + ci] = out[a];
-        if (ci < Nc + H) {  // Q2 = M_o2 p at the same (c, o1, o2-segment); the P box has the same origin
+        // Q2 = M_o2 p at the same (c, o1, o2-segment); the P box has the same origin. C = 0 walks c
+        // fastest, so the last c column (never read as Q) is computed from the P box's pad column rather
+        // than branched around in every warp
+        if (C == 0 || ci < Nc + H) {
           const T* ps = sP + psh + ci * PSC + (o + H) * PSO1 + (e2 + 1) * H * PSO2;
           T pc[S1 * H], q2[S1 * H];
 #pragma unroll
@@ -605,7 +608,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
           sS[(oj * No1 + e1 * H + a) * PC + ci] = sv[a];
           sT[(oj * No1 + e1 * H + a) * PC + ci] = tv[a] + mb[a];
         }
-        if (ci < Nc + H) {  // Q = M_o1 Q2 in place
+        {  // Q = M_o1 Q2 in place (the last c column is never read as Q: no branch, see pass 1)
           T* q = sQ + (oj * No1 + e1 * H) * PC + ci;
           T q2[S2 * H], qq[S2 * H];
 #pragma unroll
