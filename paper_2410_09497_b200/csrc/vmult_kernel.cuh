@@ -641,6 +641,10 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
     constexpr int ITEMS = NL * (NCc / S3);
     constexpr int RG = pass3_groups(ITEMS, NT, H, K);
     constexpr int RPG = H / RG;
+    // FULL (CTA-uniform): every row of the brick is held, none is a constrained boundary row, and the
+    // brick is not the last along c -- the store predicates drop out of the interior bricks' code
+    auto pass3 = [&](auto fulltag) {
+    constexpr bool FULL = decltype(fulltag)::value;
     for (int it = tid; it < ITEMS * RG; it += NT) {
       const int grp = it / ITEMS, it0 = it - grp * ITEMS;
       const int e0 = (it0 / NL) * S3, r = it0 % NL;
@@ -678,7 +682,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
               const int row = ee * H + A0 + j;
               bvel[ee * RPG + j] = T(0);
               bpre[ee * RPG + j] = T(0);
-              const bool ok = inside && gc0 + row < G.nlim[C];
+              const bool ok = FULL || (inside && gc0 + row < G.nlim[C]);
               if (DIRECT && ok) bvel[ee * RPG + j] = bc[gbase + row * st[C]];
               if (C == 2 && ok) bpre[ee * RPG + j] = B.c[3][pbase + row * pplane];
             }
@@ -706,9 +710,9 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
               sYC[(oj * No1 + oi) * NCP + e * H + a] = val;
             } else {
               const int gc = gc0 + ee * H + a;
-              if (inside && gc < G.nlim[C]) {
+              if (FULL || (inside && gc < G.nlim[C])) {
                 T rr = val;
-                if (gc == 0) rr = T(0);  // constrained boundary-normal row
+                if (!FULL && gc == 0) rr = T(0);  // constrained boundary-normal row
                 else if (RESID) rr = bvel[ee * RPG + a - A0] - rr;
                 yc[gbase + (ee * H + a) * st[C]] = rr;
               }
@@ -726,7 +730,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
             } else if (C == 1) {
               yp[(e * H + i) * YSC] += h2 * z;
             } else {
-              if (inside && gc0 + ee * H + i < G.nlim[2]) {
+              if (FULL || (inside && gc0 + ee * H + i < G.nlim[2])) {
                 const T vp = yp[(e * H + i) * YSC] + h2 * z;
                 Y.c[3][pbase + (ee * H + i) * pplane] = RESID ? bpre[ee * RPG + i - A0] - vp : vp;
               }
@@ -749,12 +753,18 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         }
       }
       // the constrained plane g_c = n belongs to the brick holding the last cell along c
-      if (grp == 0 && (C != 0 || !kStageUx) && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] &&
+      if (!FULL && grp == 0 && (C != 0 || !kStageUx) && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] &&
           G.mlim[C] == m) {
         g[C] = n;
         yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
       }
     }
+    };
+    if (G.g0[O1] + No1 <= G.nlim[O1] && G.g0[O2] + No2 <= G.nlim[O2] && G.g0[C] > 0 && G.g0[C] + Nc <= G.nlim[C] &&
+        G.c0[C] + NCc < G.mlim[C])
+      pass3(bool_c<true>());
+    else
+      pass3(bool_c<false>());
     if (C == 0 && kStageUx) {
       __syncthreads();
       // coalesced write-out of the u_x rows (x = c fastest), plus the constrained plane x = n
