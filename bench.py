@@ -178,7 +178,9 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 300 on the GPU arm: a timed region of ~0.1 s, several clock samples; "
+                    "100 on the reference arm)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--degree", type=int, default=DEGREE)
@@ -188,6 +190,8 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only to test the multi-rank "
                     "logic on a single-GPU box (CPU-staged exchange, timings meaningless)")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 300 if args.impl == "b200" else 100
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)

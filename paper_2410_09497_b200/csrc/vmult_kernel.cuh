@@ -551,7 +551,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         // Q2 = M_o2 p at the same (c, o1, o2-segment); the P box has the same origin. C = 0 walks c
         // fastest, so the last c column (never read as Q) is computed from the P box's pad column rather
         // than branched around in every warp
-        if (C == 0 || ci < Nc + H) {
+        if ((C == 0 && K <= 5) || ci < Nc + H) {  // (k >= 6: the extra column costs more than the branch)
           const T* ps = sP + psh + ci * PSC + (o + H) * PSO1 + (e2 + 1) * H * PSO2;
           T pc[S1 * H], q2[S1 * H];
 #pragma unroll
@@ -608,7 +608,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
           sS[(oj * No1 + e1 * H + a) * PC + ci] = sv[a];
           sT[(oj * No1 + e1 * H + a) * PC + ci] = tv[a] + mb[a];
         }
-        {  // Q = M_o1 Q2 in place (the last c column is never read as Q: no branch, see pass 1)
+        if (K <= 5 || ci < Nc + H) {  // Q = M_o1 Q2 in place (last c column never read as Q, see pass 1)
           T* q = sQ + (oj * No1 + e1 * H) * PC + ci;
           T q2[S2 * H], qq[S2 * H];
 #pragma unroll
@@ -760,8 +760,10 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       }
     }
     };
-    if (G.g0[O1] + No1 <= G.nlim[O1] && G.g0[O2] + No2 <= G.nlim[O2] && G.g0[C] > 0 && G.g0[C] + Nc <= G.nlim[C] &&
-        G.c0[C] + NCc < G.mlim[C])
+    // (not for fp64 k = 7: the second copy of its long, row-grouped pass-3 body measured slower)
+    constexpr bool kFullSpec = K != 7 || sizeof(T) == 4;
+    if (kFullSpec && G.g0[O1] + No1 <= G.nlim[O1] && G.g0[O2] + No2 <= G.nlim[O2] && G.g0[C] > 0 &&
+        G.g0[C] + Nc <= G.nlim[C] && G.c0[C] + NCc < G.mlim[C])
       pass3(bool_c<true>());
     else
       pass3(bool_c<false>());
