@@ -131,7 +131,7 @@ def test_solve_iteration_counts(k, level):
         assert res <= 2e-8
 
 
-@pytest.mark.parametrize("k,level", [(1, 2), (2, 2), (3, 1)])
+@pytest.mark.parametrize("k,level", [(1, 2), (2, 2), (3, 1), (1, 4), (2, 3)])
 def test_vmult_host_blockvector_path(k, level):
     # reference-facing path: BlockVector blocks with the cell-local pressure numbering
     ctx = smg.Context(k, level)
