@@ -61,6 +61,10 @@ int64_t smg_launch_count(const smg_context* ctx);
 /* ---- level layout (DoFLayout; BlockVector sizes block_vector.hpp:21-24) ---- */
 /* sizes[0..2] velocity component blocks, sizes[3] pressure, sizes[4] total stored DoFs */
 int smg_level_sizes(int degree, int level, int64_t sizes[5]);
+/* w[a] = integral of the pressure nodal basis function a over the reference cell [0,1], a = 0..degree:
+ * the separable weights of the mass-weighted pressure mean (project_zero_mean SPEC.md:212-220), for
+ * callers that reduce the mean over a partitioned vector themselves */
+int smg_pressure_node_weights(int degree, double* w);
 
 /* ---- level vectors (device) ---- */
 int smg_vec_alloc(smg_context* ctx, int level, int precision, void** dptr);
@@ -106,7 +110,7 @@ int smg_residual_slab(smg_context* ctx, int level, int precision, void* r, const
  *        residual_held       r = b - A x on the rows of cells [c0, c1) (held must cover c0-1 .. c1)
  *        smooth_colour_held  the patches of one colour whose vertex z plane is in [vz0, vz1]
  *        prolongate_add_held fine rows of fine cells [f0, f1) += P x_c
- *        restrict_held       coarse rows of coarse cells [c0, c1) = P^T r_f (reads fine cells 2c0-2 .. 2c1)
+ *        restrict_held       coarse rows of coarse cells [c0, c1) = P^T r_f (reads fine cells 2c0-2 .. 2c1-1)
  *        dot_held            dot over the rows of cells [c0, c1) (fp64 accumulate; caller all-reduces) ---- */
 int smg_held_sizes(int degree, int level, int zlo, int zhi, int64_t sizes[5]);
 int smg_residual_held(smg_context* ctx, int level, int precision, void* r, const void* b, const void* x, int zlo,
@@ -128,6 +132,15 @@ int smg_dot_slab(smg_context* ctx, int level, int precision, const void* a, cons
 int smg_dot(smg_context* ctx, int level, int precision, const void* a, const void* b, double* out);
 int smg_axpy(smg_context* ctx, int level, int precision, double alpha, const void* x, void* y);
 int smg_convert(smg_context* ctx, int level, int dst_precision, void* dst, int src_precision, const void* src);
+/* x *= alpha (scale, block_vector.hpp:74-78) */
+int smg_scale(smg_context* ctx, int level, int precision, double alpha, void* x);
+/* y = b - y (subtract_from, block_vector.hpp:80-88: residuals computed in place) */
+int smg_subtract_from(smg_context* ctx, int level, int precision, const void* b, void* y);
+/* sqrt(dot(x, x)) with fp64 accumulation (norm, block_vector.hpp:63-66); synchronous */
+int smg_norm(smg_context* ctx, int level, int precision, const void* x, double* out);
+/* subtract the mass-weighted mean of the pressure block so that int p_h dx = 0
+ * (project_zero_mean); velocity blocks untouched */
+int smg_project_zero_mean(smg_context* ctx, int level, int precision, void* x);
 
 /* ---- host BlockVector <-> device level vector (BlockVector<dim,T> block_vector.hpp:15-18 with the
  *      DoFLayout of SPEC.md:173-176: velocity component blocks lexicographic x-fastest including the

@@ -19,10 +19,29 @@ def build():
     subprocess.check_call(["make", "-s", "-C", _HERE], stdout=subprocess.DEVNULL)
 
 
+def build_native():
+    """-march=native build for the timed CPU-baseline legs (the reference's Release flags,
+    proj/CMakeLists.txt:26-27); compiled on the host that runs it, into oracle/_native/."""
+    subprocess.check_call(["make", "-s", "-C", _HERE, "native"], stdout=subprocess.DEVNULL)
+
+
+def use_native():
+    """Load the -march=native build instead of the portable one (call before the first lib())."""
+    global _NATIVE
+    _NATIVE = True
+
+
+_NATIVE = False
+
+
 def lib():
     global _LIB
     if _LIB is None:
-        path = os.path.join(_HERE, "liboracle.so")
+        if _NATIVE:
+            build_native()
+            path = os.path.join(_HERE, "_native", "liboracle.so")
+        else:
+            path = os.path.join(_HERE, "liboracle.so")
         if not os.path.exists(path):
             build()
         _LIB = ctypes.CDLL(path)
@@ -200,6 +219,31 @@ def fgmres(k, level, b, tol=1e-8, max_iter=50, opts=None):
     if it < 0:
         raise ValueError("fgmres failed")
     return x, it, hist[: it + 1]
+
+
+def project_zero_mean(k, level, x):
+    """Mass-weighted pressure mean removal (project_zero_mean)."""
+    x = np.array(x, dtype=np.float64, copy=True)
+    if lib().orc_project_zero_mean(k, level, _ptr(x)) != 0:
+        raise ValueError("project_zero_mean failed")
+    return x
+
+
+def apply_stokes_sample(k, level, x, z0, z1, y=None):
+    """Timing sample: the operator on the cells z in [z0, z1) (rows at the ends incomplete)."""
+    y = np.zeros_like(x) if y is None else y
+    if lib().orc_apply_stokes_sample(k, level, _ptr(x), _ptr(y), int(z0), int(z1)) != 0:
+        raise ValueError("apply_stokes_sample failed")
+    return y
+
+
+def smooth_sample(k, level, x, b, vz0, vz1, opts=None):
+    """Timing sample: one smoothing step on the patches with vertex z plane in [vz0, vz1], in place."""
+    opts = opts or cg_opts()
+    it = ctypes.c_int()
+    if lib().orc_smooth_sample(k, level, _ptr(x), _ptr(b), ctypes.byref(opts), int(vz0), int(vz1), ctypes.byref(it)):
+        raise ValueError("smooth_sample failed")
+    return it.value
 
 
 def set_threads(n):

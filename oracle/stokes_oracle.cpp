@@ -700,16 +700,31 @@ const OpTables& tables(int k) {
   return *p;
 }
 
-void apply_stokes(const Level& L, const double* x, double* y) {
+// Cells with z in [z0, z1) only (default: all): the timed CPU-baseline legs use a z-slab of the
+// benchmarked level as a bounded sample (same per-DoF work as the whole level); the rows near the
+// ends of the sample are then incomplete, which only the timing legs accept.
+void apply_stokes(const Level& L, const double* x, double* y, int z0 = 0, int z1 = -1) {
   const OpTables& T = tables(L.k);
-  std::fill(y, y + L.total, 0.0);
   const int m = L.m;
+  if (z1 < 0) z1 = m;
+  if (z0 == 0 && z1 == m) {
+    std::fill(y, y + L.total, 0.0);
+  } else {
+    const int64_t H = L.k + 1;
+    for (int c = 0; c < 4; ++c) {
+      const int64_t pl = c < 3 ? L.dims[c][0] * L.dims[c][1] : int64_t(L.n) * L.n;
+      std::fill(y + L.off[c] + z0 * H * pl, y + L.off[c] + std::min<int64_t>(z1 * H + 1, c == 2 ? L.n + 1 : L.n) * pl,
+                0.0);
+    }
+  }
+  // first index >= lo with the parity p
+  auto first = [](int p, int lo) { return lo + ((p - lo) & 1); };
   // cells in 8 parity colours: same-colour cells share no DoF, so the scatter is race-free and the
   // result is independent of the thread count.
   for (int col = 0; col < 8; ++col) {
     const int px = col & 1, py = (col >> 1) & 1, pz = (col >> 2) & 1;
 #pragma omp parallel for collapse(2) schedule(static)
-    for (int ez = pz; ez < m; ez += 2)
+    for (int ez = first(pz, z0); ez < z1; ez += 2)
       for (int ey = py; ey < m; ey += 2)
         for (int ex = px; ex < m; ex += 2) {
           int e[3] = {ex, ey, ez};
@@ -722,7 +737,7 @@ void apply_stokes(const Level& L, const double* x, double* y) {
     for (int col = 0; col < 8; ++col) {
       const int px = col & 1, py = (col >> 1) & 1, pz = (col >> 2) & 1;
 #pragma omp parallel for collapse(2) schedule(static)
-      for (int ez = pz; ez < m; ez += 2)
+      for (int ez = first(pz, z0); ez < z1; ez += 2)
         for (int ey = py; ey < m; ey += 2)
           for (int ex = px; ex < m; ex += 2) {
             int e[3] = {ex, ey, ez};
@@ -732,19 +747,24 @@ void apply_stokes(const Level& L, const double* x, double* y) {
     }
   // boundary faces, 4 parity colours of the tangential cell coordinates
   for (int d = 0; d < 3; ++d)
-    for (int upper = 0; upper < 2; ++upper)
+    for (int upper = 0; upper < 2; ++upper) {
+      if (d == 2 && !(upper ? z1 == m : z0 == 0)) continue;
       for (int col = 0; col < 4; ++col) {
+        const int a1 = (d + 1) % 3, a2 = (d + 2) % 3;
+        // the loop coordinate along z (i for d = 1, j for d = 0) runs over [z0, z1)
+        const int ilo = a1 == 2 ? z0 : 0, ihi = a1 == 2 ? z1 : m;
+        const int jlo = a2 == 2 ? z0 : 0, jhi = a2 == 2 ? z1 : m;
 #pragma omp parallel for collapse(2) schedule(static)
-        for (int j = (col >> 1); j < m; j += 2)
-          for (int i = (col & 1); i < m; i += 2) {
+        for (int j = first(col >> 1, jlo); j < jhi; j += 2)
+          for (int i = first(col & 1, ilo); i < ihi; i += 2) {
             int e[3];
-            const int a1 = (d + 1) % 3, a2 = (d + 2) % 3;
             e[d] = upper ? m - 1 : 0;
             e[a1] = i;
             e[a2] = j;
             boundary_face(L, T, d, upper != 0, e, x, y);
           }
       }
+    }
 }
 
 // ================================================================================================
@@ -984,20 +1004,26 @@ void patch_scatter_add(const Level& L, const PatchCtx& P, const int* v, const st
 // one smoothing step (Alg. 2): colours 0..7 in fixed order (mesh.hpp:83-85,
 // SPEC.md:425); per colour a fresh global residual, then all patches of the colour
 // independently (their writes are disjoint).
-int smooth(const Level& L, double* x, const double* b, const orc_cg_opts& o) {
+// vz_lo / vz_hi: only the patches with vertex z plane in [vz_lo, vz_hi] and the residual on the cells
+// around them (timing samples of the CPU-baseline legs; default: the whole level)
+int smooth(const Level& L, double* x, const double* b, const orc_cg_opts& o, int vz_lo = 1, int vz_hi = -1) {
   const int nv = L.m - 1;
   if (nv <= 0) return 0;
+  if (vz_hi < 0) vz_hi = nv;
+  const bool full = vz_lo <= 1 && vz_hi >= nv;
   std::vector<double> r(L.total);
   int total_iters = 0;
   for (int col = 0; col < 8; ++col) {
-    apply_stokes(L, x, r.data());
+    if (full) apply_stokes(L, x, r.data());
+    else apply_stokes(L, x, r.data(), std::max(vz_lo - 1, 0), std::min(vz_hi + 1, L.m));
     for (int64_t i = 0; i < L.total; ++i) r[i] = b[i] - r[i];
     const int px = col & 1, py = (col >> 1) & 1, pz = (col >> 2) & 1;
     // vertex coordinate v_i has parity bit (v_i % 2) == colour bit i
     const int sx = px ? 1 : 2, sy = py ? 1 : 2, sz = pz ? 1 : 2;
     int iters = 0;
+    const int vz0 = std::max(sz, vz_lo + ((sz - vz_lo) & 1));
 #pragma omp parallel for collapse(2) schedule(dynamic) reduction(+ : iters)
-    for (int vz = sz; vz <= nv; vz += 2)
+    for (int vz = vz0; vz <= std::min(nv, vz_hi); vz += 2)
       for (int vy = sy; vy <= nv; vy += 2)
         for (int vx = sx; vx <= nv; vx += 2) {
           int v[3] = {vx, vy, vz};
@@ -1444,6 +1470,28 @@ int orc_vcycle(int k, int level, const double* b, double* x, const orc_cg_opts* 
 int orc_fgmres(int k, int level, const double* b, double* x, double rel_tol, int max_iter, const orc_cg_opts* opts,
                double* history) {
   return guard([&] { return fgmres(k, level, b, x, rel_tol, max_iter, *opts, history); });
+}
+// mass-weighted pressure mean removal on a full level vector (project_zero_mean SPEC.md:212-220)
+int orc_project_zero_mean(int k, int level, double* x) {
+  return guard([&] {
+    project_pressure_mass(Level(k, level), x);
+    return 0;
+  });
+}
+// timing samples for the CPU-baseline legs (bench.py): the operator on the cells z in [z0, z1) of the
+// level, and one smoothing step restricted to the patches with vertex z plane in [vz0, vz1]
+int orc_apply_stokes_sample(int k, int level, const double* x, double* y, int z0, int z1) {
+  return guard([&] {
+    apply_stokes(Level(k, level), x, y, z0, z1);
+    return 0;
+  });
+}
+int orc_smooth_sample(int k, int level, double* x, const double* b, const orc_cg_opts* opts, int vz0, int vz1,
+                      int* iters) {
+  return guard([&] {
+    *iters = smooth(Level(k, level), x, b, *opts, vz0, vz1);
+    return 0;
+  });
 }
 void orc_set_threads(int n) { omp_set_num_threads(n); }
 }

@@ -73,6 +73,15 @@ int orc_vcycle(int k, int level, const double* b, double* x, const orc_cg_opts* 
 int orc_fgmres(int k, int level, const double* b, double* x, double rel_tol, int max_iter, const orc_cg_opts* opts,
                double* history);
 
+// mass-weighted zero-mean projection of the pressure block of a level vector
+int orc_project_zero_mean(int k, int level, double* x);
+
+// timing samples (bench.py CPU legs): operator on the cells z in [z0, z1); one smoothing step on the
+// patches with vertex z plane in [vz0, vz1] (rows at the sample ends are incomplete: timing only)
+int orc_apply_stokes_sample(int k, int level, const double* x, double* y, int z0, int z1);
+int orc_smooth_sample(int k, int level, double* x, const double* b, const orc_cg_opts* opts, int vz0, int vz1,
+                      int* iters);
+
 void orc_set_threads(int n);
 
 #ifdef __cplusplus

@@ -26,7 +26,8 @@ EXPORTED = [
     "smg_prolongate_add", "smg_restrict", "smg_coarse_solve", "smg_vcycle", "smg_solve", "smg_dot", "smg_axpy",
     "smg_convert", "smg_vmult_host", "smg_vec_upload", "smg_vec_download", "smg_slab_sizes", "smg_vmult_slab",
     "smg_residual_slab", "smg_dot_slab", "smg_held_sizes", "smg_residual_held", "smg_smooth_colour_held",
-    "smg_prolongate_add_held", "smg_restrict_held", "smg_dot_held",
+    "smg_prolongate_add_held", "smg_restrict_held", "smg_dot_held", "smg_scale", "smg_subtract_from", "smg_norm",
+    "smg_project_zero_mean", "smg_pressure_node_weights",
 ]
 
 
@@ -80,6 +81,11 @@ def lib():
         L.smg_dot.argtypes = [P, I, I, P, P, ctypes.POINTER(D)]
         L.smg_axpy.argtypes = [P, I, I, D, P, P]
         L.smg_convert.argtypes = [P, I, I, P, I, P]
+        L.smg_pressure_node_weights.argtypes = [I, P]
+        L.smg_scale.argtypes = [P, I, I, D, P]
+        L.smg_subtract_from.argtypes = [P, I, I, P, P]
+        L.smg_norm.argtypes = [P, I, I, P, ctypes.POINTER(D)]
+        L.smg_project_zero_mean.argtypes = [P, I, I, P]
         L.smg_vmult_host.argtypes = [P, I, I, P, P, P, P]
         L.smg_vec_upload.argtypes = [P, I, I, P, P, P]
         L.smg_slab_sizes.argtypes = [I, I, I, I, P]
@@ -103,6 +109,14 @@ def level_sizes(degree, level):
     if rc != SMG_OK:
         raise ValueError(f"invalid degree/level ({degree}, {level})")
     return [int(v) for v in s]
+
+
+def pressure_node_weights(degree):
+    """Integrals of the pressure nodal basis over the reference cell (weights of the mass-weighted mean)."""
+    w = np.zeros(degree + 1)
+    if lib().smg_pressure_node_weights(degree, w.ctypes.data_as(ctypes.c_void_p)) != SMG_OK:
+        raise ValueError(f"invalid degree {degree}")
+    return w
 
 
 def _ptr(t):
@@ -177,6 +191,20 @@ class Context:
         if t.numel() != self.sizes(level)[4]:
             raise ValueError(f"vector has {t.numel()} entries, level {level} needs {self.sizes(level)[4]}")
 
+    def _vec(self, t, level, prec=None):
+        """Validate a device level vector: CUDA, contiguous, on this context's device, float64/float32
+        (and equal to `prec` if given), exactly the stored size of `level`. The C ABI takes raw pointers
+        without sizes, so a mismatch here would otherwise be an out-of-bounds device access."""
+        p = self._prec(t)
+        if t.device.index != self.device:
+            raise ValueError(f"vector is on cuda:{t.device.index}, the context on cuda:{self.device}")
+        if prec is not None and p != prec:
+            raise ValueError("all vectors of a call must have the same precision")
+        if level < 0 or level > self.max_level:
+            raise ValueError(f"level {level} out of range 0..{self.max_level}")
+        self._check_size(t, level)
+        return p
+
     def sizes(self, level):
         return level_sizes(self.degree, level)
 
@@ -191,9 +219,9 @@ class Context:
     # ---- hot path ----
     def apply_stokes(self, level, x, out=None):
         """y = A x (apply_stokes)."""
-        p = self._prec(x)
-        self._check_size(x, level)
+        p = self._vec(x, level)
         y = self._torch.empty_like(x) if out is None else out
+        self._vec(y, level, p)
         self._sync_stream()
         self._check(lib().smg_vmult(self._h, level, p, _ptr(y), _ptr(x)))
         return y
@@ -201,42 +229,47 @@ class Context:
     vmult = apply_stokes
 
     def residual(self, level, b, x, out=None):
-        p = self._prec(x)
+        p = self._vec(x, level)
+        self._vec(b, level, p)
         r = self._torch.empty_like(x) if out is None else out
+        self._vec(r, level, p)
         self._sync_stream()
         self._check(lib().smg_residual(self._h, level, p, _ptr(r), _ptr(b), _ptr(x)))
         return r
 
     def smooth(self, level, x, b, zero_init=False):
         """one multiplicative colour-by-colour vertex-patch step, in place on x."""
-        p = self._prec(x)
+        p = self._vec(x, level)
+        self._vec(b, level, p)
         self._sync_stream()
         self._check(lib().smg_smooth(self._h, level, p, _ptr(x), _ptr(b), int(zero_init)))
         return x
 
     def prolongate_add(self, coarse_level, x_fine, x_coarse):
-        p = self._prec(x_fine)
+        p = self._vec(x_fine, coarse_level + 1)
+        self._vec(x_coarse, coarse_level, p)
         self._sync_stream()
         self._check(lib().smg_prolongate_add(self._h, coarse_level, p, _ptr(x_fine), _ptr(x_coarse)))
         return x_fine
 
     def restrict(self, coarse_level, r_fine, out=None):
-        p = self._prec(r_fine)
+        p = self._vec(r_fine, coarse_level + 1)
         rc = out if out is not None else self._torch.zeros(self.sizes(coarse_level)[4], dtype=r_fine.dtype,
                                                            device=r_fine.device)
+        self._vec(rc, coarse_level, p)
         self._sync_stream()
         self._check(lib().smg_restrict(self._h, coarse_level, p, _ptr(rc), _ptr(r_fine)))
         return rc
 
     def coarse_solve(self, b):
-        p = self._prec(b)
+        p = self._vec(b, 0)
         x = self._torch.zeros_like(b)
         self._sync_stream()
         self._check(lib().smg_coarse_solve(self._h, p, _ptr(x), _ptr(b)))
         return x
 
     def vcycle(self, level, b):
-        p = self._prec(b)
+        p = self._vec(b, level)
         x = self._torch.zeros_like(b)
         self._sync_stream()
         self._check(lib().smg_vcycle(self._h, level, p, _ptr(x), _ptr(b)))
@@ -244,7 +277,7 @@ class Context:
 
     def solve(self, level, b, rel_tol=1e-8, max_iter=50, vcycle_precision=F32, allow_not_converged=False):
         """MG-preconditioned FGMRES (solve_mixed SPEC.md:525-533). Returns (x, iterations, history)."""
-        if self._prec(b) != F64:
+        if self._vec(b, level) != F64:
             raise ValueError("solve expects a float64 right-hand side")
         x = self._torch.zeros_like(b)
         it = ctypes.c_int()
@@ -258,10 +291,50 @@ class Context:
         return x, it.value, hist[: it.value + 1]
 
     def dot(self, level, a, b):
+        p = self._vec(a, level)
+        self._vec(b, level, p)
         out = ctypes.c_double()
         self._sync_stream()
-        self._check(lib().smg_dot(self._h, level, self._prec(a), _ptr(a), _ptr(b), ctypes.byref(out)))
+        self._check(lib().smg_dot(self._h, level, p, _ptr(a), _ptr(b), ctypes.byref(out)))
         return out.value
+
+    def norm(self, level, x):
+        """sqrt(dot(x, x)), fp64 accumulation (norm, block_vector.hpp:63-66)."""
+        p = self._vec(x, level)
+        out = ctypes.c_double()
+        self._sync_stream()
+        self._check(lib().smg_norm(self._h, level, p, _ptr(x), ctypes.byref(out)))
+        return out.value
+
+    def axpy(self, level, alpha, x, y):
+        """y += alpha x (axpy, block_vector.hpp:68-76)."""
+        p = self._vec(x, level)
+        self._vec(y, level, p)
+        self._sync_stream()
+        self._check(lib().smg_axpy(self._h, level, p, float(alpha), _ptr(x), _ptr(y)))
+        return y
+
+    def scale(self, level, alpha, x):
+        """x *= alpha (scale, block_vector.hpp:74-78)."""
+        p = self._vec(x, level)
+        self._sync_stream()
+        self._check(lib().smg_scale(self._h, level, p, float(alpha), _ptr(x)))
+        return x
+
+    def subtract_from(self, level, b, y):
+        """y = b - y (subtract_from, block_vector.hpp:80-88)."""
+        p = self._vec(y, level)
+        self._vec(b, level, p)
+        self._sync_stream()
+        self._check(lib().smg_subtract_from(self._h, level, p, _ptr(b), _ptr(y)))
+        return y
+
+    def project_zero_mean(self, level, x):
+        """Remove the mass-weighted pressure mean in place (project_zero_mean)."""
+        p = self._vec(x, level)
+        self._sync_stream()
+        self._check(lib().smg_project_zero_mean(self._h, level, p, _ptr(x)))
+        return x
 
     def vmult_host(self, level, x_blocks, precision=F64, out=None):
         """Reference-facing path: host arrays in the BlockVector layout (3 velocity blocks + the pressure

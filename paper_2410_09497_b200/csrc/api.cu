@@ -11,6 +11,9 @@
 #include <string>
 #include <cstdlib>
 #include <vector>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 #include "smg_internal.cuh"
 
@@ -400,6 +403,8 @@ template <class F>
 int guarded(smg_context* h, F&& f) {
   Context* c = reinterpret_cast<Context*>(h);
   try {
+    // launches and allocations go to the context's device whatever device the caller made current
+    if (c && c->device_ready) SMG_CUDA(cudaSetDevice(c->device));
     return f();
   } catch (const std::invalid_argument& e) {
     if (c) c->last_error = e.what();
@@ -415,6 +420,19 @@ int guarded(smg_context* h, F&& f) {
     return SMG_ECUDA;
   }
 }
+
+}  // namespace
+
+void ensure_smem_attr(const void* kernel, int device, size_t bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, size_t>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({device, kernel, bytes})) return;
+  SMG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  done.insert({device, kernel, bytes});
+}
+
+namespace {
 
 Context& ctx_of(smg_context* h) {
   if (!h) throw std::invalid_argument("null context");
@@ -463,6 +481,13 @@ int smg_level_sizes(int degree, int level, int64_t sizes[5]) {
   }
 }
 
+int smg_pressure_node_weights(int degree, double* w) {
+  if (degree < 1 || degree > 7 || !w) return SMG_EINVAL;
+  const auto v = smg::pressure_node_weights(degree);
+  for (int a = 0; a <= degree; ++a) w[a] = v[a];
+  return SMG_OK;
+}
+
 static thread_local std::string g_create_error;
 
 int smg_create(const smg_config* cfg, smg_context** out) {
@@ -483,6 +508,7 @@ int smg_create(const smg_config* cfg, smg_context** out) {
     SMG_CUDA(cudaGetDeviceProperties(&prop, cfg->device));
     if (prop.major < 10) throw smg::cuda_error("libsmg_b200 needs an sm_100 (Blackwell) device");
     c->device = cfg->device;
+    c->num_sms = prop.multiProcessorCount;
     smg::upload_reference_tables();
     const int L = cfg->max_level;
     c->ttab = smg::build_transfer_tables(cfg->degree);
@@ -509,6 +535,7 @@ int smg_create(const smg_config* cfg, smg_context** out) {
     SMG_CUDA(cudaMallocHost(&c->dot_host, 64));
     SMG_CUDA(cudaMalloc(&c->tmap_dev, static_cast<size_t>(smg::kTmapSlots) * smg::kTmapSlotBytes));
     c->allocations.push_back(c->tmap_dev);
+    c->device_ready = true;
     return SMG_OK;
   });
   if (rc != SMG_OK) {
@@ -811,6 +838,50 @@ int smg_convert(smg_context* h, int level, int dp, void* dst, int sp, const void
     smg::check_prec(dp);
     smg::check_prec(sp);
     smg::launch_convert(c, c.dev[0][level].lay.total, dp, dst, sp, src);
+    return SMG_OK;
+  });
+}
+
+int smg_scale(smg_context* h, int level, int precision, double alpha, void* x) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!x) throw std::invalid_argument("scale: null vector");
+    smg::launch_scale(c, c.dev[0][level].lay.total, precision, alpha, x);
+    return SMG_OK;
+  });
+}
+
+int smg_subtract_from(smg_context* h, int level, int precision, const void* b, void* y) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!b || !y) throw std::invalid_argument("subtract_from: null vector");
+    smg::launch_axpby(c, c.dev[0][level].lay.total, precision, 1.0, b, -1.0, y);  // y = b - y
+    return SMG_OK;
+  });
+}
+
+int smg_norm(smg_context* h, int level, int precision, const void* x, double* out) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!x || !out) throw std::invalid_argument("norm: null pointer");
+    *out = std::sqrt(smg::dot(c, c.dev[0][level].lay.total, precision, x, x));
+    return SMG_OK;
+  });
+}
+
+int smg_project_zero_mean(smg_context* h, int level, int precision, void* x) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    smg::check_level(c, level);
+    smg::check_prec(precision);
+    if (!x) throw std::invalid_argument("project_zero_mean: null vector");
+    smg::launch_sub_pressure_mean(c, level, precision, x);
     return SMG_OK;
   });
 }

@@ -99,6 +99,8 @@ struct TmapKey {
 struct Context {
   smg_config cfg{};
   int device = 0;
+  bool device_ready = false;  // set once smg_create validated the device: every entry point then pins it
+  int num_sms = 0;            // SM count of `device` (persistent grids)
   cudaStream_t stream = nullptr;
   std::string last_error;
   int64_t launches = 0;
@@ -132,6 +134,10 @@ constexpr int kTmapSlots = 64;         // cached TMA descriptor sets (global mem
 constexpr int kTmapSlotBytes = 512;    // 4 CUtensorMap (128 B each)
 
 size_t elem_size(int precision);
+
+// raise a kernel's dynamic shared-memory limit once per (device, kernel, size); thread-safe. The
+// attribute is per device, so a process-wide "done" flag would skip it for a second device.
+void ensure_smem_attr(const void* kernel, int device, size_t bytes);
 
 void upload_reference_tables();  // __constant__ reference-cell blocks (vmult.cu)
 

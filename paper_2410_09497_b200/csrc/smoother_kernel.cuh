@@ -135,7 +135,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 // per-patch latency dominates)
 template <int GS>
 __device__ __forceinline__ void gsync() {
-  if constexpr (GS == 32) gsync<GS>();
+  if constexpr (GS == 32) __syncwarp();
   else __syncthreads();
 }
 template <int GS, typename T>
@@ -473,11 +473,7 @@ void launch_group(Context& ctx, const DevLevel& dl, const LevelLayout& lay, int 
   constexpr int MINB = smem_c * 3 <= 233472 ? 3 : (smem_c * 2 <= 233472 ? 2 : 1);
   static_assert(smem_c <= 233472, "patch workspace exceeds shared memory");
   auto kern = patch_smooth_kernel<T, K, W, MINB, GS>;
-  static bool attr = false;
-  if (!attr) {
-    SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = true;
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(kern), ctx.device, smem);
   kern<<<(npatch + W - 1) / W, GS * W, smem, ctx.stream>>>(
       sblocks(lay, static_cast<T*>(x)), sblocks(lay, static_cast<const T*>(r)), static_cast<const T*>(dl.patch),
       dl.lay.m, colour, vz_first, cnt_z, ctx.cfg.cg_max_iter, static_cast<T>(ctx.cfg.cg_tol), ctx.cfg.cg_fixed,

@@ -93,7 +93,9 @@ __global__ void prolongate_kernel(const TBlocks<T> xf, const TBlocks<const T> xc
 
 // Restriction = P^T: coarse node gc collects fine rows r < 2H of every coarse cell containing it
 // (the fine vertex at r = 2H of cell E is row 0 of cell E+1, counted once).
-// coarse rows of the coarse cells [c0, c1) (all rows: c0 = 0, c1 = mc); reads fine cells [2 c0 - 1, 2 c1]
+// coarse rows of the coarse cells [c0, c1) (all rows: c0 = 0, c1 = mc); reads fine cells [2 c0 - 2, 2 c1): a
+// u_z node on the bottom plane of coarse cell c0 (j = 0) also lies in coarse cell c0 - 1 and collects its
+// fine rows (fine cells 2 c0 - 2, 2 c0 - 1)
 template <typename T, int K>
 __global__ void restrict_kernel(const TBlocks<T> rc, const TBlocks<const T> rf, const T* __restrict__ tab, int mc,
                                 int c0, int c1) {
@@ -198,8 +200,8 @@ void transfer_k(Context& ctx, int coarse_level, void* out, const void* in, bool 
                                                               tblocks(cl, static_cast<const T*>(in)),
                                                               static_cast<const T*>(fine.transfer), mc, t.r0, t.r1);
   } else {
-    // coarse cells [r0, r1) read fine cells [2 r0 - 1, 2 r1] (within the domain)
-    if (t.r0 < t.czlo || t.r1 > t.czhi || std::max(2 * t.r0 - 1, 0) < t.fzlo || std::min(2 * t.r1 + 1, 2 * mc) > t.fzhi)
+    // coarse cells [r0, r1) read fine cells [2 r0 - 2, 2 r1) (within the domain), see restrict_kernel
+    if (t.r0 < t.czlo || t.r1 > t.czhi || std::max(2 * t.r0 - 2, 0) < t.fzlo || std::min(2 * t.r1, 2 * mc) > t.fzhi)
       throw std::invalid_argument("restrict: held ranges do not cover the rows");
     const int64_t rows = (static_cast<int64_t>(t.r1 - t.r0) * (K + 1) + 1) * cl.plane[0];
     dim3 grid(grid_for(rows), 4);

@@ -1046,9 +1046,7 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
   const Blocks<const T> B = block_bases(lay, static_cast<const T*>(a.b));
   const T h = static_cast<T>(1.0 / m);
   const int nbricks = ((m + BX - 1) / BX) * ((m + BY - 1) / BY) * ((a.z1 - a.z0 + BZ - 1) / BZ);
-  static int num_sms = 0;
-  if (num_sms == 0) SMG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, ctx.device));
-  const dim3 grid(std::min(nbricks, OCC * num_sms));
+  const dim3 grid(std::min(nbricks, OCC * ctx.num_sms));
   const size_t smem = BR::BYTES;
   static const bool no_tma = std::getenv("SMG_NO_TMA") != nullptr;  // diagnostics: force the cp.async path
   bool aligned = true;
@@ -1076,9 +1074,7 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
   }
   static_assert(sizeof(Maps) <= kTmapSlotBytes, "tensor-map slot too small");
   auto go = [&](auto kern) {
-    static std::set<const void*> attr_set;  // kernels whose smem limit is raised already
-    if (attr_set.insert(reinterpret_cast<const void*>(kern)).second)
-      SMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), ctx.device, smem);
     kern<<<grid, NT, smem, ctx.stream>>>(X, Y, B, m, a.z0, a.z1, a.zlo, a.zhi, h, dmaps);
   };
   if (a.b) {

@@ -20,7 +20,7 @@ import math
 
 import numpy as np
 
-from . import F32, F64, SMG_OK, _ptr, lib
+from . import F32, F64, SMG_OK, NotConverged, _ptr, lib, pressure_node_weights
 from .slab import partition
 
 GHOST = 3
@@ -273,9 +273,44 @@ class SlabMG:
         self.smooth(l, x, b, r)
         return {p: x[p].clone() for p in self.parts}
 
+    def allreduce_scalar(self, v):
+        if self.virtual or self.world == 1:
+            return v
+        import torch
+        import torch.distributed as dist
+        gloo = dist.get_backend(self.group) == "gloo"
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if gloo else f"cuda:{self.ctx.device}")
+        dist.all_reduce(t, group=self.group)
+        return float(t.item())
+
+    def project_zero_mean(self, x):
+        """Subtract the mass-weighted pressure mean (project_zero_mean SPEC.md:212-220) from every held
+        pressure row; the weighted sum runs over the owned rows and is all-reduced, so all ranks subtract
+        the same constant -- the one smg_solve subtracts on one GPU."""
+        import torch
+        L, H = self.L, self.k + 1
+        w1 = pressure_node_weights(self.k)
+        tot = 0.0
+        for p in self.parts:
+            S = self.slabs[p][L]
+            a, b = S.owned_planes(3)
+            pb = S.block(x[p], 3)[a:b]
+            dev = pb.device
+            wz = torch.tensor(w1[(np.arange(S.zlo * H + a, S.zlo * H + b)) % H], dtype=torch.float64, device=dev)
+            wn = torch.tensor(w1[np.arange(S.n) % H], dtype=torch.float64, device=dev)
+            wxy = torch.outer(wn, wn).reshape(-1)
+            tot += float((wz[:, None] * wxy[None, :] * pb.double()).sum())
+        tot = self.allreduce_scalar(tot)
+        mean = tot / (float(w1.sum()) ** 3 * float(2 << L) ** 3)
+        for p in self.parts:
+            self.slabs[p][L].block(x[p], 3).sub_(mean)
+        return x
+
     # ---- FGMRES (smg_solve semantics) ----
-    def solve(self, b, tol=1e-8, max_iter=50, vcycle_precision=F32):
-        """b: {part: fp64 held vector with valid owned rows}. Returns ({part: x}, iterations, history)."""
+    def solve(self, b, tol=1e-8, max_iter=50, vcycle_precision=F32, allow_not_converged=False):
+        """b: {part: fp64 held vector with valid owned rows}. Returns ({part: x}, iterations, history).
+        As smg_solve: the mass-weighted pressure mean of x is removed, and NotConverged is raised if the
+        relative residual did not reach `tol` within max_iter (unless allow_not_converged)."""
         import torch
         L = self.L
         d32 = torch.float32 if vcycle_precision == F32 else torch.float64
@@ -290,6 +325,7 @@ class SlabMG:
         cs, sn, g = np.zeros(max_iter), np.zeros(max_iter), np.zeros(max_iter + 1)
         g[0] = beta
         it = 0
+        converged = False
         for j in range(max_iter):
             z = self.vcycle(L, {p: V[j][p].to(d32) for p in self.parts}, d32)
             Z.append({p: z[p].double() for p in self.parts})
@@ -316,6 +352,7 @@ class SlabMG:
             it = j + 1
             hist.append(abs(g[j + 1]))
             if abs(g[j + 1]) <= tol * beta or wn == 0.0:
+                converged = True
                 break
             V.append({p: w[p] / wn for p in self.parts})
         y = np.zeros(it)
@@ -324,6 +361,10 @@ class SlabMG:
         for i in range(it):
             for p in self.parts:
                 x[p] += y[i] * Z[i][p]
+        self.project_zero_mean(x)
+        if not converged and not allow_not_converged:
+            raise NotConverged(-101, f"slab FGMRES: relative residual {hist[-1] / beta:.3e} > {tol:g} "
+                                     f"after {it} iterations")
         return x, it, hist
 
 

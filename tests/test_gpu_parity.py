@@ -310,6 +310,8 @@ def test_slab_multigrid_matches_single_gpu(k, level, nparts):
         mg.slabs[p][level].add_owned_into(got, xs[p])
     res = float((rhs - ctx.apply_stokes(level, got)).norm() / rhs.norm())
     assert res <= 2e-8
+    # same solution as smg_solve, including the mass-weighted pressure mean (both remove it)
+    assert rel(got.cpu().numpy(), x_ref.cpu().numpy()) <= 1e-6
 
 
 def test_cp_async_staging_path_matches_oracle():

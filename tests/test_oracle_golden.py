@@ -90,3 +90,27 @@ def test_generalized_eig_against_lapack():
             close(S.T @ M @ S, np.eye(len(lam)), tol=1e-11)
             close(L @ S, M @ S @ np.diag(lam), tol=1e-10)
             assert lam.min() > 0
+
+
+def test_oracle_project_zero_mean_kats():
+    # constant pressure -> 0; idempotent to 1e-14; mass-weighted mean of the output 0
+    import numpy as np
+    k, level = 2, 1
+    s = oracle.sizes(k, level)
+    npr = s[3]
+    c = np.zeros(s[4])
+    c[-npr:] = 2.5
+    assert np.abs(oracle.project_zero_mean(k, level, c)).max() <= 1e-14 * 2.5  # relative to the constant
+    x = np.random.default_rng(7).uniform(-1, 1, s[4]) + 0.3
+    y = oracle.project_zero_mean(k, level, x)
+    assert np.array_equal(y[:-npr], x[:-npr])
+    assert np.abs(oracle.project_zero_mean(k, level, y) - y).max() <= 1e-14
+    # the weights are the integrals of the nodal basis: a constant's weighted mean is the constant
+    n = (2 << level) * (k + 1)
+    p = y[-npr:].reshape(n, n, n)
+    gl, gw = oracle.gauss_quadrature(k + 2)
+    nodes = oracle.gauss_lobatto_points(k + 1)
+    w1 = np.array([sum(gw[q] * np.prod([(gl[q] - nodes[j]) / (nodes[a] - nodes[j]) for j in range(k + 1) if j != a])
+                       for q in range(k + 2)) for a in range(k + 1)])
+    w = w1[np.arange(n) % (k + 1)]
+    assert abs(np.einsum("zyx,z,y,x->", p, w, w, w)) <= 1e-13
