@@ -26,6 +26,7 @@ sys.path.insert(0, ROOT)
 
 DEGREE, LEVEL = 2, 5
 FP64_PEAK_TFLOPS = 33.3  # tools/fma_peak.cu on this pool's B200 (profiles/r01/fma_peaks.txt)
+FP32_PEAK_TFLOPS = 69.58
 METRIC = "Stokes operator-apply DoF/s (fp64), RT_2 64^3 cells; + fp32 smoother DoF/s and MG-FGMRES solve time"
 
 
@@ -122,26 +123,82 @@ def ncu_traffic(key):
         return None
 
 
-def cpu_baseline(k, level, budget_s=12.0):
-    """The CPU oracle (restatement of the reference algorithm, Alg. 1 cell/face loops, OpenMP) timed on
-    this host on a bounded sample: level-1 of the workload (1/8 of its DoF)."""
-    import numpy as np
-
+def _oracle_native():
     import oracle
-    sample_level = max(level - 1, 0)
-    n = dofs(k, sample_level)
-    x = np.random.default_rng(0).uniform(-1, 1, n)
-    oracle.apply_stokes(k, sample_level, x)  # warm-up (tables)
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        oracle.apply_stokes(k, sample_level, x)
-        reps += 1
-        if time.perf_counter() - t0 >= budget_s or reps >= 50:
-            break
-    dt = time.perf_counter() - t0
-    return {"value": n * reps / dt, "unit": "DoF/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"oracle Alg.1 vmult fp64 at k={k}, level {sample_level} ({2 << sample_level}^3 cells, {n} DoF),"
-                      f" {reps} reps in {dt:.1f}s, OpenMP all host threads"}
+    oracle.use_native()  # -march=native build, compiled on this host (reference Release flags)
+    return oracle
+
+
+def cpu_baseline(k, level, smoke=False):
+    """The CPU oracle (restatement of the reference algorithm: Alg. 1 cell/face loops, colour-parallel
+    patch smoother; built with the reference's Release flags -O3 -march=native -funroll-loops + OpenMP,
+    proj/CMakeLists.txt:26-27) timed on this host's cores, BASELINE.md §5 legs:
+      vmult at the benchmarked workload (C2, all threads: the whole level; 1 thread: a z-slab sample),
+      the smoothing step at C2 (z-slab samples of patches + their residual rows, all / 1 thread),
+      V-cycle at C1 (whole problem, all / 1 thread) and the MG-FGMRES solve at C1 (all threads).
+    Samples are z-slabs of the SAME level (identical per-DoF work); DoF/s = DoF in the sample / time."""
+    import numpy as np
+    oracle = _oracle_native()
+    ncpu = os.cpu_count()
+    m = 2 << level
+    N = dofs(k, level)
+    per_layer = N / m
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, N)
+    y = np.zeros(N)
+    legs = {}
+
+    def timeit(fn, min_s=1.0, max_reps=20):
+        fn()  # warm-up (tables, page faults)
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            fn()
+            reps += 1
+            if time.perf_counter() - t0 >= min_s or reps >= max_reps:
+                break
+        return (time.perf_counter() - t0) / reps, reps
+
+    for threads in (ncpu, 1):
+        oracle.set_threads(threads)
+        tag = "all" if threads == ncpu else "1thread"
+        nz = m if threads == ncpu else max(2, m // 32)
+        if nz == m:
+            dt, reps = timeit(lambda: oracle.apply_stokes(k, level, x), 2.0, 5)
+        else:
+            dt, reps = timeit(lambda: oracle.apply_stokes_sample(k, level, x, 0, nz, y), 1.0, 5)
+        legs[f"vmult_C2_{tag}"] = {"dofs_per_s": per_layer * nz / dt, "threads": threads, "reps": reps,
+                                   "sample": "whole level" if nz == m else f"cells z in [0,{nz}) of {m}"}
+        if smoke:
+            continue
+        # smoothing step (fp64 oracle; the GPU step is fp32), patches with vertex planes [1, vz1]
+        vz1 = 8 if threads == ncpu else 1
+        b = oracle.apply_stokes(k, level, x) if threads == ncpu else y
+        xs = np.zeros(N)
+        opts = oracle.cg_opts(30, 1e-5, False, 1)
+        t0 = time.perf_counter()
+        oracle.smooth_sample(k, level, xs, b, 1, vz1, opts)
+        dt = time.perf_counter() - t0
+        legs[f"smooth_C2_{tag}"] = {"dofs_per_s": per_layer * vz1 / dt, "threads": threads, "s_per_sample": dt,
+                                    "sample": f"patches with vertex z in [1,{vz1}] + their residual rows "
+                                              f"(~{vz1} of {m} cell layers), cg_tol 1e-5"}
+        # C1: V-cycle and solve (k=1, level 3), whole problem
+        k1, l1 = 1, 3
+        n1 = dofs(k1, l1)
+        b1 = oracle.apply_stokes(k1, l1, rng.uniform(-1, 1, n1))
+        o1 = oracle.cg_opts(30, 1e-8, False, 1)
+        dt, reps = timeit(lambda: oracle.vcycle(k1, l1, b1, o1), 0.5, 10)
+        legs[f"vcycle_C1_{tag}"] = {"s": dt, "dofs_per_s": n1 / dt, "threads": threads}
+        if threads == ncpu:  # (single-threaded: ~20 s, the V-cycle leg gives the 1-thread rate)
+            t0 = time.perf_counter()
+            _, it, _ = oracle.fgmres(k1, l1, b1, 1e-8, 40, o1)
+            dt = time.perf_counter() - t0
+            legs[f"solve_C1_{tag}"] = {"s": dt, "iterations": it, "ns_per_dof": dt / n1 * 1e9, "threads": threads}
+    oracle.set_threads(ncpu)
+    v = legs["vmult_C2_all"]["dofs_per_s"]
+    return {"value": v, "unit": "DoF/s", "cores": ncpu, "kind": "port",
+            "sample": f"oracle Alg.1 vmult fp64 at k={k}, level {level} ({m}^3 cells, {N} DoF, the benchmarked "
+                      f"workload), whole level, OpenMP {ncpu} threads; -O3 -march=native -funroll-loops",
+            "legs": legs}
 
 
 def run_reference(args):
@@ -149,30 +206,57 @@ def run_reference(args):
     if rank != 0:
         return
     import numpy as np
-
-    import oracle
+    oracle = _oracle_native()
     k, level = args.degree, args.level
-    sample_level = max(level - 1, 0)
-    n = dofs(k, sample_level)
-    x = np.random.default_rng(0).uniform(-1, 1, n)
+    m = 2 << level
+    N = dofs(k, level)
+    x = np.random.default_rng(0).uniform(-1, 1, N)
+    y = np.zeros(N)
+    # one whole-level apply measures the cost; every step is then a z-slab sample of the SAME level
+    # (identical per-DoF work) sized so that the --steps run stays within ~90 s
+    t0 = time.perf_counter()
+    oracle.apply_stokes(k, level, x)
+    t_full = time.perf_counter() - t0
+    nz = max(1, min(m, int(m * 90.0 / max(args.steps * t_full, 1e-9))))
     for _ in range(args.warmup):
-        oracle.apply_stokes(k, sample_level, x)
+        oracle.apply_stokes_sample(k, level, x, 0, nz, y)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.apply_stokes(k, sample_level, x)
+        oracle.apply_stokes_sample(k, level, x, 0, nz, y)
     dt = time.perf_counter() - t0
-    value = n * args.steps / dt
-    sample = (f"reference CPU path (oracle restatement; the reference ships no code for this path) vmult fp64, "
-              f"k={k}, level {sample_level} ({n} DoF) per step, all {os.cpu_count()} host threads")
+    n_sample = N * nz / m
+    value = n_sample * args.steps / dt
+    sample = (f"reference CPU path (oracle restatement of Alg. 1; the reference ships no code for this path), "
+              f"vmult fp64 at k={k}, level {level} ({m}^3 cells): each step the cells z in [0,{nz}) of the level "
+              f"(~{n_sample:.0f} DoF; whole level {t_full:.2f} s); all {os.cpu_count()} host threads, "
+              f"-O3 -march=native -funroll-loops")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C2 sample: RT_{k} {2 << sample_level}^3 cells (1/8 of the 64^3 workload)",
-                   "degree": k, "level": sample_level, "dofs": n},
+        "config": workload_config(k, level),
         "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": os.cpu_count(), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+
+
+def workload_config(k, level):
+    m = 2 << level
+    name = {(2, 5): "C2", (3, 6): "C3", (1, 3): "C1"}.get((k, level), "custom")
+    n = dofs(k, level)
+    return {"workload": f"{name}: 3D unit-cube Stokes RT_{k}/DGQ_{k}, {m}^3 cells (level {level}), fp64 operator apply",
+            "degree": k, "level": level, "dofs": n,
+            "l2": f"inputs larger than L2 (x, y {8 * n / 1e6:.0f} MB each vs 126 MB L2); no flush" if 8 * n > 126e6
+            else "inputs smaller than L2: an L2 flush is NOT applied, numbers are L2-resident"}
+
+
+def smoother_flops(k, patches, cg_iters):
+    """Algorithmic flops of the patch smoother kernel: per inner CG iteration 12 NP NO^3 + 8 NO^4 FMAs (the
+    18 contractions of S d = sum_c G_c Lambda_c^-1 G_c^T d plus the 3 of the pressure-mass preconditioner,
+    csrc/smoother_kernel.cuh), and the gather / right-hand side / final update counted as 2 iterations."""
+    NP, NO = 2 * k + 1, 2 * k + 2
+    per_it = 2 * (12 * NP * NO ** 3 + 8 * NO ** 4)
+    return per_it * (cg_iters + 2 * patches)
 
 
 def main():
@@ -267,9 +351,20 @@ def main():
         # ---- fp32 smoothing step (8 colours: residual + patch solve each) ----
         b32 = ctx.apply_stokes(level, x32)
         xs = torch.zeros_like(b32)
-        ms_smooth, _ = timed(lambda: ctx.smooth(level, xs, b32, zero_init=False), max(1, min(args.steps, 3)))
+        sm_steps = max(3, min(args.steps, 20))
+        ctx.smoother_stats(reset=True)
+        ms_smooth, _ = timed(lambda: ctx.smooth(level, xs, b32, zero_init=True), sm_steps)
+        npatch, cgit = ctx.smoother_stats(reset=True)
+        fl = smoother_flops(k, npatch, cgit) / (sm_steps + args.warmup)
+        sm_tf = fl / (ms_smooth * 1e-3) / 1e12
         extra["smoother_fp32"] = {"value": N / (ms_smooth * 1e-3), "unit": "DoF/s", "ms_per_step": ms_smooth,
-                                  "ns_per_dof": ms_smooth * 1e6 / N}
+                                  "ns_per_dof": ms_smooth * 1e6 / N, "timed_steps": sm_steps,
+                                  "mean_inner_cg_iterations": cgit / max(npatch, 1), "cg_tol": 1e-5,
+                                  "roofline": {"bound": "fp32 fma", "achieved_tflops": sm_tf,
+                                               "peak_tflops": FP32_PEAK_TFLOPS, "frac": sm_tf / FP32_PEAK_TFLOPS,
+                                               "algorithmic_flops_per_step": fl,
+                                               "note": "whole step incl. the 8 residual launches; patch-kernel "
+                                                       "flops only (bench.smoother_flops)"}}
 
         # ---- MG-FGMRES solve (mixed precision: fp64 Krylov, fp32 V-cycle) ----
         if not args.no_solve:
@@ -380,10 +475,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform random x, seed 1234)",
-        "config": {"workload": f"C2: 3D unit-cube Stokes RT_{k}/DGQ_{k}, {2 << level}^3 cells (level {level}), "
-                               f"fp64 operator apply", "degree": k, "level": level, "dofs": N,
-                   "parallelism": parallelism,
-                   "l2": "inputs larger than L2 (x, y 227 MB each vs 126 MB L2); no flush"},
+        "config": dict(workload_config(k, level), parallelism=parallelism),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,

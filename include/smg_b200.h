@@ -80,6 +80,10 @@ int smg_residual(smg_context* ctx, int level, int precision, void* r, const void
  *      Alg. 2, local solver schur_solve SPEC.md:356-364). zero_init: x := 0 first. */
 int smg_smooth(smg_context* ctx, int level, int precision, void* x, const void* b, int zero_init);
 
+/* counters of the patch smoother since context creation or the last reset: patches solved and inner
+ * Schur-CG iterations summed over them (mean iterations = cg_iterations / patches); synchronous */
+int smg_smoother_stats(smg_context* ctx, int reset, int64_t* patches, int64_t* cg_iterations);
+
 /* ---- transfer (prolongate / restrict SPEC.md:441-458): x_f += P x_c ;  r_c = P^T r_f ---- */
 int smg_prolongate_add(smg_context* ctx, int coarse_level, int precision, void* x_fine, const void* x_coarse);
 int smg_restrict(smg_context* ctx, int coarse_level, int precision, void* r_coarse, const void* r_fine);

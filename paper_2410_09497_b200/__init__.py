@@ -27,7 +27,7 @@ EXPORTED = [
     "smg_convert", "smg_vmult_host", "smg_vec_upload", "smg_vec_download", "smg_slab_sizes", "smg_vmult_slab",
     "smg_residual_slab", "smg_dot_slab", "smg_held_sizes", "smg_residual_held", "smg_smooth_colour_held",
     "smg_prolongate_add_held", "smg_restrict_held", "smg_dot_held", "smg_scale", "smg_subtract_from", "smg_norm",
-    "smg_project_zero_mean", "smg_pressure_node_weights",
+    "smg_project_zero_mean", "smg_pressure_node_weights", "smg_smoother_stats",
 ]
 
 
@@ -82,6 +82,7 @@ def lib():
         L.smg_axpy.argtypes = [P, I, I, D, P, P]
         L.smg_convert.argtypes = [P, I, I, P, I, P]
         L.smg_pressure_node_weights.argtypes = [I, P]
+        L.smg_smoother_stats.argtypes = [P, I, P, P]
         L.smg_scale.argtypes = [P, I, I, D, P]
         L.smg_subtract_from.argtypes = [P, I, I, P, P]
         L.smg_norm.argtypes = [P, I, I, P, ctypes.POINTER(D)]
@@ -297,6 +298,13 @@ class Context:
         self._sync_stream()
         self._check(lib().smg_dot(self._h, level, p, _ptr(a), _ptr(b), ctypes.byref(out)))
         return out.value
+
+    def smoother_stats(self, reset=False):
+        """(patches solved, inner Schur-CG iterations) since creation / the last reset."""
+        p, it = ctypes.c_int64(), ctypes.c_int64()
+        self._sync_stream()
+        self._check(lib().smg_smoother_stats(self._h, int(reset), ctypes.byref(p), ctypes.byref(it)))
+        return p.value, it.value
 
     def norm(self, level, x):
         """sqrt(dot(x, x)), fp64 accumulation (norm, block_vector.hpp:63-66)."""

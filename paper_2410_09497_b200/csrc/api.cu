@@ -92,11 +92,14 @@ void setup_coarse(Context& c) {
   std::vector<int> blk(nf);
   std::vector<int> co(3 * nf);
   for (int i = 0; i < nf; ++i) decode(fr[i], blk[i], &co[3 * i]);
+  const int band = 2 * (c.cfg.degree + 1) + 1;  // every 1D factor vanishes beyond one neighbour cell
+#pragma omp parallel for schedule(dynamic, 64)
   for (int i = 0; i < nf; ++i)
     for (int j = 0; j < nf; ++j) {
       const int bi = blk[i], bj = blk[j];
       const int* gi = &co[3 * i];
       const int* gj = &co[3 * j];
+      if (std::abs(gi[0] - gj[0]) > band || std::abs(gi[1] - gj[1]) > band || std::abs(gi[2] - gj[2]) > band) continue;
       double v = 0.0;
       if (bi < 3 && bj == bi) {
         // Kronecker sum: sum_d L_d (x) M_others, par factors along axis bi
@@ -123,13 +126,8 @@ void setup_coarse(Context& c) {
     }
   for (int i = 0; i < nf; ++i)
     if (blk[i] == 3) K(i, nf) = K(nf, i) = 1.0;
-  const Dense Ki = inverse(K);
-  std::vector<double> pinv(static_cast<size_t>(nf) * nf);
-  for (int i = 0; i < nf; ++i)
-    for (int j = 0; j < nf; ++j) pinv[static_cast<size_t>(i) * nf + j] = 0.5 * (Ki(i, j) + Ki(j, i));
   c.coarse_free = fr;
-  c.coarse_pinv[0] = dev_upload(c, pinv, SMG_F64);
-  c.coarse_pinv[1] = dev_upload(c, pinv, SMG_F32);
+  coarse_inverse_device(c, K, nf, &c.coarse_pinv[0], &c.coarse_pinv[1]);
   void* d = nullptr;
   SMG_CUDA(cudaMalloc(&d, fr.size() * sizeof(int64_t)));
   c.allocations.push_back(d);
@@ -533,6 +531,9 @@ int smg_create(const smg_config* cfg, smg_context** out) {
     SMG_CUDA(cudaMalloc(&c->dot_partials, (smg::kDotBlocks + 8) * sizeof(double)));
     c->allocations.push_back(c->dot_partials);
     SMG_CUDA(cudaMallocHost(&c->dot_host, 64));
+    SMG_CUDA(cudaMalloc(&c->smoother_stats, 2 * sizeof(unsigned long long)));
+    c->allocations.push_back(c->smoother_stats);
+    SMG_CUDA(cudaMemset(c->smoother_stats, 0, 2 * sizeof(unsigned long long)));
     SMG_CUDA(cudaMalloc(&c->tmap_dev, static_cast<size_t>(smg::kTmapSlots) * smg::kTmapSlotBytes));
     c->allocations.push_back(c->tmap_dev);
     c->device_ready = true;
@@ -838,6 +839,19 @@ int smg_convert(smg_context* h, int level, int dp, void* dst, int sp, const void
     smg::check_prec(dp);
     smg::check_prec(sp);
     smg::launch_convert(c, c.dev[0][level].lay.total, dp, dst, sp, src);
+    return SMG_OK;
+  });
+}
+
+int smg_smoother_stats(smg_context* h, int reset, int64_t* patches, int64_t* cg_iterations) {
+  return smg::guarded(h, [&] {
+    Context& c = smg::ctx_of(h);
+    unsigned long long v[2];
+    SMG_CUDA(cudaMemcpyAsync(v, c.smoother_stats, sizeof(v), cudaMemcpyDeviceToHost, c.stream));
+    SMG_CUDA(cudaStreamSynchronize(c.stream));
+    if (patches) *patches = static_cast<int64_t>(v[0]);
+    if (cg_iterations) *cg_iterations = static_cast<int64_t>(v[1]);
+    if (reset) SMG_CUDA(cudaMemsetAsync(c.smoother_stats, 0, sizeof(v), c.stream));
     return SMG_OK;
   });
 }

@@ -115,6 +115,7 @@ struct Context {
   // scratch
   void* dot_partials = nullptr;  // double[kDotBlocks]
   void* dot_host = nullptr;      // pinned double[kDotBlocks]
+  void* smoother_stats = nullptr;  // unsigned long long[2]: patches solved, inner CG iterations
   std::vector<void*> allocations;
   // per-level work vectors for the smoother / V-cycle (allocated lazily): [prec][level]
   std::vector<void*> work_r[2], work_x[2], work_b[2];
@@ -138,6 +139,10 @@ size_t elem_size(int precision);
 // raise a kernel's dynamic shared-memory limit once per (device, kernel, size); thread-safe. The
 // attribute is per device, so a process-wide "done" flag would skip it for a second device.
 void ensure_smem_attr(const void* kernel, int device, size_t bytes);
+
+// level-0 pseudo-inverse from the bordered (nf+1)^2 system K on the device (coarse.cu): fp64 and fp32
+// nf x nf copies, owned by the context
+void coarse_inverse_device(Context& c, const Dense& K, int nf, void** pinv64, void** pinv32);
 
 void upload_reference_tables();  // __constant__ reference-cell blocks (vmult.cu)
 

@@ -284,7 +284,8 @@ template <typename T, int K, int W, int MINB, int GS>
 __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlocks<T> x, const SBlocks<const T> r,
                                                               const T* __restrict__ ptab, int m, int colour,
                                                               int vz_first, int cnt_z, int cg_max_iter, T cg_tol,
-                                                              int cg_fixed, int cg_precond) {
+                                                              int cg_fixed, int cg_precond,
+                                                              unsigned long long* __restrict__ stats) {
   using P = PD<K>;
   constexpr int H = K + 1, NO = P::NO;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -386,7 +387,8 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
   gsync<GS>();
   T rz = ps.dot(Pr, Pz);
   const T r0 = sqrt(ps.dot(Pr, Pr));
-  for (int it = 0; it < cg_max_iter; ++it) {
+  int it = 0;
+  for (; it < cg_max_iter; ++it) {
     if (!cg_fixed) {
       if (sqrt(ps.dot(Pr, Pr)) <= cg_tol * r0) break;
     }
@@ -421,6 +423,10 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
     gsync<GS>();
   }
   ps.project(Px);
+  if (lane == 0) {  // patches solved and inner CG iterations (smg_smoother_stats)
+    atomicAdd(&stats[0], 1ull);
+    atomicAdd(&stats[1], static_cast<unsigned long long>(it));
+  }
   // ---- U_c = (S (x) S (x) S) Lambda_c^-1 [Fh_c - G_c^T P];  x += R^T (U, P) ----
   SMG_FOR_C({
     ps.template gt3<C>(Px, T1, T2);
@@ -477,7 +483,7 @@ void launch_group(Context& ctx, const DevLevel& dl, const LevelLayout& lay, int 
   kern<<<(npatch + W - 1) / W, GS * W, smem, ctx.stream>>>(
       sblocks(lay, static_cast<T*>(x)), sblocks(lay, static_cast<const T*>(r)), static_cast<const T*>(dl.patch),
       dl.lay.m, colour, vz_first, cnt_z, ctx.cfg.cg_max_iter, static_cast<T>(ctx.cfg.cg_tol), ctx.cfg.cg_fixed,
-      ctx.cfg.cg_precond);
+      ctx.cfg.cg_precond, static_cast<unsigned long long*>(ctx.smoother_stats));
   SMG_CUDA(cudaGetLastError());
   ++ctx.launches;
 }

@@ -229,3 +229,13 @@ def test_restrict_held_minimal_range(k):
     rc = lib.smg_restrict_held(ctx._h, level - 1, smg.F64, ctypes.c_void_p(rch.data_ptr()),
                                ctypes.c_void_p(rfh.data_ptr()), fzlo + 1, fzhi, C.zlo, C.zhi, c0, c1)
     assert rc == smg.SMG_EINVAL
+
+
+def test_coarse_solve_k4_device_factorisation():
+    # level-0 pseudo-inverse built by the device LU (coarse.cu) at k = 4 (nf = 4300), against the oracle
+    k = 4
+    ctx = smg.Context(k, 1)
+    b = oracle.apply_stokes(k, 0, rand_vec(k, 0, 48))
+    ref = oracle.coarse_solve(k, b)
+    got = ctx.coarse_solve(dev(b)).cpu().numpy()
+    assert rel(got, ref) <= 1e-10
