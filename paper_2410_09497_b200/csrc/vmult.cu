@@ -17,9 +17,14 @@ void upload_reference_tables() {
   vmult_upload_k<5>(t.data(), f.data());
   vmult_upload_k<6>(t.data(), f.data());
   vmult_upload_k<7>(t.data(), f.data());
+  zm_upload_k<1>(t.data(), f.data());
+  zm_upload_k<2>(t.data(), f.data());
 }
 
 void launch_vmult_args(Context& ctx, int level, int prec, const VmultArgs& a) {
+  // k <= 2: the z-march kernel where its tiles fit the level, else the brick kernel
+  if (ctx.cfg.degree == 1 && zm_vmult_launch_k<1>(ctx, level, prec, a)) return;
+  if (ctx.cfg.degree == 2 && zm_vmult_launch_k<2>(ctx, level, prec, a)) return;
   switch (ctx.cfg.degree) {
     case 1: vmult_launch_k<1>(ctx, level, prec, a); break;
     case 2: vmult_launch_k<2>(ctx, level, prec, a); break;

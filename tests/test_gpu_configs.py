@@ -239,3 +239,35 @@ def test_coarse_solve_k4_device_factorisation():
     ref = oracle.coarse_solve(k, b)
     got = ctx.coarse_solve(dev(b)).cpu().numpy()
     assert rel(got, ref) <= 1e-10
+
+
+def test_zmarch_operator_opt_in_matches_oracle():
+    # the opt-in z-march operator (vmult_zm.cuh, SMG_ZMARCH=1, read once per process) in a fresh
+    # interpreter: apply and residual, k = 1, 2, fp64 / fp32
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle
+import paper_2410_09497_b200 as smg
+worst64 = worst32 = 0.0
+for k, level in ((1, 3), (2, 2), (2, 3)):
+    ctx = smg.Context(k, level)
+    rng = np.random.default_rng(k + 7 * level)
+    x = rng.uniform(-1, 1, oracle.sizes(k, level)[4]); b = rng.uniform(-1, 1, x.size)
+    y_ref = oracle.apply_stokes(k, level, x)
+    r_ref = b - y_ref; r_ref[oracle.constrained_mask(k, level)] = 0.0
+    for dt in (torch.float64, torch.float32):
+        xd = torch.from_numpy(x).to("cuda", dt)
+        y = ctx.apply_stokes(level, xd).double().cpu().numpy()
+        r = ctx.residual(level, torch.from_numpy(b).to("cuda", dt), xd).double().cpu().numpy()
+        e = max(np.abs(y - y_ref).max() / np.abs(y_ref).max(), np.abs(r - r_ref).max() / np.abs(r_ref).max())
+        if dt == torch.float64: worst64 = max(worst64, e)
+        else: worst32 = max(worst32, e)
+print(worst64, worst32)
+'''
+    env = dict(os.environ, SMG_ZMARCH="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root, timeout=600)
+    assert out.returncode == 0, out.stderr
+    e64, e32 = map(float, out.stdout.strip().splitlines()[-1].split())
+    assert e64 <= 1e-12 and e32 <= 1e-5
