@@ -18,7 +18,10 @@ void dispatch(Context& ctx, int level, int prec, int colour, void* x, const void
     case 2: smooth_launch_k<2>(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1); break;
     case 3: smooth_launch_k<3>(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1); break;
     case 4: smooth_launch_k<4>(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1); break;
-    default: throw std::invalid_argument("degree not supported by the patch smoother kernel (1..4)");
+    case 5: smooth_launch_k<5>(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1); break;
+    case 6: smooth_launch_k<6>(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1); break;
+    case 7: smooth_launch_k<7>(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1); break;
+    default: throw std::invalid_argument("degree not supported by the patch smoother kernel (1..7)");
   }
 }
 

@@ -50,7 +50,9 @@ struct PD {
   static constexpr int MPI = G_ORTHT + 4 * SQO;          // M'^-1 rows          NO x R4(NO)
   static constexpr int TAB = MPI + SQO;
   static constexpr int TABP = (TAB + 3) / 4 * 4;
-  static constexpr int LINV = (3 * NV + 3) / 4 * 4;  // CTA-shared reciprocal eigenvalue sums (interior)
+  // CTA-shared reciprocal eigenvalue sums of interior patches; none for k >= 6 (the table would not fit
+  // next to the one-patch workspace, those patches divide like the boundary ones)
+  static constexpr int LINV = K >= 6 ? 0 : (3 * NV + 3) / 4 * 4;
   // per-patch workspace: Fh (3 NV) | r z d q x (5 NPR) | T1 T2 (2 BIG)
   static constexpr int WS = 3 * NV + 5 * NPR + 2 * BIG;
   static constexpr int dv(int c, int a) { return a == c ? NP : NO; }
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
   T* tab = reinterpret_cast<T*>(smem_raw);
   for (int i = threadIdx.x; i < P::TAB; i += blockDim.x) tab[i] = ptab[i];
   __syncthreads();
-  {  // reciprocal eigenvalue sums of interior patches (end variant 0 on every axis), per component
+  if constexpr (P::LINV > 0) {  // reciprocal eigenvalue sums of interior patches (end variant 0 on every axis)
     T* li = tab + P::TABP;
     for (int i = threadIdx.x; i < 3 * P::NV; i += blockDim.x) {
       const int c = i / P::NV, o = i % P::NV;
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
   ps.lane = lane;
   for (int a = 0; a < 3; ++a) ps.var[a] = 2 * (v[a] == 1) + (v[a] == m - 1);
   ps.linv = tab + P::TABP;  // CTA-shared table filled above
-  ps.interior = ps.var[0] == 0 && ps.var[1] == 0 && ps.var[2] == 0;
+  ps.interior = P::LINV > 0 && ps.var[0] == 0 && ps.var[1] == 0 && ps.var[2] == 0;
   const int n = m * H;
 
   // ---- gather R_j r: velocity blocks -> T1 -> eigen coefficients Fh_c; pressure -> Pq (= G) ----
@@ -505,11 +507,21 @@ void launch_k(Context& ctx, int level, int colour, void* x, const void* r, int z
     throw std::invalid_argument("smooth: patches need the cells on both sides of their vertex plane");
   const int npatch = cnt(colour & 1) * cnt((colour >> 1) & 1) * cnt_z;
   if (npatch <= 0) return;
-  // few patches (coarse levels): a 4- or 8-warp CTA per patch cuts the per-patch latency; many
-  // patches: one warp per patch, several per CTA
-  if (npatch <= 148) launch_group<T, K, 1, 256>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
-  else if (npatch < 148 * 8) launch_group<T, K, 1, 128>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
-  else launch_group<T, K, warps_per_cta<T, K>(), 32>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
+  if constexpr (K >= 5) {
+    // high degrees (k = 5..7): one 8-warp CTA per patch -- a patch's workspace
+    // (fp32 k = 7: 161 KB) only fits one per SM; fp64 fits up to k = 5
+    if constexpr (sizeof(T) == 8 && K >= 6)
+      throw std::invalid_argument("the fp64 patch smoother supports k <= 5: run the V-cycle in fp32 "
+                                  "(vcycle_precision = SMG_F32) for k = 6, 7");
+    else
+      launch_group<T, K, 1, 256>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
+  } else {
+    // few patches (coarse levels): a 4- or 8-warp CTA per patch cuts the per-patch latency; many
+    // patches: one warp per patch, several per CTA
+    if (npatch <= 148) launch_group<T, K, 1, 256>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
+    else if (npatch < 148 * 8) launch_group<T, K, 1, 128>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
+    else launch_group<T, K, warps_per_cta<T, K>(), 32>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
+  }
 }
 
 }  // namespace

@@ -271,3 +271,45 @@ print(worst64, worst32)
     assert out.returncode == 0, out.stderr
     e64, e32 = map(float, out.stdout.strip().splitlines()[-1].split())
     assert e64 <= 1e-12 and e32 <= 1e-5
+
+
+# ---- high degrees (k = 5..7): one CTA per patch; fp64 up to k = 5 ----
+@pytest.mark.parametrize("k,dtype,tol", [(5, torch.float64, 1e-12), (5, torch.float32, 1e-5), (6, torch.float32, 1e-5),
+                                         (7, torch.float32, 1e-5)])
+def test_smoother_high_degree_matches_oracle(k, dtype, tol):
+    level = 1
+    ctx = smg.Context(k, level, cg_max_iter=8, cg_fixed=True, cg_precond=1)
+    x0, b = rand_vec(k, level, 50), rand_vec(k, level, 51)
+    x_ref, _ = oracle.smooth(k, level, x0, b, oracle.cg_opts(8, 0.0, True, 1))
+    x = dev(x0, dtype)
+    ctx.smooth(level, x, dev(b, dtype))
+    assert rel(x.double().cpu().numpy(), x_ref) <= tol
+
+
+def test_smoother_fp64_k6_refuses():
+    ctx = smg.Context(6, 1)
+    x = ctx.new_vector(1)
+    with pytest.raises(ValueError):
+        ctx.smooth(1, x, x.clone())
+
+
+@pytest.mark.parametrize("k", [5, 7])
+def test_mg_fgmres_high_degree_converges(k):
+    # MG-FGMRES (fp32 V-cycle) at k = 5 and k = 7, level 2: the device coarse factorisation at
+    # nf = 7344 / 17152 and the one-CTA-per-patch smoother; converged residual checked with the oracle
+    level = 2
+    ctx = smg.Context(k, level, cg_max_iter=30, cg_tol=1e-5)
+    b = oracle.apply_stokes(k, level, rand_vec(k, level, 52))
+    x, it, hist = ctx.solve(level, dev(b), 1e-8, 30, smg.F32)
+    res = np.linalg.norm(b - oracle.apply_stokes(k, level, x.cpu().numpy())) / np.linalg.norm(b)
+    assert res <= 1.5e-8 and it <= 8, (it, res)
+
+
+@pytest.mark.skipif(os.environ.get("SMG_SLOW") != "1", reason="k = 5 oracle coarse pseudo-inverse takes minutes")
+def test_fgmres_k5_iterations_match_oracle():
+    k, level = 5, 1
+    ctx = smg.Context(k, level, cg_max_iter=10, cg_fixed=True)
+    b = oracle.apply_stokes(k, level, rand_vec(k, level, 53))
+    _, it_ref, _ = oracle.fgmres(k, level, b, 1e-8, 30, oracle.cg_opts(10, 0.0, True, 1))
+    _, it, _ = ctx.solve(level, dev(b), 1e-8, 30, smg.F64)
+    assert abs(it - it_ref) <= 1, (it, it_ref)
