@@ -11,7 +11,8 @@ is needed between steps. Under torchrun (N > 1) the SAME global problem is split
 per GPU (strong scaling): each step is the ghost-layer exchange over NCCL (P2P send/recv of one cell
 layer per neighbour and block) followed by the slab operator; value = global DoF / max-over-ranks
 step time. The MG solve runs on the same slabs (slab_mg: ghost exchange per smoothing colour, coarse
-levels agglomerated); the smoother DoF/s line is reported at N = 1 only.
+levels agglomerated) -- all through the C ABI's multi-GPU driver (smg_dist_*, csrc/dist.cu); the smoother
+DoF/s line is reported at N = 1 only.
 """
 import argparse
 import json
@@ -396,55 +397,57 @@ def main():
                "path": "smg_vmult_host: BlockVector host arrays (pinned), pipelined over z-chunks: H2D / vmult / D2H on three streams"}
         parallelism = "single GPU"
     else:
-        # ---- z-slab partition of the same global problem, NCCL ghost exchange per apply ----
-        from paper_2410_09497_b200 import slab
-        z0, z1 = slab.partition(level, world)[rank]
-        op = slab.SlabOperator(ctx, level, z0, z1, rank, world)
-        L = op.lay
-        xsl = L.extract(x).contiguous()
-        # correctness of the partitioned operator (exchange overlapped with the interior rows) against
-        # the whole-level operator on this rank's owned rows
-        yref = L.extract(ctx.apply_stokes(level, x))
-        ychk = op.vmult(op.new_vector(), xsl.clone())
-        err = 0.0
-        for c in range(4):
-            a_, b_ = L.owned_planes(c)
-            d = (L.block(ychk, c)[a_:b_] - L.block(yref, c)[a_:b_]).abs().max()
-            err = max(err, float(d) / max(float(yref.abs().max()), 1e-300))
+        # ---- z-slab partition of the same global problem through the C ABI's multi-GPU driver
+        #      (csrc/dist.cu: NCCL ghost exchange + slab operator, slab V-cycle and FGMRES in C++) ----
+        from paper_2410_09497_b200 import dist as sd
+        D = sd.DistContext(ctx, world, rank)
+        if args.dist_backend == "nccl":
+            D.init_nccl()
+        else:
+            D.init_torch_transport()  # gloo: host-staged callbacks (multi-rank logic runs on one GPU)
+        (z0, z1, zlo, zhi), hs = D.held(level)
+        xsl = D.extract(level, x)
+        # correctness of the partitioned operator against the whole-level operator on the owned rows
+        yref = ctx.apply_stokes(level, x)
+        ysl = torch.zeros_like(xsl)
+        D.vmult(level, ysl, xsl)
+        yfull = torch.zeros_like(yref)
+        D.insert_owned(level, yfull, ysl)
+        mask = torch.zeros_like(yref)
+        D.insert_owned(level, mask, torch.ones_like(ysl))
+        err = float(((yfull - yref) * mask).abs().max()) / max(float(yref.abs().max()), 1e-300)
         extra["slab_check_rel_err"] = max_over_ranks(err)
-        del yref, ychk
+        del yfull, mask
         if not args.no_solve:
-            # distributed MG-FGMRES: same global right-hand side, z-slab multigrid (slab_mg)
-            from paper_2410_09497_b200 import slab_mg
-            bglob = ctx.apply_stokes(level, x)
-            mg = slab_mg.SlabMG(ctx, level, slab.partition(level, world), [rank], world=world)
-            bparts = {rank: mg.slabs[rank][level].extract(bglob)}
-            del bglob
-            mg.solve(bparts, 1e-8, 30, smg.F32)  # warm-up
+            bh = D.extract(level, yref)
+            D.solve(bh, 1e-8, 30, smg.F32)  # warm-up
             barrier()
             t0 = time.perf_counter()
-            _, it, hist = mg.solve(bparts, 1e-8, 30, smg.F32)
+            _, it, hist = D.solve(bh, 1e-8, 30, smg.F32)
             torch.cuda.synchronize()
             ts = max_over_ranks(time.perf_counter() - t0)
             extra["solve"] = {"iterations": it, "rel_residual": float(hist[-1] / hist[0]), "time_s": ts,
                               "ns_per_dof": ts / N * 1e9, "tol": 1e-8,
-                              "precision": "fp64 FGMRES + fp32 V-cycle, z-slab multigrid over the ranks "
-                                           f"(agglomerated below level {mg.la + 1})"}
-        del x
+                              "precision": "fp64 FGMRES + fp32 V-cycle, z-slab multigrid in C++ (smg_dist_solve)"}
+        del yref, x
         torch.cuda.empty_cache()
-        ysl = op.new_vector()
         l0 = ctx.launch_count
-        ms, clk = timed(lambda: op.vmult(ysl, xsl), args.steps, clocks=True)
+        ms, clk = timed(lambda: D.vmult(level, ysl, xsl), args.steps, clocks=True)
         launches = (ctx.launch_count - l0) * args.steps // (args.steps + args.warmup)
-        ms_kernel, _ = timed(lambda: op.vmult(ysl, xsl, exchange=False), args.steps)
-        owned = sum((b1 - a1) * L.plane[c] for c, (a1, b1) in enumerate(L.owned_planes(c) for c in range(4)))
-        xh = torch.empty(L.total, dtype=torch.float64, pin_memory=True)
-        yh = torch.empty(L.total, dtype=torch.float64, pin_memory=True)
+        # kernel-only: the slab operator without the exchange (smg_residual_held on the owned rows)
+        from paper_2410_09497_b200 import lib, _ptr
+        ms_kernel, _ = timed(lambda: lib().smg_residual_held(ctx._h, level, smg.F64, _ptr(ysl), None, _ptr(xsl), zlo,
+                                                             zhi, z0, z1), args.steps)
+        H = k + 1
+        n_ = (2 << level) * H
+        owned = sum((z1 - z0) * H * p for p in ((n_ + 1) * n_, n_ * (n_ + 1), n_ * n_, n_ * n_))
+        xh = torch.empty(xsl.numel(), dtype=torch.float64, pin_memory=True)
+        yh = torch.empty(xsl.numel(), dtype=torch.float64, pin_memory=True)
         xh.copy_(xsl)
 
         def e2e_step():
             xsl.copy_(xh, non_blocking=True)
-            op.vmult(ysl, xsl)
+            D.vmult(level, ysl, xsl)
             yh.copy_(ysl, non_blocking=True)
             torch.cuda.current_stream().synchronize()
         for _ in range(args.warmup):
@@ -454,11 +457,12 @@ def main():
         for _ in range(args.steps):
             e2e_step()
         te = max_over_ranks((time.perf_counter() - t0) / args.steps)
-        e2e = {"value": N / te, "unit": "DoF/s", "h2d_bytes_per_step": 8 * L.total, "d2h_bytes_per_step": 8 * L.total,
-               "path": "per rank: pinned slab -> H2D -> NCCL ghost exchange -> smg_vmult_slab -> D2H"}
+        e2e = {"value": N / te, "unit": "DoF/s", "h2d_bytes_per_step": 8 * xsl.numel(),
+               "d2h_bytes_per_step": 8 * xsl.numel(),
+               "path": "per rank: pinned held slab -> H2D -> smg_dist_vmult (NCCL ghost exchange + slab operator) -> D2H"}
         extra["kernel_ms"] = ms_kernel
-        extra["slab"] = {"z_cells": [z0, z1], "owned_dofs": owned, "held_dofs": L.total}
-        parallelism = f"z-slabs x{world} (NCCL ghost exchange)"
+        extra["slab"] = {"z_cells": [z0, z1], "held_cells": [zlo, zhi], "owned_dofs": owned, "held_dofs": hs[4]}
+        parallelism = f"z-slabs x{world} (C-ABI dist driver, NCCL ghost exchange)"
     value = N / (ms * 1e-3)
 
     if rank != 0:

@@ -132,6 +132,41 @@ int smg_dot_held(smg_context* ctx, int level, int precision, const void* a, cons
 int smg_dot_slab(smg_context* ctx, int level, int precision, const void* a, const void* b, int z0, int z1,
                  double* out);
 
+/* ---- multi-GPU driver (one context per GPU / rank; z-slab partition). The C form of the
+ *      reference's seams for a partitioned mesh: fgmres(apply_A, apply_P, ...) and
+ *      v_cycle. The ghost exchange and the reductions go through NCCL
+ *      (smg_dist_init_nccl; rank 0 creates the id with smg_nccl_unique_id and the caller distributes it)
+ *      or through caller callbacks (smg_dist_init_transport: MPI, torch.distributed, ...). All traffic is
+ *      ordered on the context's stream. Distributed vectors use the HELD layout of smg_dist_held: the
+ *      owned cells [z0, z1) of the rank plus 3 ghost cell layers per interior side (zlo, zhi); only the
+ *      owned rows of inputs need to be valid. ---- */
+typedef struct {
+  /* post the given device->device messages between ranks (send[i] to rank send_peer[i], receive into
+   * recv[i] from recv_peer[i]); stream-ordered on `stream` (cudaStream_t); 0 on success */
+  int (*exchange)(void* user, int nsend, const void* const* send_ptr, const size_t* send_bytes,
+                  const int* send_peer, int nrecv, void* const* recv_ptr, const size_t* recv_bytes,
+                  const int* recv_peer, void* stream);
+  /* in-place sum over the ranks of `count` device values (precision SMG_F64 / SMG_F32) */
+  int (*allreduce_sum)(void* user, void* dev_values, size_t count, int precision, void* stream);
+  void* user;
+} smg_transport;
+int smg_nccl_unique_id(char id[128]);
+int smg_dist_init_nccl(smg_context* ctx, const char id[128], int nranks, int rank);
+int smg_dist_init_transport(smg_context* ctx, const smg_transport* transport, int nranks, int rank);
+/* owned cells [z0, z1) of `rank` on `level` (the partition every rank uses) */
+int smg_dist_partition(int level, int nranks, int rank, int* z0, int* z1);
+/* cells = {z0, z1, zlo, zhi} (owned, held) and sizes (held layout) of this rank's vectors on `level` */
+int smg_dist_held(smg_context* ctx, int level, int cells[4], int64_t sizes[5]);
+/* y = A x on the owned rows (x's ghost layers are exchanged first) */
+int smg_dist_vmult(smg_context* ctx, int level, int precision, void* y, void* x);
+/* dot over the owned rows, summed over the ranks (synchronous) */
+int smg_dist_dot(smg_context* ctx, int level, int precision, const void* a, const void* b, double* out);
+/* x = V-cycle(b) on the finest level (levels too thin to split are agglomerated and run replicated) */
+int smg_dist_vcycle(smg_context* ctx, int precision, void* x, const void* b);
+/* MG-preconditioned FGMRES over the slabs, smg_solve semantics (mass-weighted pressure mean removed) */
+int smg_dist_solve(smg_context* ctx, void* x, const void* b, double rel_tol, int max_iter, int vcycle_precision,
+                   int* iters, double* history);
+
 /* ---- BLAS-1 on level vectors (block_vector.hpp:52-93); dots accumulate in fp64 ---- */
 int smg_dot(smg_context* ctx, int level, int precision, const void* a, const void* b, double* out);
 int smg_axpy(smg_context* ctx, int level, int precision, double alpha, const void* x, void* y);

@@ -27,7 +27,9 @@ EXPORTED = [
     "smg_convert", "smg_vmult_host", "smg_vec_upload", "smg_vec_download", "smg_slab_sizes", "smg_vmult_slab",
     "smg_residual_slab", "smg_dot_slab", "smg_held_sizes", "smg_residual_held", "smg_smooth_colour_held",
     "smg_prolongate_add_held", "smg_restrict_held", "smg_dot_held", "smg_scale", "smg_subtract_from", "smg_norm",
-    "smg_project_zero_mean", "smg_pressure_node_weights", "smg_smoother_stats",
+    "smg_project_zero_mean", "smg_pressure_node_weights", "smg_smoother_stats", "smg_nccl_unique_id",
+    "smg_dist_init_nccl", "smg_dist_init_transport", "smg_dist_partition", "smg_dist_held", "smg_dist_vmult",
+    "smg_dist_dot", "smg_dist_vcycle", "smg_dist_solve",
 ]
 
 
@@ -83,6 +85,15 @@ def lib():
         L.smg_convert.argtypes = [P, I, I, P, I, P]
         L.smg_pressure_node_weights.argtypes = [I, P]
         L.smg_smoother_stats.argtypes = [P, I, P, P]
+        L.smg_nccl_unique_id.argtypes = [P]
+        L.smg_dist_init_nccl.argtypes = [P, P, I, I]
+        L.smg_dist_init_transport.argtypes = [P, P, I, I]
+        L.smg_dist_partition.argtypes = [I, I, I, P, P]
+        L.smg_dist_held.argtypes = [P, I, P, P]
+        L.smg_dist_vmult.argtypes = [P, I, I, P, P]
+        L.smg_dist_dot.argtypes = [P, I, I, P, P, ctypes.POINTER(D)]
+        L.smg_dist_vcycle.argtypes = [P, I, P, P]
+        L.smg_dist_solve.argtypes = [P, P, P, D, I, I, ctypes.POINTER(I), P]
         L.smg_scale.argtypes = [P, I, I, D, P]
         L.smg_subtract_from.argtypes = [P, I, I, P, P]
         L.smg_norm.argtypes = [P, I, I, P, ctypes.POINTER(D)]

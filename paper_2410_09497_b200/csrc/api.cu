@@ -188,9 +188,59 @@ void vcycle(Context& c, int level, int prec, void* x, const void* b) {
   smooth(c, level, prec, x, b);
 }
 
-// FGMRES, right-preconditioned, no restart, MGS + one re-orthogonalisation pass, x0 = 0
-// (SPEC.md:507-515, 549-550); the V-cycle runs in `vp` precision with conversion at its boundary
-// (SPEC.md:528).
+// V-cycle on the context's fixed work vectors (x = vx, b = vb of `level`) replayed from a CUDA graph:
+// the ~36 launches per level (8 colours x (residual + patches) x 2 steps, transfers, coarse solve) are
+// captured once per (level, precision) after a warm-up V-cycle has created every lazily built object
+// (work vectors, coarse pseudo-inverse, TMA descriptors, whose slots are then pinned), and replayed
+// with one cudaGraphLaunch. SMG_NO_GRAPH=1: plain launches.
+void vcycle_graph(Context& c, int level, int prec, void* vx, const void* vb) {
+  static const bool off = std::getenv("SMG_NO_GRAPH") != nullptr;
+  const int L = c.cfg.max_level;
+  if (c.vgraph[prec].empty()) {
+    c.vgraph[prec].assign(L + 1, nullptr);
+    c.vgraph_launches[prec].assign(L + 1, 0);
+  }
+  if (off) {
+    vcycle(c, level, prec, vx, vb);
+    return;
+  }
+  cudaGraphExec_t& ge = c.vgraph[prec][level];
+  if (!ge) {
+    vcycle(c, level, prec, vx, vb);  // warm-up: lazy set-up happens outside the capture
+    SMG_CUDA(cudaStreamSynchronize(c.stream));
+    // captured on a private stream (the caller's may be the legacy default stream, which cannot be
+    // captured); the replay below is ordered on the caller's stream
+    if (!c.s_capture) SMG_CUDA(cudaStreamCreateWithFlags(&c.s_capture, cudaStreamNonBlocking));
+    const cudaStream_t user = c.stream;
+    c.stream = c.s_capture;
+    const int64_t l0 = c.launches;
+    cudaGraph_t g = nullptr;
+    SMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      vcycle(c, level, prec, vx, vb);
+    } catch (...) {
+      cudaStreamEndCapture(c.stream, &g);
+      if (g) cudaGraphDestroy(g);
+      c.stream = user;
+      throw;
+    }
+    c.stream = user;
+    SMG_CUDA(cudaStreamEndCapture(c.s_capture, &g));
+    SMG_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    c.vgraph_launches[prec][level] = c.launches - l0;
+    if (c.tmap_pinned.size() != static_cast<size_t>(kTmapSlots)) c.tmap_pinned.assign(kTmapSlots, false);
+    for (auto& kv : c.tmap_slots) c.tmap_pinned[kv.second] = true;  // the graph holds their addresses
+    c.launches -= c.vgraph_launches[prec][level];  // counted on every replay below
+  }
+  SMG_CUDA(cudaGraphLaunch(ge, c.stream));
+  c.launches += c.vgraph_launches[prec][level];
+}
+
+// FGMRES, right-preconditioned, no restart, x0 = 0; Gram-Schmidt twice per
+// iteration as SPEC.md:550 asks (MGS + re-orthogonalisation with SMG_KRYLOV_MGS=1, else the batched
+// classical form CGS2: one host sync per iteration instead of 2(j+1)+1); the V-cycle runs in `vp`
+// precision with conversion at its boundary, replayed from a CUDA graph.
 int fgmres(Context& c, int level, double* x, const double* b, double tol, int max_iter, int vp, int* iters,
            double* hist) {
   const int64_t N = c.dev[0][level].lay.total;
@@ -214,9 +264,17 @@ int fgmres(Context& c, int level, double* x, const double* b, double tol, int ma
     if (iters) *iters = 0;
     return SMG_OK;
   }
+  if (max_iter + 1 >= kMaxKrylov) throw std::invalid_argument("max_iter exceeds the Krylov basis capacity (254)");
+  static const bool mgs = std::getenv("SMG_KRYLOV_MGS") != nullptr;
+  // basis vector i's pointer into the device pointer table (for the batched Gram-Schmidt kernels)
+  auto publish = [&](int i, const double* p) {
+    SMG_CUDA(cudaMemcpyAsync(static_cast<double**>(c.krylov_ptrs) + i, &p, sizeof(double*), cudaMemcpyHostToDevice,
+                             c.stream));
+  };
   V.push_back(newvec());
   launch_convert(c, N, SMG_F64, V[0], SMG_F64, b);
   launch_scale(c, N, SMG_F64, 1.0 / beta, V[0]);
+  publish(0, V[0]);
   g[0] = beta;
   double* w = newvec();
   bool converged = false;
@@ -230,17 +288,40 @@ int fgmres(Context& c, int level, double* x, const double* b, double tol, int ma
       vb = c.work_b[SMG_F32][level];
       vx = c.work_x[SMG_F32][level];
       launch_convert(c, N, SMG_F32, vb, SMG_F64, V[j]);
-      vcycle(c, level, SMG_F32, vx, vb);
+      vcycle_graph(c, level, SMG_F32, vx, vb);
       launch_convert(c, N, SMG_F64, Z[j], SMG_F32, vx);
     }
     launch_vmult(c, level, SMG_F64, w, Z[j], nullptr);
-    for (int pass = 0; pass < 2; ++pass)
-      for (int i = 0; i <= j; ++i) {
-        const double hij = dot(c, N, SMG_F64, w, V[i]);
-        H[i][j] += hij;
-        launch_axpy(c, N, SMG_F64, -hij, V[i], w);
-      }
-    const double wn = std::sqrt(dot(c, N, SMG_F64, w, w));
+    double wn;
+    if (mgs) {
+      // SPEC-literal (SMG_KRYLOV_MGS=1): modified Gram-Schmidt + one re-orthogonalisation pass, one
+      // host-synchronous dot per coefficient
+      for (int pass = 0; pass < 2; ++pass)
+        for (int i = 0; i <= j; ++i) {
+          const double hij = dot(c, N, SMG_F64, w, V[i]);
+          H[i][j] += hij;
+          launch_axpy(c, N, SMG_F64, -hij, V[i], w);
+        }
+      wn = std::sqrt(dot(c, N, SMG_F64, w, w));
+    } else {
+      // classical Gram-Schmidt applied twice (CGS2): all coefficients of a pass in one batched dot,
+      // the update in one kernel with the coefficients left on the device, one host sync per iteration
+      const double* const* Vd = static_cast<const double* const*>(c.krylov_ptrs);
+      double* coef = static_cast<double*>(c.krylov_coef);
+      launch_multidot(c, N, Vd, j + 1, w, coef);
+      launch_multi_axpy(c, N, Vd, j + 1, coef, w);
+      launch_multidot(c, N, Vd, j + 1, w, coef + kMaxKrylov);
+      launch_multi_axpy(c, N, Vd, j + 1, coef + kMaxKrylov, w);
+      const double* wp = w;
+      SMG_CUDA(cudaMemcpyAsync(static_cast<double**>(c.krylov_ptrs) + kMaxKrylov - 1, &wp, sizeof(double*),
+                               cudaMemcpyHostToDevice, c.stream));
+      launch_multidot(c, N, Vd + kMaxKrylov - 1, 1, w, coef + 2 * kMaxKrylov);
+      SMG_CUDA(cudaMemcpyAsync(c.krylov_host, coef, 3 * kMaxKrylov * sizeof(double), cudaMemcpyDeviceToHost,
+                               c.stream));
+      SMG_CUDA(cudaStreamSynchronize(c.stream));
+      for (int i = 0; i <= j; ++i) H[i][j] = c.krylov_host[i] + c.krylov_host[kMaxKrylov + i];
+      wn = std::sqrt(c.krylov_host[2 * kMaxKrylov]);
+    }
     H[j + 1][j] = wn;
     for (int i = 0; i < j; ++i) {
       const double t = cs[i] * H[i][j] + sn[i] * H[i + 1][j];
@@ -263,6 +344,7 @@ int fgmres(Context& c, int level, double* x, const double* b, double tol, int ma
     V.push_back(newvec());
     launch_convert(c, N, SMG_F64, V.back(), SMG_F64, w);
     launch_scale(c, N, SMG_F64, 1.0 / wn, V.back());
+    publish(static_cast<int>(V.size()) - 1, V.back());
   }
   std::vector<double> y(it, 0.0);
   for (int i = it - 1; i >= 0; --i) {
@@ -397,26 +479,10 @@ void vmult_host_pipelined(Context& c, int level, int prec, void* const y_vel[3],
   SMG_CUDA(cudaStreamSynchronize(c.stream));
 }
 
+// launches and allocations go to the context's device whatever device the caller made current
 template <class F>
 int guarded(smg_context* h, F&& f) {
-  Context* c = reinterpret_cast<Context*>(h);
-  try {
-    // launches and allocations go to the context's device whatever device the caller made current
-    if (c && c->device_ready) SMG_CUDA(cudaSetDevice(c->device));
-    return f();
-  } catch (const std::invalid_argument& e) {
-    if (c) c->last_error = e.what();
-    return SMG_EINVAL;
-  } catch (const std::bad_alloc& e) {
-    if (c) c->last_error = "out of memory";
-    return SMG_ENOMEM;
-  } catch (const not_converged& e) {
-    if (c) c->last_error = e.what();
-    return SMG_ENOTCONV;
-  } catch (const std::exception& e) {
-    if (c) c->last_error = e.what();
-    return SMG_ECUDA;
-  }
+  return guarded_call(h, std::forward<F>(f));
 }
 
 }  // namespace
@@ -443,11 +509,21 @@ void check_prec(int p) {
 
 }  // namespace
 
+// entry points of the single-GPU V-cycle for the z-slab driver (dist.cu): the replicated coarse levels
+void vcycle_level(Context& c, int level, int prec, void* x, const void* b) { vcycle(c, level, prec, x, b); }
+
 Context::~Context() {
+  if (dist) dist_destroy(dist);
+  if (dist_pw) cudaFree(dist_pw);
   if (s_in) cudaStreamDestroy(s_in);
   if (s_out) cudaStreamDestroy(s_out);
+  if (s_capture) cudaStreamDestroy(s_capture);
   for (void* p : allocations) cudaFree(p);
   if (dot_host) cudaFreeHost(dot_host);
+  if (krylov_host) cudaFreeHost(krylov_host);
+  for (auto& g : vgraph)
+    for (cudaGraphExec_t e : g)
+      if (e) cudaGraphExecDestroy(e);
 }
 
 }  // namespace smg
@@ -531,6 +607,13 @@ int smg_create(const smg_config* cfg, smg_context** out) {
     SMG_CUDA(cudaMalloc(&c->dot_partials, (smg::kDotBlocks + 8) * sizeof(double)));
     c->allocations.push_back(c->dot_partials);
     SMG_CUDA(cudaMallocHost(&c->dot_host, 64));
+    SMG_CUDA(cudaMalloc(&c->multidot_partials, smg::kDotBlocks * sizeof(double)));
+    c->allocations.push_back(c->multidot_partials);
+    SMG_CUDA(cudaMalloc(&c->krylov_ptrs, smg::kMaxKrylov * sizeof(double*)));
+    c->allocations.push_back(c->krylov_ptrs);
+    SMG_CUDA(cudaMalloc(&c->krylov_coef, 3 * smg::kMaxKrylov * sizeof(double)));
+    c->allocations.push_back(c->krylov_coef);
+    SMG_CUDA(cudaMallocHost(&c->krylov_host, 3 * smg::kMaxKrylov * sizeof(double)));
     SMG_CUDA(cudaMalloc(&c->smoother_stats, 2 * sizeof(unsigned long long)));
     c->allocations.push_back(c->smoother_stats);
     SMG_CUDA(cudaMemset(c->smoother_stats, 0, 2 * sizeof(unsigned long long)));

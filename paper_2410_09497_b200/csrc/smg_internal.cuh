@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <map>
+#include <new>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -96,6 +97,9 @@ struct TmapKey {
   }
 };
 
+struct DistState;                // dist.cu: z-slab multi-GPU state
+void dist_destroy(DistState* d);
+
 struct Context {
   smg_config cfg{};
   int device = 0;
@@ -116,21 +120,33 @@ struct Context {
   void* dot_partials = nullptr;  // double[kDotBlocks]
   void* dot_host = nullptr;      // pinned double[kDotBlocks]
   void* smoother_stats = nullptr;  // unsigned long long[2]: patches solved, inner CG iterations
+  void* multidot_partials = nullptr;  // double[kDotBlocks]: batched Gram-Schmidt partial sums
+  void* krylov_ptrs = nullptr;        // device array of the Krylov basis pointers (kMaxKrylov)
+  void* krylov_coef = nullptr;        // device double[3 kMaxKrylov]: h1 | h2 | norm^2 of an iteration
+  double* krylov_host = nullptr;      // pinned mirror of krylov_coef
   std::vector<void*> allocations;
   // per-level work vectors for the smoother / V-cycle (allocated lazily): [prec][level]
   std::vector<void*> work_r[2], work_x[2], work_b[2];
   std::vector<void*> krylov;  // FGMRES basis pool (fp64, finest-level size)
   void* pstage[2] = {nullptr, nullptr};
   void* pstage_out[2] = {nullptr, nullptr};
+  cudaStream_t s_capture = nullptr;  // private stream for CUDA-graph capture
   cudaStream_t s_in = nullptr, s_out = nullptr;  // host-path copy streams (created on first use)  // pressure staging for the BlockVector host path (finest level size)
   // TMA descriptors of input vectors (vmult.cu)
   void* tmap_dev = nullptr;
   std::map<TmapKey, int> tmap_slots;
   int tmap_next = 0;
+  std::vector<bool> tmap_pinned;  // slots referenced by captured CUDA graphs: never recycled
+  // captured V-cycle graphs: [prec][level] (smg_solve, fixed work-vector pointers)
+  std::vector<cudaGraphExec_t> vgraph[2];
+  std::vector<int64_t> vgraph_launches[2];
+  DistState* dist = nullptr;  // multi-GPU set-up (smg_dist_init_*), owned
+  void* dist_pw = nullptr;    // pressure node weights of the finest level (distributed mean projection)
   ~Context();
 };
 
 constexpr int kDotBlocks = 1184;  // 8 x 148 SMs
+constexpr int kMaxKrylov = 256;   // FGMRES basis vectors per solve (max_iter + 1)
 constexpr int kTmapSlots = 64;         // cached TMA descriptor sets (global memory)
 constexpr int kTmapSlotBytes = 512;    // 4 CUtensorMap (128 B each)
 
@@ -177,9 +193,54 @@ void launch_axpby(Context& c, int64_t n, int prec, double alpha, const void* x, 
 void launch_convert(Context& c, int64_t n, int dst_prec, void* dst, int src_prec, const void* src);
 void launch_zero(Context& c, int64_t n, int prec, void* x);
 void launch_scale(Context& c, int64_t n, int prec, double alpha, void* x);
+void launch_add_scalar(Context& c, int64_t n, int prec, double alpha, void* x);  // x += alpha
+// out_dev[i] = <V_i, w>, i < nv (fp64; V_dev: device array of nv device pointers); one launch pair
+void launch_multidot(Context& c, int64_t n, const double* const* V_dev, int nv, const double* w, double* out_dev);
+// w -= sum_i coef_dev[i] V_i
+void launch_multi_axpy(Context& c, int64_t n, const double* const* V_dev, int nv, const double* coef_dev, double* w);
 void launch_sub_pressure_mean(Context& c, int level, int prec, void* x);  // mass-weighted mean removal
 // pressure block global lexicographic <-> cell-local (BlockVector / DoFLayout order)
 void launch_pressure_permute(Context& c, int level, int prec, void* dst, const void* src, bool to_cell_local,
                              int z0 = 0, int z1 = -1, cudaStream_t stream = nullptr);
+
+// next TMA descriptor slot (round robin over the unpinned slots); the caller re-keys it
+inline int tmap_alloc_slot(Context& c) {
+  if (c.tmap_pinned.size() != static_cast<size_t>(kTmapSlots)) c.tmap_pinned.assign(kTmapSlots, false);
+  for (int tries = 0; tries < kTmapSlots; ++tries) {
+    const int slot = c.tmap_next++ % kTmapSlots;
+    if (!c.tmap_pinned[slot]) {
+      for (auto e = c.tmap_slots.begin(); e != c.tmap_slots.end();)
+        e = (e->second == slot) ? c.tmap_slots.erase(e) : std::next(e);
+      return slot;
+    }
+  }
+  throw std::runtime_error("all tensor-map slots are pinned by captured graphs");
+}
+
+// C-ABI plumbing shared by the entry-point files: map exceptions to status codes, pin the device
+template <class F>
+int guarded_call(smg_context* h, F&& f) {
+  Context* c = reinterpret_cast<Context*>(h);
+  try {
+    if (c && c->device_ready) SMG_CUDA(cudaSetDevice(c->device));
+    return f();
+  } catch (const std::invalid_argument& e) {
+    if (c) c->last_error = e.what();
+    return SMG_EINVAL;
+  } catch (const std::bad_alloc&) {
+    if (c) c->last_error = "out of memory";
+    return SMG_ENOMEM;
+  } catch (const not_converged& e) {
+    if (c) c->last_error = e.what();
+    return SMG_ENOTCONV;
+  } catch (const std::exception& e) {
+    if (c) c->last_error = e.what();
+    return SMG_ECUDA;
+  }
+}
+inline Context& context_of(smg_context* h) {
+  if (!h) throw std::invalid_argument("null context");
+  return *reinterpret_cast<Context*>(h);
+}
 
 }  // namespace smg

@@ -66,6 +66,13 @@ __global__ void scale_kernel(int64_t n, T alpha, T* __restrict__ y) {
     y[i] *= alpha;
 }
 
+template <typename T>
+__global__ void add_scalar_kernel(int64_t n, T alpha, T* __restrict__ y) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] += alpha;
+}
+
 template <typename D, typename S>
 __global__ void convert_kernel(int64_t n, D* __restrict__ dst, const S* __restrict__ src) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -117,6 +124,49 @@ __global__ void pressure_permute_kernel(T* __restrict__ dst, const T* __restrict
     const int64_t c = cell * H * H * H + ((gz % H) * H + gy % H) * H + gx % H;
     if (TO_CELL) dst[c] = src[i];
     else dst[i] = src[c];
+  }
+}
+
+// out[i] = <V_i, w> for i < nv (fp64), blockIdx.y = i: one launch + one final reduction for all the
+// Gram-Schmidt coefficients of an FGMRES iteration
+__global__ void multidot_partial_kernel(const double* const* __restrict__ V, const double* __restrict__ w, int64_t n,
+                                        double* __restrict__ partial) {
+  const double* v = V[blockIdx.y];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    s += v[i] * w[i];
+  __shared__ double red[kThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+__global__ void multidot_final_kernel(const double* __restrict__ partial, int nparts, double* __restrict__ out) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += partial[blockIdx.x * nparts + i];
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+  }
+}
+// w -= sum_i coef[i] V_i (coefficients on the device: no host round trip between the passes)
+__global__ void multi_axpy_kernel(const double* const* __restrict__ V, const double* __restrict__ coef, int nv,
+                                  int64_t n, double* __restrict__ w) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = w[i];
+    for (int j = 0; j < nv; ++j) s -= coef[j] * V[j][i];
+    w[i] = s;
   }
 }
 
@@ -178,6 +228,21 @@ double dot_ranges(Context& c, int prec, const void* a, const void* b, const int6
   return h[0];
 }
 
+void launch_multidot(Context& c, int64_t n, const double* const* V_dev, int nv, const double* w, double* out_dev) {
+  const int per = std::max(1, std::min(grid_for(n), kDotBlocks / std::max(nv, 1)));
+  double* part = static_cast<double*>(c.multidot_partials);
+  multidot_partial_kernel<<<dim3(per, nv), kThreads, 0, c.stream>>>(V_dev, w, n, part);
+  multidot_final_kernel<<<nv, 1024, 0, c.stream>>>(part, per, out_dev);
+  c.launches += 2;
+  SMG_CUDA(cudaGetLastError());
+}
+
+void launch_multi_axpy(Context& c, int64_t n, const double* const* V_dev, int nv, const double* coef_dev, double* w) {
+  multi_axpy_kernel<<<grid_for(n), kThreads, 0, c.stream>>>(V_dev, coef_dev, nv, n, w);
+  ++c.launches;
+  SMG_CUDA(cudaGetLastError());
+}
+
 void launch_axpy(Context& c, int64_t n, int prec, double alpha, const void* x, void* y) {
   if (prec == SMG_F64)
     axpy_kernel<double><<<grid_for(n), kThreads, 0, c.stream>>>(n, alpha, static_cast<const double*>(x),
@@ -206,6 +271,16 @@ void launch_scale(Context& c, int64_t n, int prec, double alpha, void* x) {
     scale_kernel<double><<<grid_for(n), kThreads, 0, c.stream>>>(n, alpha, static_cast<double*>(x));
   else
     scale_kernel<float><<<grid_for(n), kThreads, 0, c.stream>>>(n, static_cast<float>(alpha), static_cast<float*>(x));
+  ++c.launches;
+  SMG_CUDA(cudaGetLastError());
+}
+
+void launch_add_scalar(Context& c, int64_t n, int prec, double alpha, void* x) {
+  if (prec == SMG_F64)
+    add_scalar_kernel<double><<<grid_for(n), kThreads, 0, c.stream>>>(n, alpha, static_cast<double*>(x));
+  else
+    add_scalar_kernel<float><<<grid_for(n), kThreads, 0, c.stream>>>(n, static_cast<float>(alpha),
+                                                                      static_cast<float*>(x));
   ++c.launches;
   SMG_CUDA(cudaGetLastError());
 }

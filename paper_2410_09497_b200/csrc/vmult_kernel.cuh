@@ -1060,9 +1060,7 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
     const TmapKey key{a.x, level, static_cast<int>(sizeof(T)), a.zlo, a.zhi};
     auto it = ctx.tmap_slots.find(key);
     if (it == ctx.tmap_slots.end()) {
-      const int slot = ctx.tmap_next++ % kTmapSlots;
-      for (auto e = ctx.tmap_slots.begin(); e != ctx.tmap_slots.end();)
-        e = (e->second == slot) ? ctx.tmap_slots.erase(e) : std::next(e);
+      const int slot = tmap_alloc_slot(ctx);
       Maps mh = make_maps<T, K, BX, BY, BZ, OCC>(lay, static_cast<const T*>(a.x));
       char* dst = static_cast<char*>(ctx.tmap_dev) + static_cast<size_t>(slot) * kTmapSlotBytes;
       SMG_CUDA(cudaMemcpyAsync(dst, &mh, sizeof(Maps), cudaMemcpyHostToDevice, ctx.stream));

@@ -69,3 +69,13 @@ def test_blockvector_pressure_numbering(k, level):
                             i += 1
     v = np.random.default_rng(0).uniform(size=smg.level_sizes(k, level)[4])
     assert np.array_equal(smg.from_blockvector(smg.to_blockvector(v, k, level), k, level), v)
+
+
+def test_dist_partition_matches_slab_partition():
+    from paper_2410_09497_b200 import dist as sd
+    from paper_2410_09497_b200 import slab
+    for level in (2, 3, 5, 7):
+        for world in (1, 2, 3, 4, 8):
+            if (2 << level) < world:
+                continue
+            assert [sd.partition(level, world, r) for r in range(world)] == slab.partition(level, world)

@@ -313,3 +313,56 @@ def test_fgmres_k5_iterations_match_oracle():
     _, it_ref, _ = oracle.fgmres(k, level, b, 1e-8, 30, oracle.cg_opts(10, 0.0, True, 1))
     _, it, _ = ctx.solve(level, dev(b), 1e-8, 30, smg.F64)
     assert abs(it - it_ref) <= 1, (it, it_ref)
+
+
+# ---- multi-GPU driver behind the C ABI (csrc/dist.cu) ----
+def test_dist_single_rank_equals_single_gpu():
+    from paper_2410_09497_b200 import dist as sd
+    k, level = 2, 3
+    ctx = smg.Context(k, level, cg_max_iter=10, cg_fixed=True)
+    D = sd.DistContext(ctx, 1, 0).init_single()
+    b = dev(oracle.apply_stokes(k, level, rand_vec(k, level, 60)))
+    x_ref, it_ref, _ = ctx.solve(level, b, 1e-8, 30, smg.F64)
+    x, it, _ = D.solve(D.extract(level, b), 1e-8, 30, smg.F64)
+    assert it == it_ref
+    assert rel(x.cpu().numpy(), x_ref.cpu().numpy()) <= 1e-12
+    y = torch.zeros_like(b)
+    D.vmult(level, y, b.clone())
+    assert rel(y.cpu().numpy(), ctx.apply_stokes(level, b).cpu().numpy()) <= 1e-14
+
+
+def test_dist_nccl_transport_one_rank():
+    # the in-library NCCL transport (dlopen'ed libnccl) with one rank: init, all-reduce, solve
+    import torch.distributed as dist
+    from paper_2410_09497_b200 import dist as sd
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29531", rank=0, world_size=1)
+    k, level = 1, 3
+    ctx = smg.Context(k, level, cg_max_iter=10, cg_fixed=True)
+    D = sd.DistContext(ctx, 1, 0).init_nccl()
+    b = dev(oracle.apply_stokes(k, level, rand_vec(k, level, 61)))
+    x_ref, it_ref, _ = ctx.solve(level, b, 1e-8, 30, smg.F32)
+    x, it, _ = D.solve(D.extract(level, b), 1e-8, 30, smg.F32)
+    assert abs(it - it_ref) <= 1
+    assert rel(x.cpu().numpy(), x_ref.cpu().numpy()) <= 1e-6
+    assert abs(D.dot(level, D.extract(level, b), D.extract(level, b)) - float(b @ b)) <= 1e-12 * float(b @ b)
+
+
+@pytest.mark.parametrize("k,level,world", [(2, 3, 2), (1, 4, 2), (2, 4, 3)])
+def test_dist_multi_process_equals_single_gpu(k, level, world):
+    # `world` processes on one GPU, gloo transport callbacks: slab operator, slab V-cycle and FGMRES in
+    # C++ == the single-GPU results
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29540 + world + 3 * k + level),
+           os.path.join(root, "tests", "dist_worker.py"), str(k), str(level)]
+    out = subprocess.run(cmd, capture_output=True, text=True, cwd=root, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    r = json.loads(lines[-1])
+    assert r["vmult_rel"] <= 1e-14
+    assert r["f64"]["iters"] == r["f64"]["iters_single"] and r["f64"]["x_rel"] <= 1e-10
+    assert abs(r["f32"]["iters"] - r["f32"]["iters_single"]) <= 1 and r["f32"]["x_rel"] <= 1e-6
