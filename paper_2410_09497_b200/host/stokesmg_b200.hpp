@@ -249,5 +249,58 @@ inline SolveResult solve_mixed(Context& ctx, int level, DeviceVector<double>& x,
   return r;
 }
 
+// ---- multi-GPU: one Context per GPU / rank over the C ABI's z-slab driver (smg_dist_*) ----
+// The reference's seams for a partitioned mesh: DistOperator::vmult is apply_A of
+// fgmres(apply_A, apply_P, ...), DistContext::vcycle is apply_P (v_cycle SPEC.md:459-467)
+// and DistContext::solve runs the whole MG-preconditioned FGMRES over the slabs. Vectors are device
+// buffers in the held layout (held() sizes: owned cells + 3 ghost layers per interior side).
+class DistContext {
+ public:
+  // NCCL transport: rank 0 calls nccl_unique_id() and the caller distributes the 128 bytes
+  static std::vector<char> nccl_unique_id() {
+    std::vector<char> id(128);
+    check(smg_nccl_unique_id(id.data()), nullptr);
+    return id;
+  }
+  DistContext(Context& ctx, const std::vector<char>& nccl_id, int nranks, int rank) : ctx_(&ctx) {
+    if (nccl_id.size() != 128) throw std::invalid_argument("NCCL unique id must be 128 bytes");
+    check(smg_dist_init_nccl(ctx.handle(), nccl_id.data(), nranks, rank), ctx.handle());
+  }
+  // caller transport (MPI, a shared-memory mailbox, ...); `t` must stay valid while the context lives
+  DistContext(Context& ctx, const smg_transport& t, int nranks, int rank) : ctx_(&ctx) {
+    check(smg_dist_init_transport(ctx.handle(), &t, nranks, rank), ctx.handle());
+  }
+  struct Held {
+    int z0, z1, zlo, zhi;        // owned and held cells
+    std::vector<int64_t> sizes;  // block sizes of the held layout + total
+  };
+  Held held(int level) const {
+    int cells[4];
+    int64_t s[5];
+    check(smg_dist_held(ctx_->handle(), level, cells, s), ctx_->handle());
+    return Held{cells[0], cells[1], cells[2], cells[3], std::vector<int64_t>(s, s + 5)};
+  }
+  template <class T>
+  void vmult(int level, void* y, void* x) const {
+    check(smg_dist_vmult(ctx_->handle(), level, precision_of<T>(), y, x), ctx_->handle());
+  }
+  template <class T>
+  void vcycle(void* x, const void* b) const {
+    check(smg_dist_vcycle(ctx_->handle(), precision_of<T>(), x, b), ctx_->handle());
+  }
+  SolveResult solve(void* x, const void* b, double rel_tol, int max_iter, bool fp32_vcycle = true) const {
+    SolveResult r;
+    r.history.assign(static_cast<size_t>(max_iter) + 1, 0.0);
+    const int rc = smg_dist_solve(ctx_->handle(), x, b, rel_tol, max_iter, fp32_vcycle ? SMG_F32 : SMG_F64,
+                                  &r.iterations, r.history.data());
+    r.history.resize(static_cast<size_t>(r.iterations) + 1);
+    check(rc, ctx_->handle());
+    return r;
+  }
+
+ private:
+  Context* ctx_;
+};
+
 }  // namespace b200
 }  // namespace stokesmg

@@ -10,12 +10,22 @@
 
 #include "../../paper_2410_09497_b200/host/stokesmg_b200.hpp"
 
-// caller-side block vector with the reference's member layout (block_vector.hpp:15-18)
+// The reference's own BlockVector (proj/include/stokesmg/block_vector.hpp:15-93, Eigen-free) when its
+// header is on the include path (__graft_entry__.build() places it under baseline/_ref/include, git-
+// ignored, from /root/reference); otherwise a caller-side struct with the same member layout.
+#if __has_include(<stokesmg/block_vector.hpp>)
+#include <stokesmg/block_vector.hpp>
+template <int dim, class T>
+using BlockVector = stokesmg::BlockVector<dim, T>;
+static const char* kBlockVector = "reference stokesmg::BlockVector";
+#else
 template <int dim, class T>
 struct BlockVector {
   std::array<std::vector<T>, dim> velocity;
   std::vector<T> pressure;
 };
+static const char* kBlockVector = "look-alike BlockVector";
+#endif
 
 using namespace stokesmg::b200;
 
@@ -86,7 +96,13 @@ int main() {
     threw = true;
   }
   REQUIRE(threw);
-  std::printf("host wrapper ok: iterations %d, rel residual %.3e, launches %lld\n", res.iterations, rn / bn,
-              static_cast<long long>(ctx.launches()));
+  // the reference's BLAS-1 on the downloaded vectors agrees with the device dot (block_vector.hpp:53-61)
+#if __has_include(<stokesmg/block_vector.hpp>)
+  BlockVector<3, double> yd;
+  dy.download(yd);
+  REQUIRE(std::fabs(stokesmg::dot(yd, yd) - dy.dot(dy)) <= 1e-12 * dy.dot(dy));
+#endif
+  std::printf("host wrapper ok (%s): iterations %d, rel residual %.3e, launches %lld\n", kBlockVector,
+              res.iterations, rn / bn, static_cast<long long>(ctx.launches()));
   return 0;
 }

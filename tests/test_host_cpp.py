@@ -9,17 +9,33 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "tests", "cpp", "host_wrapper_check.cpp")
 BIN = os.path.join(ROOT, "tests", "cpp", "build", "host_wrapper_check")
 LIBDIR = os.path.join(ROOT, "paper_2410_09497_b200")
+# the reference's Eigen-free block_vector.hpp, placed here by __graft_entry__.build() (git-ignored)
+REF_INCLUDE = os.path.join(ROOT, "baseline", "_ref", "include")
 
 
 def build():
     os.makedirs(os.path.dirname(BIN), exist_ok=True)
-    subprocess.check_call(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"), SRC,
-                           "-L", LIBDIR, "-lsmg_b200", f"-Wl,-rpath,{LIBDIR}", "-o", BIN])
+    subprocess.check_call(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", os.path.join(ROOT, "include"),
+                           "-I", REF_INCLUDE, SRC, "-L", LIBDIR, "-lsmg_b200", f"-Wl,-rpath,{LIBDIR}", "-o", BIN])
     return BIN
+
+
+DIST_SRC = os.path.join(ROOT, "tests", "cpp", "dist_check.cpp")
+DIST_BIN = os.path.join(ROOT, "tests", "cpp", "build", "dist_check")
+
+
+def build_dist():
+    os.makedirs(os.path.dirname(DIST_BIN), exist_ok=True)
+    subprocess.check_call(["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+                           "-I", "/usr/local/cuda/include", DIST_SRC, "-L", LIBDIR, "-lsmg_b200",
+                           f"-Wl,-rpath,{LIBDIR}", "-L", "/usr/local/cuda/lib64", "-lcudart", "-lpthread",
+                           "-Wl,-rpath,/usr/local/cuda/lib64", "-o", DIST_BIN])
+    return DIST_BIN
 
 
 def test_host_wrapper_compiles_and_links():
     assert os.path.exists(build())
+    assert os.path.exists(build_dist())
 
 
 @pytest.mark.gpu
@@ -27,3 +43,14 @@ def test_host_wrapper_runs():
     out = subprocess.run([build()], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr + out.stdout
     assert "host wrapper ok" in out.stdout
+    if os.path.exists(os.path.join(REF_INCLUDE, "stokesmg", "block_vector.hpp")):
+        assert "reference stokesmg::BlockVector" in out.stdout
+
+
+@pytest.mark.gpu
+def test_dist_cpp_caller_two_ranks():
+    # two host threads = two ranks, one Context each, shared-memory transport callbacks: the C++ caller of
+    # smg_dist_solve gets the single-GPU solution
+    out = subprocess.run([build_dist()], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr + out.stdout
+    assert "dist ok" in out.stdout
