@@ -46,6 +46,8 @@ typedef struct {
   double cg_tol;     /* patch Schur-CG relative tolerance */
   int cg_fixed;      /* 1: exactly cg_max_iter iterations (parity mode) */
   int cg_precond;    /* 0: none (SPEC-literal), 1: pressure-mass preconditioned (default) */
+  int smoother_fused; /* 1: fused halo-residual patch kernel (k <= 3), 0: one residual
+                         launch per colour (default) */
 } smg_config;
 
 /* ---- context (replaces the reference's per-level setup: build_hierarchy mesh.hpp:30-36, the 1D

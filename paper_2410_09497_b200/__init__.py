@@ -36,7 +36,7 @@ EXPORTED = [
 class SmgConfig(ctypes.Structure):
     _fields_ = [("degree", ctypes.c_int), ("max_level", ctypes.c_int), ("device", ctypes.c_int),
                 ("cg_max_iter", ctypes.c_int), ("cg_tol", ctypes.c_double), ("cg_fixed", ctypes.c_int),
-                ("cg_precond", ctypes.c_int)]
+                ("cg_precond", ctypes.c_int), ("smoother_fused", ctypes.c_int)]
 
 
 class SmgError(RuntimeError):
@@ -143,10 +143,12 @@ class Context:
     float32 = SMG_F32) in the stored level layout and launch on torch's current CUDA stream.
     """
 
-    def __init__(self, degree, max_level, device=0, cg_max_iter=30, cg_tol=1e-8, cg_fixed=False, cg_precond=1):
+    def __init__(self, degree, max_level, device=0, cg_max_iter=30, cg_tol=1e-8, cg_fixed=False, cg_precond=1,
+                 smoother_fused=False):
         import torch
         self._torch = torch
-        cfg = SmgConfig(degree, max_level, device, cg_max_iter, cg_tol, int(cg_fixed), int(cg_precond))
+        cfg = SmgConfig(degree, max_level, device, cg_max_iter, cg_tol, int(cg_fixed), int(cg_precond),
+                        int(smoother_fused))
         h = ctypes.c_void_p()
         rc = lib().smg_create(ctypes.byref(cfg), ctypes.byref(h))
         if rc != SMG_OK:

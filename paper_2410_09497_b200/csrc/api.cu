@@ -161,6 +161,18 @@ void check_level(const Context& c, int level) {
 
 void smooth(Context& c, int level, int prec, void* x, const void* b) {
   ensure_work(c, prec);
+  if (c.cfg.smoother_fused && c.cfg.degree <= 3) {
+    // fused halo residual: colour c reads the snapshot buf[c % 2] and writes buf[(c+1) % 2] (a copy of
+    // the snapshot plus the colour's corrections) -- same-colour patches read each other's halos, so the
+    // snapshot stays untouched; after the 8 colours the result is back in x
+    void* buf[2] = {x, c.work_r[prec][level]};
+    const size_t bytes = static_cast<size_t>(c.dev[0][level].lay.total) * elem_size(prec);
+    for (int col = 0; col < 8; ++col) {
+      SMG_CUDA(cudaMemcpyAsync(buf[(col + 1) & 1], buf[col & 1], bytes, cudaMemcpyDeviceToDevice, c.stream));
+      launch_smooth_colour_fused(c, level, prec, col, buf[(col + 1) & 1], buf[col & 1], b);
+    }
+    return;
+  }
   void* r = c.work_r[prec][level];
   for (int col = 0; col < 8; ++col) {
     launch_vmult(c, level, prec, r, x, b);
@@ -541,6 +553,7 @@ int smg_config_default(smg_config* cfg) {
   cfg->cg_tol = 1e-8;
   cfg->cg_fixed = 0;
   cfg->cg_precond = 1;
+  cfg->smoother_fused = 0;
   return SMG_OK;
 }
 

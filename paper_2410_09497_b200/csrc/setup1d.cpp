@@ -251,6 +251,52 @@ PatchTables build_patch_tables(const LevelTables& lt) {
   }
   P.Mp = P.orth_M;
   P.Mpinv = inverse(P.Mp);
+  // global-operator rows at the patch DoFs over the patch window (fused halo residual)
+  {
+    const int nf = 2 * k + 3, n4 = 4 * no;
+    P.win_MO4 = Dense(n2, n4);
+    for (int e = 0; e < 2; ++e)
+      for (int a = 0; a < no; ++a)
+        for (int b = 0; b < no; ++b) P.win_MO4(e * no + a, (e + 1) * no + b) = C.Mo(a, b);
+    Dense Lf(nf, nf), Mf(nf, nf), Df(n2, nf);
+    for (int e = 0; e < 2; ++e) {
+      for (int a = 0; a < np; ++a)
+        for (int b = 0; b < np; ++b) {
+          Lf(e * no + a, e * no + b) += C.Kp(a, b);
+          Mf(e * no + a, e * no + b) += C.Mp(a, b);
+        }
+      for (int a = 0; a < no; ++a)
+        for (int b = 0; b < np; ++b) Df(e * no + a, e * no + b) += C.Dc(a, b);
+    }
+    for (int v = 0; v < 4; ++v) {
+      const bool lb = (v >> 1) & 1, rb = v & 1;
+      Dense& W = P.win_LO[v];
+      W = Dense(n2, n4);
+      for (int a = 0; a < no; ++a)
+        for (int b = 0; b < no; ++b) {
+          // cell v-1 (window cell 1): left neighbour (window cell 0) exists unless lb
+          if (!lb) W(a, b) = F.RL(a, b);
+          W(a, no + b) = C.Ko(a, b) + (lb ? F.NitL(a, b) : F.RR(a, b)) + F.LL(a, b);
+          W(a, 2 * no + b) = F.LR(a, b);
+          // cell v (window cell 2): right neighbour (window cell 3) exists unless rb
+          W(no + a, no + b) = F.RL(a, b);
+          W(no + a, 2 * no + b) = C.Ko(a, b) + F.RR(a, b) + (rb ? F.NitR(a, b) : F.LL(a, b));
+          if (!rb) W(no + a, 3 * no + b) = F.LR(a, b);
+        }
+      P.win_LP[v] = Dense(nf - 2, nf);
+      P.win_MP[v] = Dense(nf - 2, nf);
+      P.win_D[v] = Dense(n2, nf);
+      for (int j = 0; j < nf; ++j) {
+        const bool constrained = (j == 0 && lb) || (j == nf - 1 && rb);  // global node 0 / n
+        if (constrained) continue;
+        for (int i = 0; i < nf - 2; ++i) {
+          P.win_LP[v](i, j) = Lf(i + 1, j);
+          P.win_MP[v](i, j) = Mf(i + 1, j);
+        }
+        for (int i = 0; i < n2; ++i) P.win_D[v](i, j) = Df(i, j);
+      }
+    }
+  }
   return P;
 }
 

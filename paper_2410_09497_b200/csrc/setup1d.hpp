@@ -54,6 +54,13 @@ struct PatchTables {
   Dense Mpinv;  // its inverse (pressure-mass preconditioner of the inner CG)
   // patch matrices kept for tests / diagnostics
   Dense par_L, par_M, orth_L[4], orth_M;
+  // rows of the GLOBAL operator at the patch DoFs, restricted to the columns of the patch window
+  // (fused halo-residual smoother): per axis-position variant v = 2*left_on_boundary + right_on_boundary
+  //   win_LO[v]  (2k+2) x (4k+4)  SIPG rows of the 2 patch cells from cells v-2 .. v+1
+  //   win_MO4    (2k+2) x (4k+4)  DG mass of the 2 patch cells in the same 4-cell columns
+  //   win_LP[v], win_MP[v]  (2k+1) x (2k+3)  C0 rows of the interior nodes from the 2 cells' C0 nodes
+  //   win_D[v]   (2k+2) x (2k+3)  divergence rows; constrained (boundary-normal) columns are zero
+  Dense win_LO[4], win_MO4, win_LP[4], win_MP[4], win_D[4];
 };
 
 // Transfer: canonical embedding (fem1d.hpp:243-264)

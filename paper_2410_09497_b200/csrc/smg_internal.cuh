@@ -173,6 +173,9 @@ void launch_vmult_args_public(Context& c, int level, int prec, void* y, const vo
 // operator rows of the cells [z0, z1) of a whole-level vector (bricks restricted to that z range)
 void launch_vmult_zrange(Context& c, int level, int prec, void* y, const void* x, const void* b, int z0, int z1);
 void launch_smooth_colour(Context& c, int level, int prec, int colour, void* x, const void* r);
+// fused halo-residual colour (k <= 3): x_out (holding a copy of x_in) += corrections from b - A x_in
+void launch_smooth_colour_fused(Context& c, int level, int prec, int colour, void* x_out, const void* x_in,
+                                const void* b);
 // one colour on vectors holding the cells [zlo, zhi): patches with vertex z planes in [vz0, vz1]
 void launch_smooth_colour_held(Context& c, int level, int prec, int colour, void* x, const void* r, int zlo, int zhi,
                                int vz0, int vz1);

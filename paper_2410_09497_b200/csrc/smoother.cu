@@ -32,6 +32,16 @@ void launch_smooth_colour(Context& ctx, int level, int prec, int colour, void* x
   dispatch(ctx, level, prec, colour, x, r, 0, m, 1, m - 1);
 }
 
+void launch_smooth_colour_fused(Context& ctx, int level, int prec, int colour, void* x_out, const void* x_in,
+                                const void* b) {
+  switch (ctx.cfg.degree) {
+    case 1: smooth_fused_launch_k<1>(ctx, level, prec, colour, x_out, x_in, b); break;
+    case 2: smooth_fused_launch_k<2>(ctx, level, prec, colour, x_out, x_in, b); break;
+    case 3: smooth_fused_launch_k<3>(ctx, level, prec, colour, x_out, x_in, b); break;
+    default: throw std::invalid_argument("the fused halo-residual smoother supports k <= 3");
+  }
+}
+
 void launch_smooth_colour_held(Context& ctx, int level, int prec, int colour, void* x, const void* r, int zlo,
                                int zhi, int vz0, int vz1) {
   dispatch(ctx, level, prec, colour, x, r, zlo, zhi, vz0, vz1);
@@ -76,6 +86,15 @@ std::vector<double> pack_patch_tables(const PatchTables& P) {
   for (int v = 0; v < 4; ++v) rows(NO, NO, [&](int i, int j) { return Go[v](i, j); });
   for (int v = 0; v < 4; ++v) rows(NO, NO, [&](int i, int j) { return Go[v](j, i); });
   rows(NO, NO, [&](int i, int j) { return P.Mpinv(i, j); });
+  // fused halo-residual windows (PD<K>::WLO ...): every matrix as padded rows
+  const int NF = NP + 2, N4 = 2 * NO;
+  for (int v = 0; v < 4; ++v) rows(NO, N4, [&](int i, int j) { return P.win_LO[v](i, j); });
+  rows(NO, N4, [&](int i, int j) { return P.win_MO4(i, j); });
+  rows(NO, NO, [&](int i, int j) { return P.Mp(i, j); });
+  for (int v = 0; v < 4; ++v) rows(NP, NF, [&](int i, int j) { return P.win_LP[v](i, j); });
+  for (int v = 0; v < 4; ++v) rows(NP, NF, [&](int i, int j) { return P.win_MP[v](i, j); });
+  for (int v = 0; v < 4; ++v) rows(NO, NF, [&](int i, int j) { return P.win_D[v](i, j); });
+  rows(NP, NO, [&](int i, int j) { return P.D(j, i); });  // D^T: C0 interior rows from DG pressure
   return t;
 }
 

@@ -48,13 +48,28 @@ struct PD {
   static constexpr int G_ORTH = G_PART + NP * R4(NO);    // 4 x (M' S_orth) rows
   static constexpr int G_ORTHT = G_ORTH + 4 * SQO;       // 4 x transposed
   static constexpr int MPI = G_ORTHT + 4 * SQO;          // M'^-1 rows          NO x R4(NO)
-  static constexpr int TAB = MPI + SQO;
+  // fused halo residual (global-operator rows over the patch window, see PatchTables::win_*)
+  static constexpr int NF = NP + 2, N4 = 2 * NO;         // C0 window nodes, DG window (4 cells)
+  static constexpr int WLO = MPI + SQO;                  // 4 x SIPG window    NO x R4(N4)
+  static constexpr int WMO4 = WLO + 4 * NO * R4(N4);     // DG mass window     NO x R4(N4)
+  static constexpr int WMOO = WMO4 + NO * R4(N4);        // DG mass (own)      NO x R4(NO)
+  static constexpr int WLP = WMOO + SQO;                 // 4 x C0 stiffness   NP x R4(NF)
+  static constexpr int WMP = WLP + 4 * NP * R4(NF);      // 4 x C0 mass        NP x R4(NF)
+  static constexpr int WD = WMP + 4 * NP * R4(NF);       // 4 x divergence     NO x R4(NF)
+  static constexpr int WDT = WD + 4 * NO * R4(NF);       // D^T                NP x R4(NO)
+  static constexpr int TAB = WDT + NP * R4(NO);
   static constexpr int TABP = (TAB + 3) / 4 * 4;
   // CTA-shared reciprocal eigenvalue sums of interior patches; none for k >= 6 (the table would not fit
   // next to the one-patch workspace, those patches divide like the boundary ones)
   static constexpr int LINV = K >= 6 ? 0 : (3 * NV + 3) / 4 * 4;
   // per-patch workspace: Fh (3 NV) | r z d q x (5 NPR) | T1 T2 (2 BIG)
   static constexpr int WS = 3 * NV + 5 * NPR + 2 * BIG;
+  // fused halo residual: the window gathers and contractions run in the CG region (free before the
+  // solve), grown where needed, plus the pressure rows B u and the patch pressure (2 NPR)
+  static constexpr int SX = NF * N4 * NO, SST = NF * NO * NO;
+  static constexpr int RS = (5 * NPR + 2 * BIG) > (2 * SX + 2 * SST) ? (5 * NPR + 2 * BIG) : (2 * SX + 2 * SST);
+  static constexpr int WSF = 3 * NV + RS + 2 * NPR;
+  static_assert(SX + NV <= 5 * NPR && 2 * NPR <= SX, "fused residual scratch layout");
   static constexpr int dv(int c, int a) { return a == c ? NP : NO; }
 };
 
@@ -282,8 +297,9 @@ struct SBlocks {
   T* c[4];
 };
 
-template <typename T, int K, int W, int MINB, int GS>
+template <typename T, int K, int W, int MINB, int GS, bool FUSED>
 __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlocks<T> x, const SBlocks<const T> r,
+                                                              const SBlocks<const T> xin,
                                                               const T* __restrict__ ptab, int m, int colour,
                                                               int vz_first, int cnt_z, int cg_max_iter, T cg_tol,
                                                               int cg_fixed, int cg_precond,
@@ -314,7 +330,7 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
   if (pid >= npatch) return;
   const int v[3] = {((colour & 1) ? 1 : 2) + 2 * (pid % cnt[0]), (((colour >> 1) & 1) ? 1 : 2) + 2 * ((pid / cnt[0]) % cnt[1]),
                     vz_first + 2 * (pid / (cnt[0] * cnt[1]))};
-  T* ws = tab + P::TABP + P::LINV + warp * P::WS;
+  T* ws = tab + P::TABP + P::LINV + warp * (FUSED ? P::WSF : P::WS);
   T* Fh = ws;                // 3 x NV eigen coefficients of F_c
   T* Pr = Fh + 3 * P::NV;    // CG residual
   T* Pz = Pr + P::NPR;       // preconditioned residual
@@ -348,12 +364,92 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
   };
 #define SMG_FOR_C(...) \
   { constexpr int C = 0; __VA_ARGS__ } { constexpr int C = 1; __VA_ARGS__ } { constexpr int C = 2; __VA_ARGS__ }
-  SMG_FOR_C({
-    for (int o = lane; o < P::NV; o += GS) T1[o] = r.c[C][vel_index(C, o)];
-    gsync<GS>();
-    ps.template s3<C, true>(T1, Fh + C * P::NV, T2);
-  })
-  for (int o = lane; o < P::NPR; o += GS) Pq[o] = r.c[3][pres_index(o)];
+  if constexpr (FUSED) {
+    // ---- fused halo residual: r = b - A x_in on the patch rows, from the patch window of
+    // the snapshot x_in (cells v-2 .. v+1 across, the 2 patch cells along each component's own axis)
+    // with the global operator's rows (PatchTables::win_*); x (the output buffer) holds a copy of x_in
+    T* R = Pr;                     // contraction scratch (the CG region, free before the solve)
+    T* PB = Fh + 3 * P::NV + P::RS;  // pressure rows B x_in
+    T* PP = PB + P::NPR;           // patch pressure of x_in
+    constexpr int NF = P::NF, N4 = P::N4, NP = P::NP;
+    for (int o = lane; o < P::NPR; o += GS) PP[o] = xin.c[3][pres_index(o)];
+    SMG_FOR_C({
+      constexpr int O1 = C == 0 ? 1 : 0, O2 = C == 2 ? 1 : 2;
+      // extents per axis: along C xc, along O1 x1, along O2 x2
+      constexpr auto dm = [](int a, int xc, int x1, int x2) { return a == C ? xc : (a == O1 ? x1 : x2); };
+      int64_t gd[3] = {n, n, n};
+      gd[C] = n + 1;
+      // gather a window: along C the C0 nodes (v_C - 1) H + i, i < NF (constrained nodes 0, n read as 0);
+      // along O1 / O2 `wide` ? 4 cells from v - 2 : the 2 patch cells
+      auto gather = [&](T* dst, bool wide1, bool wide2) {
+        const int e0 = NF, e1 = wide1 ? N4 : NO, e2 = wide2 ? N4 : NO;
+        const int ext[3] = {dm(0, e0, e1, e2), dm(1, e0, e1, e2), dm(2, e0, e1, e2)};
+        int org[3];
+        for (int a = 0; a < 3; ++a)
+          org[a] = (v[a] - ((a == O1 && wide1) || (a == O2 && wide2) ? 2 : 1)) * H;
+        for (int o = lane; o < ext[0] * ext[1] * ext[2]; o += GS) {
+          const int g0 = org[0] + o % ext[0], g1 = org[1] + (o / ext[0]) % ext[1], g2 = org[2] + o / (ext[0] * ext[1]);
+          const int gc = C == 0 ? g0 : (C == 1 ? g1 : g2);
+          const bool ok = g0 >= 0 && g1 >= 0 && g2 >= 0 && g0 < gd[0] && g1 < gd[1] && g2 < gd[2] && gc != 0 && gc != n;
+          dst[o] = ok ? xin.c[C][(static_cast<int64_t>(g2) * gd[1] + g1) * gd[0] + g0] : T(0);
+        }
+        gsync<GS>();
+      };
+      constexpr int SX = P::SX, SST = P::SST;
+      T* X1 = R;
+      T* A = R + SX;
+      T* S = R + 2 * SX;
+      T* Tt = S + SST;
+      const T* wlo1 = tab + P::WLO + ps.var[O1] * NO * R4(N4);
+      const T* wlo2 = tab + P::WLO + ps.var[O2] * NO * R4(N4);
+      const T* wmo4 = tab + P::WMO4;
+      const T* wmoo = tab + P::WMOO;
+      // M_o2 (own) then M_o1 / L_o1 across: S = M_o1 M_o2 x, T = L_o1 M_o2 x
+      gather(X1, true, false);
+      warp_axis<T, dm(0, NF, N4, NO), dm(1, NF, N4, NO), dm(2, NF, N4, NO), O2, NO, GS>(X1, wmoo, A, lane);
+      gsync<GS>();
+      warp_axis<T, dm(0, NF, N4, NO), dm(1, NF, N4, NO), dm(2, NF, N4, NO), O1, NO, GS>(A, wmo4, S, lane);
+      warp_axis<T, dm(0, NF, N4, NO), dm(1, NF, N4, NO), dm(2, NF, N4, NO), O1, NO, GS>(A, wlo1, Tt, lane);
+      gsync<GS>();
+      // T += M_o1 L_o2 x (L across o2 on the own o1 rows)
+      T* X2 = R;
+      T* Bo = R + SX;
+      gather(X2, false, true);
+      warp_axis<T, dm(0, NF, NO, N4), dm(1, NF, NO, N4), dm(2, NF, NO, N4), O2, NO, GS>(X2, wlo2, Bo, lane);
+      gsync<GS>();
+      warp_axis<T, dm(0, NF, NO, NO), dm(1, NF, NO, NO), dm(2, NF, NO, NO), O1, NO, GS, true>(Bo, wmoo, Tt, lane);
+      gsync<GS>();
+      // velocity rows y = L_c S + M_c T + D_c^T M M p (interior C0 nodes along c), pressure rows += D_c S
+      T* Y = R + SX;
+      const T* wlp = tab + P::WLP + ps.var[C] * NP * R4(NF);
+      const T* wmp = tab + P::WMP + ps.var[C] * NP * R4(NF);
+      const T* wd = tab + P::WD + ps.var[C] * NO * R4(NF);
+      warp_axis<T, dm(0, NF, NO, NO), dm(1, NF, NO, NO), dm(2, NF, NO, NO), C, NP, GS>(S, wlp, Y, lane);
+      gsync<GS>();
+      warp_axis<T, dm(0, NF, NO, NO), dm(1, NF, NO, NO), dm(2, NF, NO, NO), C, NP, GS, true>(Tt, wmp, Y, lane);
+      warp_axis<T, dm(0, NF, NO, NO), dm(1, NF, NO, NO), dm(2, NF, NO, NO), C, NO, GS, (C > 0)>(S, wd, PB, lane);
+      gsync<GS>();
+      T* Q1 = R;
+      T* Q = R + P::NPR;
+      warp_axis<T, NO, NO, NO, O1, NO, GS>(PP, wmoo, Q1, lane);
+      gsync<GS>();
+      warp_axis<T, NO, NO, NO, O2, NO, GS>(Q1, wmoo, Q, lane);
+      gsync<GS>();
+      warp_axis<T, NO, NO, NO, C, NP, GS, true>(Q, tab + P::WDT, Y, lane);
+      gsync<GS>();
+      for (int o = lane; o < P::NV; o += GS) T1[o] = r.c[C][vel_index(C, o)] - Y[o];
+      gsync<GS>();
+      ps.template s3<C, true>(T1, Fh + C * P::NV, T2);
+    })
+    for (int o = lane; o < P::NPR; o += GS) Pq[o] = r.c[3][pres_index(o)] - PB[o];
+  } else {
+    SMG_FOR_C({
+      for (int o = lane; o < P::NV; o += GS) T1[o] = r.c[C][vel_index(C, o)];
+      gsync<GS>();
+      ps.template s3<C, true>(T1, Fh + C * P::NV, T2);
+    })
+    for (int o = lane; o < P::NPR; o += GS) Pq[o] = r.c[3][pres_index(o)];
+  }
   // ---- rhs = sum_c G_c Lambda_c^-1 Fh_c - G  (projected) -> Pr ----
   for (int o = lane; o < P::NPR; o += GS) Pr[o] = -Pq[o];
   gsync<GS>();
@@ -443,18 +539,19 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
 }
 
 // CTAs per SM that shared memory allows for W warp-patches per CTA (1 KB reserved per CTA)
-template <typename T, int K>
+template <typename T, int K, bool FUSED>
 constexpr int ctas_per_sm(int w) {
-  const int bytes = static_cast<int>(sizeof(T)) * (PD<K>::TABP + PD<K>::LINV + w * PD<K>::WS) + 1024;
+  const int bytes =
+      static_cast<int>(sizeof(T)) * (PD<K>::TABP + PD<K>::LINV + w * (FUSED ? PD<K>::WSF : PD<K>::WS)) + 1024;
   const int c = 233472 / bytes;
   return c > 3 ? 3 : c;  // at most 3 CTAs (the register budget caps resident warps near 24)
 }
 // warp-patches per CTA maximising the patches resident per SM (ties: fewer per CTA)
-template <typename T, int K>
+template <typename T, int K, bool FUSED>
 constexpr int warps_per_cta() {
   int best = 1, best_p = 0;
   for (int w = 1; w <= 8; ++w) {
-    const int p = w * ctas_per_sm<T, K>(w);
+    const int p = w * ctas_per_sm<T, K, FUSED>(w);
     if (p > best_p) {
       best = w;
       best_p = p;
@@ -471,19 +568,21 @@ SBlocks<T> sblocks(const LevelLayout& lay, T* v) {
   return B;
 }
 
-template <typename T, int K, int W, int GS>
+template <typename T, int K, int W, int GS, bool FUSED = false>
 void launch_group(Context& ctx, const DevLevel& dl, const LevelLayout& lay, int npatch, int colour, int vz_first,
-                  int cnt_z, void* x, const void* r) {
+                  int cnt_z, void* x, const void* r, const void* xin = nullptr) {
   using P = PD<K>;
-  const size_t smem = sizeof(T) * (P::TABP + P::LINV + W * P::WS);
+  constexpr int WSP = FUSED ? P::WSF : P::WS;
+  const size_t smem = sizeof(T) * (P::TABP + P::LINV + W * WSP);
   // as many resident CTAs as shared memory allows (up to 3): registers are capped accordingly
-  constexpr size_t smem_c = sizeof(T) * (P::TABP + P::LINV + W * P::WS) + 1024;
+  constexpr size_t smem_c = sizeof(T) * (P::TABP + P::LINV + W * WSP) + 1024;
   constexpr int MINB = smem_c * 3 <= 233472 ? 3 : (smem_c * 2 <= 233472 ? 2 : 1);
   static_assert(smem_c <= 233472, "patch workspace exceeds shared memory");
-  auto kern = patch_smooth_kernel<T, K, W, MINB, GS>;
+  auto kern = patch_smooth_kernel<T, K, W, MINB, GS, FUSED>;
   ensure_smem_attr(reinterpret_cast<const void*>(kern), ctx.device, smem);
   kern<<<(npatch + W - 1) / W, GS * W, smem, ctx.stream>>>(
-      sblocks(lay, static_cast<T*>(x)), sblocks(lay, static_cast<const T*>(r)), static_cast<const T*>(dl.patch),
+      sblocks(lay, static_cast<T*>(x)), sblocks(lay, static_cast<const T*>(r)),
+      sblocks(lay, static_cast<const T*>(xin ? xin : r)), static_cast<const T*>(dl.patch),
       dl.lay.m, colour, vz_first, cnt_z, ctx.cfg.cg_max_iter, static_cast<T>(ctx.cfg.cg_tol), ctx.cfg.cg_fixed,
       ctx.cfg.cg_precond, static_cast<unsigned long long*>(ctx.smoother_stats));
   SMG_CUDA(cudaGetLastError());
@@ -520,7 +619,30 @@ void launch_k(Context& ctx, int level, int colour, void* x, const void* r, int z
     // patches: one warp per patch, several per CTA
     if (npatch <= 148) launch_group<T, K, 1, 256>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
     else if (npatch < 148 * 8) launch_group<T, K, 1, 128>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
-    else launch_group<T, K, warps_per_cta<T, K>(), 32>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
+    else launch_group<T, K, warps_per_cta<T, K, false>(), 32>(ctx, dl, lay, npatch, colour, vf, cnt_z, x, r);
+  }
+}
+
+// fused halo-residual variant (k <= 3, whole level): x_out (a copy of x_in) += the patch corrections
+// computed from r = b - A x_in on the patch rows
+template <typename T, int K>
+void launch_fused_k(Context& ctx, int level, int colour, void* x_out, const void* x_in, const void* b) {
+  if constexpr (K > 3) {
+    throw std::invalid_argument("the fused halo-residual smoother supports k <= 3");
+  } else {
+    const DevLevel& dl = ctx.dev[sizeof(T) == 8 ? 0 : 1][level];
+    const int m = dl.lay.m;
+    const LevelLayout lay(K, level);
+    auto cnt = [&](int bit) { return bit ? m / 2 : m / 2 - 1; };
+    const int zbit = (colour >> 2) & 1;
+    const int vf = zbit ? 1 : 2, cnt_z = cnt(zbit);
+    const int npatch = cnt(colour & 1) * cnt((colour >> 1) & 1) * cnt_z;
+    if (npatch <= 0) return;
+    if (npatch <= 148) launch_group<T, K, 1, 256, true>(ctx, dl, lay, npatch, colour, vf, cnt_z, x_out, b, x_in);
+    else if (npatch < 148 * 8) launch_group<T, K, 1, 128, true>(ctx, dl, lay, npatch, colour, vf, cnt_z, x_out, b, x_in);
+    else
+      launch_group<T, K, warps_per_cta<T, K, true>(), 32, true>(ctx, dl, lay, npatch, colour, vf, cnt_z, x_out, b,
+                                                                x_in);
   }
 }
 
@@ -533,7 +655,15 @@ void smooth_launch_k(Context& ctx, int level, int prec, int colour, void* x, con
   else launch_k<float, K>(ctx, level, colour, x, r, zlo, zhi, vz0, vz1);
 }
 
-#define SMG_INSTANTIATE_SMOOTH(K) \
-  template void smooth_launch_k<K>(Context&, int, int, int, void*, const void*, int, int, int, int);
+template <int K>
+void smooth_fused_launch_k(Context& ctx, int level, int prec, int colour, void* x_out, const void* x_in,
+                           const void* b) {
+  if (prec == SMG_F64) launch_fused_k<double, K>(ctx, level, colour, x_out, x_in, b);
+  else launch_fused_k<float, K>(ctx, level, colour, x_out, x_in, b);
+}
+
+#define SMG_INSTANTIATE_SMOOTH(K)                                                                      \
+  template void smooth_launch_k<K>(Context&, int, int, int, void*, const void*, int, int, int, int); \
+  template void smooth_fused_launch_k<K>(Context&, int, int, int, void*, const void*, const void*);
 
 }  // namespace smg

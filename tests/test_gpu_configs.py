@@ -366,3 +366,36 @@ def test_dist_multi_process_equals_single_gpu(k, level, world):
     assert r["vmult_rel"] <= 1e-14
     assert r["f64"]["iters"] == r["f64"]["iters_single"] and r["f64"]["x_rel"] <= 1e-10
     assert abs(r["f32"]["iters"] - r["f32"]["iters_single"]) <= 1 and r["f32"]["x_rel"] <= 1e-6
+
+
+# ---- fused halo-residual smoother ----
+@pytest.mark.parametrize("k,level", [(1, 1), (1, 3), (2, 2), (2, 4), (3, 1), (3, 3)])
+def test_fused_halo_residual_smoother_matches_unfused_and_oracle(k, level):
+    # the patch kernel evaluates r = b - A x on the patch rows from the patch window of the colour's
+    # snapshot; equal to the global residual, so the smoothing step equals the unfused one (one residual
+    # launch per colour) to rounding, and the oracle to the north_star tolerance
+    x0, b = rand_vec(k, level, 62), rand_vec(k, level, 63)
+    out = {}
+    for fused in (False, True):
+        ctx = smg.Context(k, level, cg_max_iter=8, cg_fixed=True, cg_precond=1, smoother_fused=fused)
+        x = dev(x0)
+        ctx.smooth(level, x, dev(b))
+        out[fused] = x.cpu().numpy()
+    assert rel(out[True], out[False]) <= 1e-13
+    x_ref, _ = oracle.smooth(k, level, x0, b, oracle.cg_opts(8, 0.0, True, 1))
+    assert rel(out[True], x_ref) <= 1e-12
+    # fp32 path and the full solve with the fused smoother
+    ctx = smg.Context(k, level, cg_max_iter=8, cg_fixed=True, cg_precond=1, smoother_fused=True)
+    x = dev(x0, torch.float32)
+    ctx.smooth(level, x, dev(b, torch.float32))
+    assert rel(x.double().cpu().numpy(), x_ref) <= 1e-5
+
+
+def test_fused_smoother_solve_iterations():
+    k, level = 2, 3
+    b = dev(oracle.apply_stokes(k, level, rand_vec(k, level, 64)))
+    its = {}
+    for fused in (False, True):
+        ctx = smg.Context(k, level, cg_max_iter=30, cg_tol=1e-5, smoother_fused=fused)
+        _, its[fused], _ = ctx.solve(level, b, 1e-8, 30, smg.F32)
+    assert abs(its[True] - its[False]) <= 1
