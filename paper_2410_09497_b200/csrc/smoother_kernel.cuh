@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "smg_internal.cuh"
 #include "smoother.cuh"
@@ -90,8 +91,8 @@ struct Vec16<double> {
 // M(i,j) = A[i * R4(C) + j] (rows padded to 16 B). One pencil per lane; the coefficients of output i
 // are read as 16-byte vectors (broadcast LDS.128).
 template <typename T, int D0, int D1, int D2, int AX, int R, int GS, bool ACC = false>
-__device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __restrict__ A, T* __restrict__ out,
-                                          int lane) {
+__device__ __forceinline__ void warp_axis_fma(const T* __restrict__ in, const T* __restrict__ A, T* __restrict__ out,
+                                              int lane) {
   constexpr int DI[3] = {D0, D1, D2};
   constexpr int C = DI[AX];
   constexpr int DO0 = AX == 0 ? R : D0, DO1 = AX == 1 ? R : D1;
@@ -138,6 +139,124 @@ __device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __r
       else out[bo + i * SO] = s;
     }
   }
+}
+
+// ---- tensor-core contraction (fp32 data, warp per patch): 3xTF32 mma.sync m16n8k8 ----
+// The same contraction as warp_axis_fma as a GEMM Out(pencils x R) = In(pencils x C) A^T: m16 tiles of
+// pencils, n8 tiles of outputs, k8 steps of inputs. Each fp32 operand is split into tf32 hi + lo and
+// the product taken as hi*hi + hi*lo + lo*hi (fp32 accumulate), which keeps fp32-level accuracy
+// (the smoother parity bar is 1e-5 against the fp64 oracle). Replaces the coefficient broadcasts
+// (39 % of the FFMA kernel's shared-memory wavefronts) by two coefficient loads per lane and k step.
+// Measured (round 2): parity holds (fp32 smoother tests pass at 1e-5) but the C2 fp32 smoothing step
+// takes 26.2 ms against 18.6 ms with warp_axis_fma -- the 6x6 blocks fill 56 % of an m16n8k8 tile,
+// the split / fragment / predicate work costs more instructions than the FFMAs it replaces, and the
+// three chained MMAs per tile add latency. Off by default; build with -DSMG_SMOOTHER_MMA=1 to A/B.
+#ifndef SMG_SMOOTHER_MMA
+#define SMG_SMOOTHER_MMA 0
+#endif
+__device__ __forceinline__ unsigned to_tf32(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void split_tf32(float x, unsigned& hi, unsigned& lo) {
+  hi = to_tf32(x);
+  lo = to_tf32(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], unsigned b0, unsigned b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+template <int D0, int D1, int D2, int AX, int R, bool ACC>
+__device__ __forceinline__ void warp_axis_mma(const float* __restrict__ in, const float* __restrict__ A,
+                                              float* __restrict__ out, int lane) {
+  constexpr int DI[3] = {D0, D1, D2};
+  constexpr int C = DI[AX];
+  constexpr int DO0 = AX == 0 ? R : D0, DO1 = AX == 1 ? R : D1;
+  constexpr int SI = AX == 0 ? 1 : (AX == 1 ? D0 : D0 * D1);
+  constexpr int SO = AX == 0 ? 1 : (AX == 1 ? DO0 : DO0 * DO1);
+  constexpr int QA = AX == 0 ? D1 : D0;
+  constexpr int NPEN = D0 * D1 * D2 / C;
+  constexpr int LD = R4(C);
+  constexpr int MT = (NPEN + 15) / 16, NTL = (R + 7) / 8, KS = (C + 7) / 8;
+  const int g = lane >> 2, t = lane & 3;
+  // coefficient fragments: B[k][n] = A(n, k)
+  unsigned bh[NTL][KS][2], bl[NTL][KS][2];
+#pragma unroll
+  for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = nt * 8 + g, k = ks * 8 + t + 4 * h;
+        const float v = (n < R && k < C) ? A[n * LD + k] : 0.0f;
+        split_tf32(v, bh[nt][ks][h], bl[nt][ks][h]);
+      }
+  auto pen = [&](int p, int& bi, int& bo) {
+    const int uu = p % QA, vv = p / QA;
+    if (AX == 0) {
+      bi = (vv * D1 + uu) * D0;
+      bo = (vv * DO1 + uu) * DO0;
+    } else if (AX == 1) {
+      bi = vv * D0 * D1 + uu;
+      bo = vv * DO0 * DO1 + uu;
+    } else {
+      bi = vv * D0 + uu;
+      bo = vv * DO0 + uu;
+    }
+  };
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    const int p0 = mt * 16 + g, p1 = p0 + 8;
+    const bool a0 = p0 < NPEN, a1 = p1 < NPEN;
+    int bi0 = 0, bo0 = 0, bi1 = 0, bo1 = 0;
+    if (a0) pen(p0, bi0, bo0);
+    if (a1) pen(p1, bi1, bo1);
+    float acc[NTL][4];
+#pragma unroll
+    for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[nt][e] = 0.0f;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k0 = ks * 8 + t, k1 = k0 + 4;
+      const float x[4] = {(a0 && k0 < C) ? in[bi0 + k0 * SI] : 0.0f, (a1 && k0 < C) ? in[bi1 + k0 * SI] : 0.0f,
+                          (a0 && k1 < C) ? in[bi0 + k1 * SI] : 0.0f, (a1 && k1 < C) ? in[bi1 + k1 * SI] : 0.0f};
+      unsigned ah[4], al[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) split_tf32(x[e], ah[e], al[e]);
+#pragma unroll
+      for (int nt = 0; nt < NTL; ++nt) {
+        mma_tf32(acc[nt], al, bh[nt][ks][0], bh[nt][ks][1]);
+        mma_tf32(acc[nt], ah, bl[nt][ks][0], bl[nt][ks][1]);
+        mma_tf32(acc[nt], ah, bh[nt][ks][0], bh[nt][ks][1]);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int n = nt * 8 + 2 * t + (e & 1);
+        const bool row1 = e >= 2;
+        if (n < R && (row1 ? a1 : a0)) {
+          float* o = out + (row1 ? bo1 : bo0) + n * SO;
+          if (ACC) *o += acc[nt][e];
+          else *o = acc[nt][e];
+        }
+      }
+  }
+}
+
+template <typename T, int D0, int D1, int D2, int AX, int R, int GS, bool ACC = false>
+__device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __restrict__ A, T* __restrict__ out,
+                                          int lane) {
+  constexpr int DI[3] = {D0, D1, D2};
+  if constexpr (SMG_SMOOTHER_MMA && GS == 32 && std::is_same<T, float>::value && DI[AX] <= 16 && R <= 16)
+    warp_axis_mma<D0, D1, D2, AX, R, ACC>(in, A, out, lane);
+  else
+    warp_axis_fma<T, D0, D1, D2, AX, R, GS, ACC>(in, A, out, lane);
 }
 
 template <typename T>
