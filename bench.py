@@ -367,6 +367,19 @@ def main():
                                                "note": "whole step incl. the 8 residual launches; patch-kernel "
                                                        "flops only (bench.smoother_flops)"}}
 
+        # ---- intergrid transfer (fp32, level 5 <-> 4): restrict r_c = P^T r_f, prolongate x_f += P x_c ----
+        rc32 = torch.zeros(ctx.sizes(level - 1)[4], dtype=torch.float32, device="cuda")
+        ms_r, _ = timed(lambda: ctx.restrict(level - 1, b32, out=rc32), args.steps)
+        ms_p, _ = timed(lambda: ctx.prolongate_add(level - 1, xs, rc32), args.steps)
+        peak_gbs, _ = measured_peaks()
+        nc = ctx.sizes(level - 1)[4]
+        br, bp = 4 * (N + nc), 4 * (2 * N + nc)  # algorithmic bytes: read fine + write coarse; RMW fine + read coarse
+        extra["transfer_fp32"] = {
+            "restrict": {"ms": ms_r, "gbs": br / ms_r / 1e6, "hbm_frac": br / ms_r / 1e6 / peak_gbs,
+                         "algorithmic_bytes": br},
+            "prolongate_add": {"ms": ms_p, "gbs": bp / ms_p / 1e6, "hbm_frac": bp / ms_p / 1e6 / peak_gbs,
+                               "algorithmic_bytes": bp}}
+
         # ---- MG-FGMRES solve (mixed precision: fp64 Krylov, fp32 V-cycle) ----
         if not args.no_solve:
             b = ctx.apply_stokes(level, x)

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "smg_internal.cuh"
 
@@ -159,6 +160,197 @@ __global__ void restrict_kernel(const TBlocks<T> rc, const TBlocks<const T> rf, 
   }
 }
 
+// ---- round 2: one thread per (x cell, row) of the output, compile-time stencils ----
+// The per-DoF kernels above decoded every index with 64-bit division, looped over runtime stencil
+// extents with zero-weight branches and, for restriction, re-read up to (4H)(2H)^2 fine values per
+// coarse DoF: 3.7 % / 4.7 % of the HBM bandwidth at C2 (bench transfer_fp32, round 2). Here a thread
+// owns the 2H fine x nodes (prolongation) or the H coarse x nodes (restriction) of one coarse x cell at
+// one (y, z) row: the y / z weights are combined once per tap pair and the x contraction is shared by
+// the thread's outputs.
+template <int COMP, int H>
+struct Tap {  // 1D stencil of a fine node g (prolongation): coarse base node, row in the cell table
+  __device__ static void fine(int g, int mc, bool par, int& base, int& row) {
+    int E = g / (2 * H), r = g - 2 * H * E;
+    if (par && E == mc) {
+      E = mc - 1;
+      r = 2 * H;
+    }
+    base = E * H;
+    row = r;
+  }
+};
+
+template <typename T, int K, int COMP>
+__device__ __forceinline__ void prolong_row(const TBlocks<T>& xf, const TBlocks<const T>& xc, const T* Ec, const T* Ed,
+                                            int mc, int ex, int gy, int gz) {
+  constexpr int H = K + 1, EC_C = H + 1, ED_C = H;
+  constexpr bool PX = COMP == 0, PY = COMP == 1, PZ = COMP == 2;
+  constexpr int NX = PX ? H + 1 : H, NY = PY ? H + 1 : H, NZ = PZ ? H + 1 : H;
+  const int nc = mc * H, nf = 2 * nc;
+  const int cd0 = nc + PX, cd1 = nc + PY, fd0 = nf + PX, fd1 = nf + PY;
+  int by, ry, bz, rz;
+  Tap<COMP, H>::fine(gy, mc, PY, by, ry);
+  Tap<COMP, H>::fine(gz, mc, PZ, bz, rz);
+  const T* in = xc.c[COMP];
+  T t[NX];
+#pragma unroll
+  for (int j = 0; j < NX; ++j) t[j] = T(0);
+#pragma unroll
+  for (int jz = 0; jz < NZ; ++jz) {
+    const int cz = bz + jz;
+    T wz = PZ ? Ec[rz * EC_C + jz] : Ed[rz * ED_C + jz];
+    if (PZ && (cz == 0 || cz == nc)) wz = T(0);  // constrained coarse nodes (input ignored)
+#pragma unroll
+    for (int jy = 0; jy < NY; ++jy) {
+      const int cy = by + jy;
+      T w = wz * (PY ? Ec[ry * EC_C + jy] : Ed[ry * ED_C + jy]);
+      if (PY && (cy == 0 || cy == nc)) w = T(0);
+      const T* src = in + (static_cast<int64_t>(cz) * cd1 + cy) * cd0 + ex * H;
+#pragma unroll
+      for (int jx = 0; jx < NX; ++jx) {
+        const int cx = ex * H + jx;
+        const T v = (PX && (cx == 0 || cx == nc)) ? T(0) : src[jx];
+        t[jx] += w * v;
+      }
+    }
+  }
+  T* out = xf.c[COMP] + (static_cast<int64_t>(gz) * fd1 + gy) * fd0 + 2 * H * ex;
+  const int rows = (PX && ex == mc - 1) ? 2 * H + 1 : 2 * H;
+#pragma unroll
+  for (int r = 0; r <= 2 * H; ++r) {
+    if (r >= rows) break;
+    T s = T(0);
+#pragma unroll
+    for (int jx = 0; jx < NX; ++jx) s += (PX ? Ec[r * EC_C + jx] : Ed[r * ED_C + jx]) * t[jx];
+    const int gx = 2 * H * ex + r;
+    if (!(PX && (gx == 0 || gx == nf))) out[r] += s;
+  }
+}
+
+// fine rows of the fine cells [f0, f1) along z; grid: x = (x cell, fine y) pairs, y = fine z plane,
+// z = component
+template <typename T, int K>
+__global__ void prolongate_kernel2(const TBlocks<T> xf, const TBlocks<const T> xc, const T* __restrict__ tab, int mc,
+                                   int f0, int f1) {
+  constexpr int H = K + 1;
+  constexpr int EC_R = 2 * H + 1, EC_C = H + 1, ED_R = 2 * H, ED_C = H;
+  __shared__ T Ec[EC_R * EC_C], Ed[ED_R * ED_C];
+  for (int i = threadIdx.x; i < EC_R * EC_C; i += blockDim.x) Ec[i] = tab[i];
+  for (int i = threadIdx.x; i < ED_R * ED_C; i += blockDim.x) Ed[i] = tab[EC_R * EC_C + i];
+  __syncthreads();
+  const int comp = blockIdx.z;
+  const int nf = 2 * mc * H;
+  const int fy = nf + (comp == 1);
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= mc * fy) return;
+  const int ex = t % mc, gy = t / mc;
+  const int gz = f0 * H + blockIdx.y;
+  if (gz >= f1 * H + (comp == 2 && f1 == 2 * mc ? 1 : 0)) return;
+  switch (comp) {
+    case 0: prolong_row<T, K, 0>(xf, xc, Ec, Ed, mc, ex, gy, gz); break;
+    case 1: prolong_row<T, K, 1>(xf, xc, Ec, Ed, mc, ex, gy, gz); break;
+    case 2: prolong_row<T, K, 2>(xf, xc, Ec, Ed, mc, ex, gy, gz); break;
+    default: prolong_row<T, K, 3>(xf, xc, Ec, Ed, mc, ex, gy, gz); break;
+  }
+}
+
+template <typename T, int K, int COMP>
+__device__ __forceinline__ void restrict_row(const TBlocks<T>& rc, const TBlocks<const T>& rf, const T* Ec, const T* Ed,
+                                             int mc, int ex, int cy, int cz) {
+  constexpr int H = K + 1, EC_C = H + 1, ED_C = H;
+  constexpr bool PX = COMP == 0, PY = COMP == 1, PZ = COMP == 2;
+  constexpr int NXC = PX ? 2 : 1;  // fine x cells read (C0: the previous cell for the shared node j = 0)
+  const int nc = mc * H, nf = 2 * nc;
+  const int cd0 = nc + PX, cd1 = nc + PY, fd0 = nf + PX, fd1 = nf + PY;
+  T* out = rc.c[COMP] + (static_cast<int64_t>(cz) * cd1 + cy) * cd0 + ex * H;
+  const bool zero_row = (PY && (cy == 0 || cy == nc)) || (PZ && (cz == 0 || cz == nc));
+  // fine x rows of cell ex (and ex - 1) summed over the (y, z) taps with their combined weights
+  T acc[NXC][2 * H];
+#pragma unroll
+  for (int c = 0; c < NXC; ++c)
+#pragma unroll
+    for (int r = 0; r < 2 * H; ++r) acc[c][r] = T(0);
+  if (!zero_row) {
+    // per axis: up to two (fine cell base, local coarse index) pairs (C0: the node on a cell boundary
+    // belongs to both cells)
+    const int Ey = cy / H, jy = cy - Ey * H, Ez = cz / H, jz = cz - Ez * H;
+#pragma unroll
+    for (int pz = 0; pz < (PZ ? 2 : 1); ++pz) {
+      const int E = pz == 0 ? Ez : Ez - 1, j = pz == 0 ? jz : H;
+      if (E < 0 || E >= mc || (pz == 1 && jz != 0)) continue;
+#pragma unroll
+      for (int rz = 0; rz < 2 * H; ++rz) {
+        const T wz = PZ ? Ec[rz * EC_C + j] : Ed[rz * ED_C + j];
+        const int fz = 2 * H * E + rz;
+        if (PZ && fz == 0) continue;
+#pragma unroll
+        for (int py = 0; py < (PY ? 2 : 1); ++py) {
+          const int Ey2 = py == 0 ? Ey : Ey - 1, j2 = py == 0 ? jy : H;
+          if (Ey2 < 0 || Ey2 >= mc || (py == 1 && jy != 0)) continue;
+#pragma unroll
+          for (int ry = 0; ry < 2 * H; ++ry) {
+            const T w = wz * (PY ? Ec[ry * EC_C + j2] : Ed[ry * ED_C + j2]);
+            const int fyy = 2 * H * Ey2 + ry;
+            if (PY && fyy == 0) continue;
+            const T* src = rf.c[COMP] + (static_cast<int64_t>(fz) * fd1 + fyy) * fd0;
+#pragma unroll
+            for (int c = 0; c < NXC; ++c) {
+              const int exc = ex - c;
+              if (exc < 0) continue;
+#pragma unroll
+              for (int r = 0; r < 2 * H; ++r) {
+                const int fx = 2 * H * exc + r;
+                const T v = (PX && fx == 0) ? T(0) : src[fx];
+                acc[c][r] += w * v;
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    T s = T(0);
+#pragma unroll
+    for (int r = 0; r < 2 * H; ++r) s += (PX ? Ec[r * EC_C + j] : Ed[r * ED_C + j]) * acc[0][r];
+    if (PX && j == 0) {
+#pragma unroll
+      for (int r = 0; r < 2 * H; ++r) s += Ec[r * EC_C + H] * acc[NXC - 1][r];
+    }
+    const int gx = ex * H + j;
+    out[j] = (zero_row || (PX && gx == 0)) ? T(0) : s;
+  }
+  if (PX && ex == mc - 1) out[H] = T(0);  // constrained last coarse node x = nc
+}
+
+// coarse rows of the coarse cells [c0, c1) along z; grid: x = (x cell, coarse y) pairs, y = coarse z
+// plane, z = component
+template <typename T, int K>
+__global__ void restrict_kernel2(const TBlocks<T> rc, const TBlocks<const T> rf, const T* __restrict__ tab, int mc,
+                                 int c0, int c1) {
+  constexpr int H = K + 1;
+  constexpr int EC_R = 2 * H + 1, EC_C = H + 1, ED_R = 2 * H, ED_C = H;
+  __shared__ T Ec[EC_R * EC_C], Ed[ED_R * ED_C];
+  for (int i = threadIdx.x; i < EC_R * EC_C; i += blockDim.x) Ec[i] = tab[i];
+  for (int i = threadIdx.x; i < ED_R * ED_C; i += blockDim.x) Ed[i] = tab[EC_R * EC_C + i];
+  __syncthreads();
+  const int comp = blockIdx.z;
+  const int nc = mc * H;
+  const int cyn = nc + (comp == 1);
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= mc * cyn) return;
+  const int ex = t % mc, cy = t / mc;
+  const int cz = c0 * H + blockIdx.y;
+  if (cz >= c1 * H + (comp == 2 && c1 == mc ? 1 : 0)) return;
+  switch (comp) {
+    case 0: restrict_row<T, K, 0>(rc, rf, Ec, Ed, mc, ex, cy, cz); break;
+    case 1: restrict_row<T, K, 1>(rc, rf, Ec, Ed, mc, ex, cy, cz); break;
+    case 2: restrict_row<T, K, 2>(rc, rf, Ec, Ed, mc, ex, cy, cz); break;
+    default: restrict_row<T, K, 3>(rc, rf, Ec, Ed, mc, ex, cy, cz); break;
+  }
+}
+
 // x_free = Pinv b_free, one warp per row (level 0: at most a few thousand free DoFs)
 template <typename T>
 __global__ void coarse_kernel(T* __restrict__ x, const T* __restrict__ b, const T* __restrict__ pinv,
@@ -179,6 +371,12 @@ int grid_for(int64_t n) {
 
 // held ranges: fine vectors hold fine cells [fzlo, fzhi), coarse ones [czlo, czhi); rows computed for
 // fine cells [r0, r1) (prolongation) or coarse cells [r0, r1) (restriction)
+// A/B switch: the round-1 per-DoF kernels (SMG_LEGACY_TRANSFER=1)
+bool legacy_transfer() {
+  static const bool v = std::getenv("SMG_LEGACY_TRANSFER") != nullptr;
+  return v;
+}
+
 struct TransferRange {
   int fzlo, fzhi, czlo, czhi, r0, r1;
 };
@@ -194,20 +392,36 @@ void transfer_k(Context& ctx, int coarse_level, void* out, const void* in, bool 
     // fine cells [r0, r1) read coarse cells [r0 / 2, (r1 + 1) / 2)
     if (t.r0 < t.fzlo || t.r1 > t.fzhi || t.r0 / 2 < t.czlo || (t.r1 + 1) / 2 > t.czhi)
       throw std::invalid_argument("prolongate: held ranges do not cover the rows");
-    const int64_t rows = (static_cast<int64_t>(t.r1 - t.r0) * (K + 1) + 1) * fl.plane[0];
-    dim3 grid(grid_for(rows), 4);
-    prolongate_kernel<T, K><<<grid, kThreads, 0, ctx.stream>>>(tblocks(fl, static_cast<T*>(out)),
-                                                              tblocks(cl, static_cast<const T*>(in)),
-                                                              static_cast<const T*>(fine.transfer), mc, t.r0, t.r1);
+    const int H = K + 1, nf = 2 * mc * H;
+    const int planes = (t.r1 - t.r0) * H + 1;
+    const dim3 grid((mc * (nf + 1) + kThreads - 1) / kThreads, planes, 4);
+    if (legacy_transfer()) {
+      const int64_t rows = (static_cast<int64_t>(t.r1 - t.r0) * (K + 1) + 1) * fl.plane[0];
+      prolongate_kernel<T, K><<<dim3(grid_for(rows), 4), kThreads, 0, ctx.stream>>>(
+          tblocks(fl, static_cast<T*>(out)), tblocks(cl, static_cast<const T*>(in)),
+          static_cast<const T*>(fine.transfer), mc, t.r0, t.r1);
+    } else {
+      prolongate_kernel2<T, K><<<grid, kThreads, 0, ctx.stream>>>(tblocks(fl, static_cast<T*>(out)),
+                                                                 tblocks(cl, static_cast<const T*>(in)),
+                                                                 static_cast<const T*>(fine.transfer), mc, t.r0, t.r1);
+    }
   } else {
     // coarse cells [r0, r1) read fine cells [2 r0 - 2, 2 r1) (within the domain), see restrict_kernel
     if (t.r0 < t.czlo || t.r1 > t.czhi || std::max(2 * t.r0 - 2, 0) < t.fzlo || std::min(2 * t.r1, 2 * mc) > t.fzhi)
       throw std::invalid_argument("restrict: held ranges do not cover the rows");
-    const int64_t rows = (static_cast<int64_t>(t.r1 - t.r0) * (K + 1) + 1) * cl.plane[0];
-    dim3 grid(grid_for(rows), 4);
-    restrict_kernel<T, K><<<grid, kThreads, 0, ctx.stream>>>(tblocks(cl, static_cast<T*>(out)),
-                                                            tblocks(fl, static_cast<const T*>(in)),
-                                                            static_cast<const T*>(fine.transfer), mc, t.r0, t.r1);
+    const int H = K + 1, nc = mc * H;
+    const int planes = (t.r1 - t.r0) * H + 1;
+    const dim3 grid((mc * (nc + 1) + kThreads - 1) / kThreads, planes, 4);
+    if (legacy_transfer()) {
+      const int64_t rows = (static_cast<int64_t>(t.r1 - t.r0) * (K + 1) + 1) * cl.plane[0];
+      restrict_kernel<T, K><<<dim3(grid_for(rows), 4), kThreads, 0, ctx.stream>>>(
+          tblocks(cl, static_cast<T*>(out)), tblocks(fl, static_cast<const T*>(in)),
+          static_cast<const T*>(fine.transfer), mc, t.r0, t.r1);
+    } else {
+      restrict_kernel2<T, K><<<grid, kThreads, 0, ctx.stream>>>(tblocks(cl, static_cast<T*>(out)),
+                                                               tblocks(fl, static_cast<const T*>(in)),
+                                                               static_cast<const T*>(fine.transfer), mc, t.r0, t.r1);
+    }
   }
   SMG_CUDA(cudaGetLastError());
   ++ctx.launches;
