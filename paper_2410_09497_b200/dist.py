@@ -67,10 +67,14 @@ class DistContext:
         return self
 
     def init_torch_transport(self, group=None):
-        """callbacks over torch.distributed (host-staged: gloo on CPU, for tests and single-GPU boxes)."""
+        """callbacks over a torch.distributed group: NCCL groups move the device slices directly (zero-copy
+        tensor views of the library's buffers), gloo groups stage them through host memory (tests and
+        single-GPU boxes)."""
         import torch
         import torch.distributed as dist
         cr = _cudart()
+        if dist.get_backend(group) == "nccl":
+            return self._init_torch_nccl_transport(group)
 
         def exchange(user, nsend, sp, sb, speer, nrecv, rp, rb, rpeer, stream):
             try:
@@ -109,6 +113,49 @@ class DistContext:
 
         tr = Transport(EXCHANGE_FN(exchange), ALLREDUCE_FN(allreduce), None)
         self._keep = (tr, exchange, allreduce)  # the callbacks must outlive the context
+        self.ctx._check(lib().smg_dist_init_transport(self.ctx._h, ctypes.byref(tr), self.nranks, self.rank))
+        return self
+
+    def _init_torch_nccl_transport(self, group):
+        import torch
+        import torch.distributed as dist
+        cr = _cudart()
+        dev = self.ctx.device
+
+        class _View:  # __cuda_array_interface__ over a raw device pointer: torch views it without a copy
+            def __init__(self, ptr, nbytes, typestr="|u1", itemsize=1):
+                self.__cuda_array_interface__ = {"shape": (nbytes // itemsize,), "typestr": typestr,
+                                                 "data": (int(ptr), False), "version": 3}
+
+        def view(ptr, nbytes, typestr="|u1", itemsize=1):
+            return torch.as_tensor(_View(ptr, nbytes, typestr, itemsize), device=f"cuda:{dev}")
+
+        def exchange(user, nsend, sp, sb, speer, nrecv, rp, rb, rpeer, stream):
+            try:
+                cr.cudaStreamSynchronize(stream)
+                ops = [dist.P2POp(dist.isend, view(sp[i], sb[i]), int(speer[i]), group) for i in range(nsend)]
+                ops += [dist.P2POp(dist.irecv, view(rp[i], rb[i]), int(rpeer[i]), group) for i in range(nrecv)]
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+                torch.cuda.current_stream(dev).synchronize()
+                return 0
+            except Exception as e:  # noqa: BLE001
+                print("exchange callback failed:", e)
+                return 1
+
+        def allreduce(user, ptr, count, prec, stream):
+            try:
+                cr.cudaStreamSynchronize(stream)
+                t = view(ptr, count * (8 if prec == F64 else 4), "<f8" if prec == F64 else "<f4", 8 if prec == F64 else 4)
+                dist.all_reduce(t, group=group)
+                torch.cuda.current_stream(dev).synchronize()
+                return 0
+            except Exception as e:  # noqa: BLE001
+                print("allreduce callback failed:", e)
+                return 1
+
+        tr = Transport(EXCHANGE_FN(exchange), ALLREDUCE_FN(allreduce), None)
+        self._keep = (tr, exchange, allreduce)
         self.ctx._check(lib().smg_dist_init_transport(self.ctx._h, ctypes.byref(tr), self.nranks, self.rank))
         return self
 
