@@ -390,6 +390,7 @@ class Context:
         if any(xs[i].size != s[i] for i in range(4)):
             raise ValueError("block sizes do not match the level layout")
         v = out if out is not None else self.new_vector(level, dtype)
+        self._vec(v, level, prec)
         vel = (ctypes.c_void_p * 3)(*[a.ctypes.data for a in xs[:3]])
         self._sync_stream()
         self._check(lib().smg_vec_upload(self._h, level, prec, _ptr(v), vel, ctypes.c_void_p(xs[3].ctypes.data)))
@@ -397,7 +398,7 @@ class Context:
 
     def download(self, level, v):
         """device level vector -> BlockVector host blocks (pressure cell-local)."""
-        prec = self._prec(v)
+        prec = self._vec(v, level)
         dt = np.float64 if prec == F64 else np.float32
         s = self.sizes(level)
         ys = [np.empty(s[i], dtype=dt) for i in range(4)]

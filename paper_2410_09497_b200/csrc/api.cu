@@ -420,11 +420,12 @@ void vmult_host_pipelined(Context& c, int level, int prec, void* const y_vel[3],
     SMG_CUDA(cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking));
     SMG_CUDA(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking));
   }
-  // chunks of 4k cells (every brick depth divides 4), at most 16
+  // z-chunks of at least 2 cells (a chunk that is not a multiple of the kernel's brick depth runs a
+  // masked partial brick); SMG_HOST_CHUNKS overrides the target count
   const int m = lay.m;
   int nch_target = 16;
   if (const char* e = std::getenv("SMG_HOST_CHUNKS")) nch_target = std::max(1, std::atoi(e));
-  int chunk = std::max(4, (m / nch_target) / 4 * 4);
+  int chunk = std::max(2, m / nch_target);
   if (m < 8) chunk = m;
   const int nchunk = (m + chunk - 1) / chunk;
   std::vector<cudaEvent_t> ev_in(nchunk), ev_comp(nchunk);
