@@ -220,3 +220,76 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def run_padded(c, UX, PC, pad_a1, pad_b1):
+    """pass 1 of component c with the o1 item extent padded to pad_a1 (A1) / pad_b1 (B1) lanes (C = 1, 2);
+    returns (wavefronts, warp load/store instructions) of pass 1"""
+    lc, lo1h = LC(c), LO1H(c)
+    No1 = N(O1(c))
+    NO2 = B(O2(c))
+    UY = LC(1) if c == 1 else N(1) + 2 * H
+    US = UX if c == 2 else UX * UY
+    tot = [0, 0]
+
+    def ub(ci, oi):
+        return ci * UX + oi if c == 1 else ci * UY * UX + oi
+
+    def acc(fn, n_items):
+        for base in range(0, n_items, 32):
+            lanes = [base + l if base + l < n_items else None for l in range(32)]
+            for addrs in fn(lanes):
+                if all(a is None for a in addrs):
+                    continue
+                tot[0] += wavefronts(addrs)
+                tot[1] += 1
+
+    P1 = pad_a1
+    NLA = lc * P1
+
+    def a1(lanes):
+        out = []
+        for j in range(2 * S1 * H):
+            ad = []
+            for it in lanes:
+                if it is None:
+                    ad.append(None)
+                    continue
+                e2 = (it // NLA) * S1
+                r = it % NLA
+                ci, oi = r // P1, r % P1
+                if oi >= lo1h:
+                    ad.append(None)
+                    continue
+                if j < S1 * H:
+                    ad.append(ub(ci, oi) + (e2 + 1) * H * US + j * US)
+                else:
+                    ad.append(((e2 * H + j - S1 * H) * lo1h + oi) * PC + ci)
+            out.append(ad)
+        return out
+    acc(a1, NLA * (NO2 // S1))
+    P2 = pad_b1
+    NLB = lc * P2
+
+    def b1(lanes):
+        out = []
+        for j in range((S1 + 2) * H + S1 * H):
+            ad = []
+            for it in lanes:
+                if it is None:
+                    ad.append(None)
+                    continue
+                e2 = (it // NLB) * S1
+                r = it % NLB
+                ci, o = r // P2, r % P2
+                if o >= No1:
+                    ad.append(None)
+                    continue
+                if j < (S1 + 2) * H:
+                    ad.append(ub(ci, o + H) + e2 * H * US + j * US)
+                else:
+                    ad.append(((e2 * H + j - (S1 + 2) * H) * No1 + o) * PC + ci)
+            out.append(ad)
+        return out
+    acc(b1, NLB * (NO2 // S1))
+    return tot
