@@ -227,6 +227,8 @@ void vcycle_graph(Context& c, int level, int prec, void* vx, const void* vb) {
     c.stream = c.s_capture;
     const int64_t l0 = c.launches;
     cudaGraph_t g = nullptr;
+    c.tmap_recorded.clear();
+    c.tmap_recording = true;
     SMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
     try {
       vcycle(c, level, prec, vx, vb);
@@ -234,15 +236,17 @@ void vcycle_graph(Context& c, int level, int prec, void* vx, const void* vb) {
       cudaStreamEndCapture(c.stream, &g);
       if (g) cudaGraphDestroy(g);
       c.stream = user;
+      c.tmap_recording = false;
       throw;
     }
     c.stream = user;
+    c.tmap_recording = false;
     SMG_CUDA(cudaStreamEndCapture(c.s_capture, &g));
     SMG_CUDA(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
     c.vgraph_launches[prec][level] = c.launches - l0;
     if (c.tmap_pinned.size() != static_cast<size_t>(kTmapSlots)) c.tmap_pinned.assign(kTmapSlots, false);
-    for (auto& kv : c.tmap_slots) c.tmap_pinned[kv.second] = true;  // the graph holds their addresses
+    for (int slot : c.tmap_recorded) c.tmap_pinned[slot] = true;  // the graph holds their addresses
     c.launches -= c.vgraph_launches[prec][level];  // counted on every replay below
   }
   SMG_CUDA(cudaGraphLaunch(ge, c.stream));

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <map>
+#include <set>
 #include <new>
 #include <memory>
 #include <stdexcept>
@@ -137,6 +138,8 @@ struct Context {
   std::map<TmapKey, int> tmap_slots;
   int tmap_next = 0;
   std::vector<bool> tmap_pinned;  // slots referenced by captured CUDA graphs: never recycled
+  bool tmap_recording = false;    // during a graph capture: collect the slots the captured kernels use
+  std::set<int> tmap_recorded;
   // captured V-cycle graphs: [prec][level] (smg_solve, fixed work-vector pointers)
   std::vector<cudaGraphExec_t> vgraph[2];
   std::vector<int64_t> vgraph_launches[2];

@@ -1069,6 +1069,7 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
     }
     dmaps = reinterpret_cast<const Maps*>(static_cast<char*>(ctx.tmap_dev) +
                                           static_cast<size_t>(it->second) * kTmapSlotBytes);
+    if (ctx.tmap_recording) ctx.tmap_recorded.insert(it->second);  // referenced by a graph being captured
   }
   static_assert(sizeof(Maps) <= kTmapSlotBytes, "tensor-map slot too small");
   auto go = [&](auto kern) {

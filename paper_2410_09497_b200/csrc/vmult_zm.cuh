@@ -816,6 +816,7 @@ void launch(Context& ctx, int level, const VmultArgs& a) {
   static_assert(sizeof(zm::ZMaps) <= kTmapSlotBytes, "tensor-map slot too small");
   const zm::ZMaps* dmaps =
       reinterpret_cast<const zm::ZMaps*>(static_cast<char*>(ctx.tmap_dev) + static_cast<size_t>(it->second) * kTmapSlotBytes);
+  if (ctx.tmap_recording) ctx.tmap_recorded.insert(it->second);
   const int units = (m / S::TX) * (m / S::TY) * (a.z1 - a.z0);
   const dim3 grid(std::min(units, S::OCC * ctx.num_sms));
   auto go = [&](auto kern) {

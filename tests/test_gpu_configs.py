@@ -399,3 +399,18 @@ def test_fused_smoother_solve_iterations():
         ctx = smg.Context(k, level, cg_max_iter=30, cg_tol=1e-5, smoother_fused=fused)
         _, its[fused], _ = ctx.solve(level, b, 1e-8, 30, smg.F32)
     assert abs(its[True] - its[False]) <= 1
+
+
+def test_graph_captured_vcycle_survives_tensor_map_recycling():
+    # the solve replays a captured V-cycle whose kernels hold tensor-map slot addresses: recycling the
+    # other slots (70 applies on distinct vectors) must not change the next solve
+    k, level = 2, 3
+    ctx = smg.Context(k, level, cg_max_iter=30, cg_tol=1e-5)
+    b = dev(oracle.apply_stokes(k, level, rand_vec(k, level, 65)))
+    x1, it1, _ = ctx.solve(level, b, 1e-8, 30, smg.F32)
+    vecs = [torch.rand_like(b) for _ in range(70)]
+    for v in vecs:
+        ctx.apply_stokes(level, v)
+    x2, it2, _ = ctx.solve(level, b, 1e-8, 30, smg.F32)
+    assert it1 == it2
+    assert rel(x2.cpu().numpy(), x1.cpu().numpy()) <= 1e-12
