@@ -92,7 +92,7 @@ struct Vec16<double> {
 // are read as 16-byte vectors (broadcast LDS.128).
 template <typename T, int D0, int D1, int D2, int AX, int R, int GS, bool ACC = false>
 __device__ __forceinline__ void warp_axis_fma(const T* __restrict__ in, const T* __restrict__ A, T* __restrict__ out,
-                                              int lane) {
+                                              int lane, const T* __restrict__ scale = nullptr) {
   constexpr int DI[3] = {D0, D1, D2};
   constexpr int C = DI[AX];
   constexpr int DO0 = AX == 0 ? R : D0, DO1 = AX == 1 ? R : D1;
@@ -118,6 +118,10 @@ __device__ __forceinline__ void warp_axis_fma(const T* __restrict__ in, const T*
     T x[NVR * NV];
 #pragma unroll
     for (int j = 0; j < NVR * NV; ++j) x[j] = j < C ? in[bi + j * SI] : T(0);
+    if (scale) {  // elementwise input scaling folded into the load (the interior patches' Lambda^-1)
+#pragma unroll
+      for (int j = 0; j < C; ++j) x[j] *= scale[bi + j * SI];
+    }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const V* Ai = reinterpret_cast<const V*>(A + i * LD);
@@ -251,12 +255,14 @@ __device__ __forceinline__ void warp_axis_mma(const float* __restrict__ in, cons
 
 template <typename T, int D0, int D1, int D2, int AX, int R, int GS, bool ACC = false>
 __device__ __forceinline__ void warp_axis(const T* __restrict__ in, const T* __restrict__ A, T* __restrict__ out,
-                                          int lane) {
+                                          int lane, const T* __restrict__ scale = nullptr) {
   constexpr int DI[3] = {D0, D1, D2};
-  if constexpr (SMG_SMOOTHER_MMA && GS == 32 && std::is_same<T, float>::value && DI[AX] <= 16 && R <= 16)
+  if constexpr (SMG_SMOOTHER_MMA && GS == 32 && std::is_same<T, float>::value && DI[AX] <= 16 && R <= 16) {
+    (void)scale;  // (the MMA path is only built without the scaled callers)
     warp_axis_mma<D0, D1, D2, AX, R, ACC>(in, A, out, lane);
-  else
-    warp_axis_fma<T, D0, D1, D2, AX, R, GS, ACC>(in, A, out, lane);
+  } else {
+    warp_axis_fma<T, D0, D1, D2, AX, R, GS, ACC>(in, A, out, lane, scale);
+  }
 }
 
 template <typename T>
@@ -352,11 +358,12 @@ struct Patch {
   }
   // eigen space of component C -> pressure: out = (G0 (x) G1 (x) G2) in
   // acc (=|+=) (G0 (x) G1 (x) G2) in; s1, s2 scratch
+  // scale (optional): in is multiplied elementwise on load (Lambda_C^-1 of interior patches)
   template <int C, bool ACC>
-  __device__ void g3acc(const T* in, T* acc, T* s1, T* s2) const {
+  __device__ void g3acc(const T* in, T* acc, T* s1, T* s2, const T* scale = nullptr) const {
     constexpr int NO = P::NO;
     constexpr int A0 = P::dv(C, 0), A1 = P::dv(C, 1), A2 = P::dv(C, 2);
-    warp_axis<T, A0, A1, A2, 0, NO, GS>(in, G(C, 0, false), s1, lane);
+    warp_axis<T, A0, A1, A2, 0, NO, GS>(in, G(C, 0, false), s1, lane, scale);
     gsync<GS>();
     warp_axis<T, NO, A1, A2, 1, NO, GS>(s1, G(C, 1, false), s2, lane);
     gsync<GS>();
@@ -614,15 +621,17 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
     // component 0, then 1 and 2 sharing their first contraction (x0 kept in Pz, which is free here:
     // it is recomputed by the preconditioner below)
     ps.template gt3<0>(Pd, T1, T2);
-    ps.template lam_inv<0>(T1);
-    ps.template g3acc<0, false>(T1, Pq, T2, T1);
+    // Lambda_C^-1: folded into the first contraction of g3acc for interior patches (its table is
+    // CTA-shared), a separate pass (division) for boundary patches
+    if (!ps.interior) ps.template lam_inv<0>(T1);
+    ps.template g3acc<0, false>(T1, Pq, T2, T1, ps.interior ? ps.linv : nullptr);
     ps.gt3_axis0_orth(Pd, Pz);
     ps.template gt3_from_axis0<1>(Pz, T1, T2);
-    ps.template lam_inv<1>(T1);
-    ps.template g3acc<1, true>(T1, Pq, T2, T1);
+    if (!ps.interior) ps.template lam_inv<1>(T1);
+    ps.template g3acc<1, true>(T1, Pq, T2, T1, ps.interior ? ps.linv + P::NV : nullptr);
     ps.template gt3_from_axis0<2>(Pz, T1, T2);
-    ps.template lam_inv<2>(T1);
-    ps.template g3acc<2, true>(T1, Pq, T2, T1);
+    if (!ps.interior) ps.template lam_inv<2>(T1);
+    ps.template g3acc<2, true>(T1, Pq, T2, T1, ps.interior ? ps.linv + 2 * P::NV : nullptr);
     const T dq = ps.dot(Pd, Pq);
     if (!(dq > T(0)) || rz == T(0)) break;
     const T alpha = rz / dq;
