@@ -5,7 +5,9 @@ import time
 import numpy as np
 import torch
 
-import paper_2410_09497_b200 as smg
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2410_09497_b200 as smg  # noqa: E402
 
 k, level = 2, 5
 ctx = smg.Context(k, level)
