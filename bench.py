@@ -367,6 +367,15 @@ def main():
                                                "note": "whole step incl. the 8 residual launches; patch-kernel "
                                                        "flops only (bench.smoother_flops)"}}
 
+        # the smoothing step with the loose inner tolerance the tuned solve uses (FGMRES iterations unchanged)
+        ctx_l = smg.Context(k, level, device=local, cg_max_iter=30, cg_tol=1e-2, cg_fixed=False, cg_precond=1)
+        ctx_l.smoother_stats(reset=True)
+        ms_sl, _ = timed(lambda: ctx_l.smooth(level, xs, b32, zero_init=True), sm_steps)
+        npl, cgl = ctx_l.smoother_stats(reset=True)
+        extra["smoother_fp32_inner_cg_tol_1e-2"] = {"value": N / (ms_sl * 1e-3), "unit": "DoF/s", "ms_per_step": ms_sl,
+                                                    "mean_inner_cg_iterations": cgl / max(npl, 1)}
+        del ctx_l
+
         # ---- intergrid transfer (fp32, level 5 <-> 4): restrict r_c = P^T r_f, prolongate x_f += P x_c ----
         rc32 = torch.zeros(ctx.sizes(level - 1)[4], dtype=torch.float32, device="cuda")
         ms_r, _ = timed(lambda: ctx.restrict(level - 1, b32, out=rc32), args.steps)
