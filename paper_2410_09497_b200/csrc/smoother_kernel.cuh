@@ -59,6 +59,9 @@ struct PD {
   static constexpr int WD = WMP + 4 * NP * R4(NF);       // 4 x divergence     NO x R4(NF)
   static constexpr int WDT = WD + 4 * NO * R4(NF);       // D^T                NP x R4(NO)
   static constexpr int TAB = WDT + NP * R4(NO);
+  // the unfused kernel stages only the tables up to the fused-residual windows
+  static constexpr int TAB0 = WLO, TABP0 = (TAB0 + 3) / 4 * 4;
+  static constexpr int tabp(bool fused) { return fused ? TABP : TABP0; }
   static constexpr int TABP = (TAB + 3) / 4 * 4;
   // CTA-shared reciprocal eigenvalue sums of interior patches; none for k >= 6 (the table would not fit
   // next to the one-patch workspace, those patches divide like the boundary ones)
@@ -434,10 +437,11 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
   constexpr int H = K + 1, NO = P::NO;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tab = reinterpret_cast<T*>(smem_raw);
-  for (int i = threadIdx.x; i < P::TAB; i += blockDim.x) tab[i] = ptab[i];
+  constexpr int TABPF = P::tabp(FUSED);
+  for (int i = threadIdx.x; i < (FUSED ? P::TAB : P::TAB0); i += blockDim.x) tab[i] = ptab[i];
   __syncthreads();
   if constexpr (P::LINV > 0) {  // reciprocal eigenvalue sums of interior patches (end variant 0 on every axis)
-    T* li = tab + P::TABP;
+    T* li = tab + TABPF;
     for (int i = threadIdx.x; i < 3 * P::NV; i += blockDim.x) {
       const int c = i / P::NV, o = i % P::NV;
       const int A0 = P::dv(c, 0), A1 = P::dv(c, 1);
@@ -456,7 +460,7 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
   if (pid >= npatch) return;
   const int v[3] = {((colour & 1) ? 1 : 2) + 2 * (pid % cnt[0]), (((colour >> 1) & 1) ? 1 : 2) + 2 * ((pid / cnt[0]) % cnt[1]),
                     vz_first + 2 * (pid / (cnt[0] * cnt[1]))};
-  T* ws = tab + P::TABP + P::LINV + warp * (FUSED ? P::WSF : P::WS);
+  T* ws = tab + TABPF + P::LINV + warp * (FUSED ? P::WSF : P::WS);
   T* Fh = ws;                // 3 x NV eigen coefficients of F_c
   T* Pr = Fh + 3 * P::NV;    // CG residual
   T* Pz = Pr + P::NPR;       // preconditioned residual
@@ -470,7 +474,7 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
   ps.tab = tab;
   ps.lane = lane;
   for (int a = 0; a < 3; ++a) ps.var[a] = 2 * (v[a] == 1) + (v[a] == m - 1);
-  ps.linv = tab + P::TABP;  // CTA-shared table filled above
+  ps.linv = tab + TABPF;  // CTA-shared table filled above
   ps.interior = P::LINV > 0 && ps.var[0] == 0 && ps.var[1] == 0 && ps.var[2] == 0;
   const int n = m * H;
 
@@ -670,16 +674,20 @@ __global__ void __launch_bounds__(GS * W, MINB) patch_smooth_kernel(const SBlock
 template <typename T, int K, bool FUSED>
 constexpr int ctas_per_sm(int w) {
   const int bytes =
-      static_cast<int>(sizeof(T)) * (PD<K>::TABP + PD<K>::LINV + w * (FUSED ? PD<K>::WSF : PD<K>::WS)) + 1024;
+      static_cast<int>(sizeof(T)) * (PD<K>::tabp(FUSED) + PD<K>::LINV + w * (FUSED ? PD<K>::WSF : PD<K>::WS)) + 1024;
   const int c = 233472 / bytes;
-  return c > 3 ? 3 : c;  // at most 3 CTAs (the register budget caps resident warps near 24)
+  return c > 3 ? 3 : c;
 }
 // warp-patches per CTA maximising the patches resident per SM (ties: fewer per CTA)
 template <typename T, int K, bool FUSED>
 constexpr int warps_per_cta() {
   int best = 1, best_p = 0;
+  // at most 24 resident warp-patches (~85 registers per thread). 26 (13 per CTA, 2 CTAs, 78 registers)
+  // measured: level-4 step of C2 2.80 vs 3.05 ms (one wave for 3600-3840 patches), level 5 18.35 vs
+  // 18.11 ms, V-cycle unchanged -- not adopted
   for (int w = 1; w <= 8; ++w) {
-    const int p = w * ctas_per_sm<T, K, FUSED>(w);
+    const int c = ctas_per_sm<T, K, FUSED>(w);
+    const int p = w * c > 24 ? 0 : w * c;
     if (p > best_p) {
       best = w;
       best_p = p;
@@ -701,9 +709,9 @@ void launch_group(Context& ctx, const DevLevel& dl, const LevelLayout& lay, int 
                   int cnt_z, void* x, const void* r, const void* xin = nullptr) {
   using P = PD<K>;
   constexpr int WSP = FUSED ? P::WSF : P::WS;
-  const size_t smem = sizeof(T) * (P::TABP + P::LINV + W * WSP);
+  const size_t smem = sizeof(T) * (P::tabp(FUSED) + P::LINV + W * WSP);
   // as many resident CTAs as shared memory allows (up to 3): registers are capped accordingly
-  constexpr size_t smem_c = sizeof(T) * (P::TABP + P::LINV + W * WSP) + 1024;
+  constexpr size_t smem_c = sizeof(T) * (P::tabp(FUSED) + P::LINV + W * WSP) + 1024;
   constexpr int MINB = smem_c * 3 <= 233472 ? 3 : (smem_c * 2 <= 233472 ? 2 : 1);
   static_assert(smem_c <= 233472, "patch workspace exceeds shared memory");
   auto kern = patch_smooth_kernel<T, K, W, MINB, GS, FUSED>;
