@@ -104,7 +104,12 @@ struct DistState {
   std::vector<void*> x[2], r[2], b[2], full[2], fullx[2];
   std::vector<void*> krylov;  // fp64 finest held vectors (FGMRES basis)
   double* dscal = nullptr;    // device scratch for reductions
+  cudaGraphExec_t vgraph[2] = {nullptr, nullptr};  // captured finest-level V-cycle per precision (NCCL)
+  int64_t vgraph_launches[2] = {0, 0};
+  bool graph_failed = false;
   ~DistState() {
+    for (cudaGraphExec_t& e : vgraph)
+      if (e) cudaGraphExecDestroy(e);
     if (use_nccl && comm) nccl().CommDestroy(comm);
     for (int p = 0; p < 2; ++p)
       for (auto* v : {&x[p], &r[p], &b[p], &full[p], &fullx[p]})
@@ -378,6 +383,58 @@ void project_mean(Context& c, int prec, void* x) {
   launch_add_scalar(c, lay.size[3], prec, -mean, static_cast<char*>(x) + lay.off[3] * es);  // every held row
 }
 
+// The finest-level fp32 V-cycle on the fixed work vectors, replayed from a CUDA graph when the
+// transport is the in-library NCCL (its send / recv / all-reduce are stream-ordered and captured with
+// the kernels); caller callbacks run on the host and cannot be captured, so they take plain launches.
+// A failed capture (e.g. an NCCL build without graph support) falls back to plain launches for good.
+void vcycle_maybe_graph(Context& c, int prec, void* vx, const void* vb) {
+  DistState& D = dist(c);
+  static const bool off = std::getenv("SMG_NO_GRAPH") != nullptr;
+  if (off || !D.use_nccl || D.graph_failed) {
+    vcycle(c, D.L, prec, vx, vb);
+    return;
+  }
+  if (!D.vgraph[prec]) {
+    vcycle(c, D.L, prec, vx, vb);  // warm-up: lazy set-up outside the capture
+    SMG_CUDA(cudaStreamSynchronize(c.stream));
+    if (!c.s_capture) SMG_CUDA(cudaStreamCreateWithFlags(&c.s_capture, cudaStreamNonBlocking));
+    const cudaStream_t user = c.stream;
+    c.stream = c.s_capture;
+    c.tmap_recorded.clear();
+    c.tmap_recording = true;
+    const int64_t l0 = c.launches;
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      try {
+        vcycle(c, D.L, prec, vx, vb);
+      } catch (...) {
+        ok = false;
+      }
+      ok = (cudaStreamEndCapture(c.stream, &g) == cudaSuccess) && ok && g;
+    }
+    c.stream = user;
+    c.tmap_recording = false;
+    if (ok && cudaGraphInstantiate(&D.vgraph[prec], g, 0) == cudaSuccess) {
+      D.vgraph_launches[prec] = c.launches - l0;
+      if (c.tmap_pinned.size() != static_cast<size_t>(kTmapSlots)) c.tmap_pinned.assign(kTmapSlots, false);
+      for (int slot : c.tmap_recorded) c.tmap_pinned[slot] = true;
+    } else {
+      D.vgraph[prec] = nullptr;
+      D.graph_failed = true;
+      cudaGetLastError();  // clear a sticky capture error
+    }
+    if (g) cudaGraphDestroy(g);
+    c.launches = l0;
+    if (D.graph_failed) {
+      vcycle(c, D.L, prec, vx, vb);
+      return;
+    }
+  }
+  SMG_CUDA(cudaGraphLaunch(D.vgraph[prec], c.stream));
+  c.launches += D.vgraph_launches[prec];
+}
+
 int fgmres(Context& c, double* x, const double* b, double tol, int max_iter, int vp, int* iters, double* hist) {
   DistState& D = dist(c);
   const int L = D.L;
@@ -417,7 +474,7 @@ int fgmres(Context& c, double* x, const double* b, double tol, int max_iter, int
       void* vb = D.b[SMG_F32][L];
       void* vx = D.x[SMG_F32][L];
       launch_convert(c, N, SMG_F32, vb, SMG_F64, V[j]);
-      vcycle(c, L, SMG_F32, vx, vb);
+      vcycle_maybe_graph(c, SMG_F32, vx, vb);
       launch_convert(c, N, SMG_F64, Z[j], SMG_F32, vx);
     }
     vmult(c, L, SMG_F64, w, Z[j]);
