@@ -159,7 +159,8 @@ void check_level(const Context& c, int level) {
   if (level < 0 || level > c.cfg.max_level) throw std::invalid_argument("level out of range");
 }
 
-void smooth(Context& c, int level, int prec, void* x, const void* b) {
+// x_zero: x is known to be 0 (pre-smoothing on descent), so colour 0's residual is b itself
+void smooth(Context& c, int level, int prec, void* x, const void* b, bool x_zero = false) {
   ensure_work(c, prec);
   if (c.cfg.smoother_fused && c.cfg.degree <= 3) {
     // fused halo residual: colour c reads the snapshot buf[c % 2] and writes buf[(c+1) % 2] (a copy of
@@ -175,6 +176,10 @@ void smooth(Context& c, int level, int prec, void* x, const void* b) {
   }
   void* r = c.work_r[prec][level];
   for (int col = 0; col < 8; ++col) {
+    if (col == 0 && x_zero) {  // r = b - A 0 on the patch rows (the gather reads patch DoFs only)
+      launch_smooth_colour(c, level, prec, col, x, b);
+      continue;
+    }
     launch_vmult(c, level, prec, r, x, b);
     launch_smooth_colour(c, level, prec, col, x, r);
   }
@@ -189,7 +194,7 @@ void vcycle(Context& c, int level, int prec, void* x, const void* b) {
   ensure_work(c, prec);
   const int64_t N = c.dev[0][level].lay.total;
   launch_zero(c, N, prec, x);
-  smooth(c, level, prec, x, b);
+  smooth(c, level, prec, x, b, /*x_zero=*/true);
   void* r = c.work_r[prec][level];
   void* bc = c.work_b[prec][level - 1];
   void* xc = c.work_x[prec][level - 1];
@@ -717,7 +722,7 @@ int smg_smooth(smg_context* h, int level, int precision, void* x, const void* b,
     smg::check_prec(precision);
     if (level < 1) throw std::invalid_argument("smooth: level 0 uses the coarse solver (SPEC.md:71)");
     if (zero_init) smg::launch_zero(c, c.dev[0][level].lay.total, precision, x);
-    smg::smooth(c, level, precision, x, b);
+    smg::smooth(c, level, precision, x, b, zero_init != 0);
     return SMG_OK;
   });
 }
