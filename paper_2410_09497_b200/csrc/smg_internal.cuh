@@ -151,7 +151,7 @@ struct Context {
 constexpr int kDotBlocks = 1184;  // 8 x 148 SMs
 constexpr int kMaxKrylov = 256;   // FGMRES basis vectors per solve (max_iter + 1)
 constexpr int kTmapSlots = 64;         // cached TMA descriptor sets (global memory)
-constexpr int kTmapSlotBytes = 512;    // 4 CUtensorMap (128 B each)
+constexpr int kTmapSlotBytes = 1024;   // up to 8 CUtensorMap (128 B each)
 
 size_t elem_size(int precision);
 

@@ -111,7 +111,12 @@ struct Brick {
   static constexpr int UX(int c) { return rup(XEXT(c) + VEC - 1); }
   static constexpr int UY(int c) { return c == 0 ? LO1H(0) : (c == 1 ? LC(1) : LO2H(2)); }
   static constexpr int UZ(int c) { return c == 2 ? LC(2) : LO2H(c); }
-  static constexpr int sizeU(int c) { return UX(c) * UY(c) * UZ(c); }  // bytes loaded by one TMA box
+  // u_x rows have the odd pitch n+1, so the rows y = q (mod VEC) form VEC tensors with a 16-B aligned
+  // pitch VEC (n+1) (make_maps): the u_x box is staged as VEC sub-boxes, sub-box s holding the rows
+  // y0 + s + VEC i (i < UYS) of every z plane, each sub-box 128-B aligned
+  static constexpr int UYS = (LO1H(0) + VEC - 1) / VEC;
+  static constexpr int SUB0 = rupa(UX(0) * UYS * UZ(0));
+  static constexpr int sizeU(int c) { return c == 0 ? VEC * SUB0 : UX(c) * UY(c) * UZ(c); }  // elements staged
   static constexpr int sizeA1(int c) { return N(O2(c)) * LO1H(c) * PC(c); }
   static constexpr int sizeST(int c) { return N(O2(c)) * N(O1(c)) * PC(c); }
   static constexpr int mx3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
@@ -152,7 +157,8 @@ struct Brick {
 };
 
 struct Maps {
-  CUtensorMap u0, u1, u2, p;  // u0 unused (u_x rows are bulk copies); 3D boxes of u_y, u_z, p
+  CUtensorMap u1, u2, p;  // 3D boxes of u_y, u_z, p
+  CUtensorMap u0[4];      // u_x rows y = q (mod VEC), q < VEC (Brick::SUB0)
 };
 
 // per-block base pointers [u_x, u_y, u_z, p] in the GLOBAL index space of the level: for a z-slab
@@ -235,11 +241,17 @@ __device__ __forceinline__ int brick_shift(const Geo& G, int H) {
   const int x0 = G.g0[0] - H;
   return PADF + x0 - max(floor_to(x0, VEC), 0);
 }
-// u_x rows: the 1D start (z n + y)(n+1) + x0 has the same residue mod VEC for every z (n % VEC == 0)
-template <typename T>
-__device__ __forceinline__ int row_shift0(const Geo& G, int H, int y) {
+// u_x box: smem offset of the element (x = x0 = g0x - H, local row oi, plane 0). Row oi lives in
+// sub-box s = oi % VEC (row i = oi / VEC), loaded from the map of rows y = q (mod VEC),
+// q = (y0 + s) mod VEC, whose x coordinate is x' = x + q; the box starts at xs = max(floor16B(x0 + q), 0)
+template <typename T, int SUB0, int UX>
+__device__ __forceinline__ int u0_row(const Geo& G, int H, int oi) {
   constexpr int VEC = 16 / static_cast<int>(sizeof(T));
-  return (y * (G.n + 1) + G.g0[0] - H) & (VEC - 1);  // non-negative residue (power-of-two VEC)
+  constexpr int PADF = 128 / static_cast<int>(sizeof(T));
+  const int s = oi & (VEC - 1);
+  const int q = (G.g0[1] - H + s) & (VEC - 1);
+  const int x0 = G.g0[0] - H;
+  return PADF + s * SUB0 + (oi / VEC) * UX + x0 + q - max(floor_to(x0 + q, VEC), 0);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -255,32 +267,21 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
   const int tid = threadIdx.x;
   if constexpr (TMA) {
     if constexpr (C == 0) {
-      // one bulk copy per x-row inside the domain (rows have the odd pitch n+1, so no tensor map);
-      // every warp issues its share of the rows and arrives once on the U barrier (initialised with
-      // NT/32 arrivals) with its bytes; rows outside the domain are zero-filled directly. A row may
-      // read past the end of u_x into u_y (same allocation); those columns are zeroed by fix_columns.
-      {
-        const int y0 = G.g0[1] - H, z0 = G.g0[2] - H;
-        unsigned bytes = 0;
-        for (int r = tid; r < UY * UZ; r += NT) {
-          const int y = y0 + r % UY, z = z0 + r / UY;
-          T* dst = sU + r * UX;
-          if (y >= 0 && y < n && z >= G.zoff && z < G.zend) {
-            const int64_t start = (static_cast<int64_t>(z) * n + y) * (n + 1) + G.g0[0] - H;
-            const int64_t sal = start & -static_cast<int64_t>(BR::VEC);  // floor to a 16-B boundary
-            // rows at y = 0 must not reach back into plane z - 1 (for a slab, that plane may not be held)
-            const int64_t row0 = static_cast<int64_t>(z) * n * (n + 1);
-            const int64_t ss = (y == 0 && sal < row0) ? row0 : sal;
-            const unsigned nb = static_cast<unsigned>((UX - (ss - sal)) * sizeof(T));
-            bulk_load(dst + (ss - sal), X.c[0] + ss, nb, bar);
-            bytes += nb;
-          } else {
+      // VEC sub-boxes from the row-residue maps u0[q] (Brick::SUB0); rows / planes outside the domain
+      // are OOB-filled with zeros, the columns x <= 0 and x >= n are zeroed by fix_columns
+      if (tid == 0) {
+        constexpr int VEC = BR::VEC;
+        mbar_expect(bar, static_cast<unsigned>(VEC * UX * BR::UYS * UZ * sizeof(T)));
+        const int y0 = G.g0[1] - H, x0 = G.g0[0] - H, zc = G.g0[2] - H - G.zoff;
 #pragma unroll
-            for (int i = 0; i < UX; ++i) dst[i] = T(0);
-          }
+        for (int s = 0; s < VEC; ++s) {
+          const int q = (y0 + s) & (VEC - 1);
+          // rows y0 + s + VEC i = VEC (j0 + i) + q of map q (exact: y0 + s - q is a multiple of VEC)
+          const int j0 = (y0 + s - q) / VEC;
+          tma_load_3d(sU + BR::PADF + s * BR::SUB0, &M.u0[q], max(floor_to(x0 + q, VEC), 0), j0, zc, bar);
         }
-        bytes = __reduce_add_sync(0xffffffffu, bytes);
-        if ((tid & 31) == 0) mbar_expect(bar, bytes);  // arrive + expect_tx after the copies: tx may go negative first
+      } else if ((tid & 31) == 0) {
+        mbar_arrive(bar);  // the U barriers count one arrival per warp
       }
     } else {
       if (tid == 0) {
@@ -304,8 +305,9 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
       bool ok = g[0] >= 0 && g[1] >= 0 && g[2] >= 0 && g[0] < gd[0] && g[1] < gd[1] && g[2] < gd[2];
       ok = ok && g[C] != 0 && g[C] != n && g[2] >= G.zoff && g[2] < G.zend + (C == 2);
       const T* src = ok ? xc + (static_cast<int64_t>(g[2]) * gd[1] + g[1]) * gd[0] + g[0] : xc;
-      const int sh = C == 0 ? row_shift0<T>(G, H, g[1]) : brick_shift<T>(G, H);
-      cp_async_elem(sU + (i / XE) * UX + sh + (l[0] + H), src, ok);
+      T* dst = C == 0 ? sU + u0_row<T, BR::SUB0, UX>(G, H, l[1] + H) + (l[2] + H) * BR::UYS * UX
+                      : sU + (i / XE) * UX + brick_shift<T>(G, H);
+      cp_async_elem(dst + (l[0] + H), src, ok);
     }
   }
 }
@@ -335,9 +337,21 @@ __device__ __forceinline__ void issue_p(T* sP, uint64_t* bar, const Blocks<const
   }
 }
 
+// CTA-uniform: does fix_columns write anything for these boxes? (interior bricks skip it and the barrier
+// after it: every thread waits on the box's mbarrier itself, so the TMA data needs no CTA barrier)
+template <typename T, int K, int BX, int BY, int BZ, int OCC>
+__device__ __forceinline__ bool fix_needed(bool u0, bool u2, const Geo& G) {
+  using BR = Brick<T, K, BX, BY, BZ, OCC>;
+  constexpr int H = K + 1;
+  const int x0 = G.g0[0] - H, zb = G.g0[2] - H;
+  if (x0 < 0) return true;
+  if (u0 && !(x0 > 0 && x0 + BR::XEXT(0) <= G.n)) return true;
+  return u2 && (zb <= 0 || zb + BR::UZ(2) > G.n);
+}
+
 // Boundary fix-ups after a TMA box landed (bricks touching the x ends only):
-//  - u_x rows are rank-1 copies that ignore the row structure: zero the columns outside [1, n-1]
-//    (halo beyond the domain and the constrained boundary-normal nodes x = 0, x = n);
+//  - u_x rows (row-residue maps: the x < 0 columns of a row are the previous row's tail): zero the
+//    columns outside [1, n-1] (halo beyond the domain and the constrained boundary-normal nodes x = 0, x = n);
 //  - u_y, u_z, p boxes clamped at x = 0 leave the x < 0 halo columns unwritten: zero them.
 template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT>
 __device__ __forceinline__ void fix_columns(T* sU0, T* sU1, T* sU2, T* sP, const Geo& G) {
@@ -363,7 +377,7 @@ __device__ __forceinline__ void fix_columns(T* sU0, T* sU1, T* sU2, T* sP, const
     for (int i = threadIdx.x; i < ROWS * per; i += NT) {
       const int r = i / per, j = i - r * per;
       const int col = j < nl ? j : hi + (j - nl);
-      sU0[r * BR::UX(0) + row_shift0<T>(G, H, G.g0[1] - H + r % UY) + col] = T(0);
+      sU0[u0_row<T, BR::SUB0, BR::UX(0)>(G, H, r % UY) + (r / UY) * BR::UYS * BR::UX(0) + col] = T(0);
     }
   }
   if (x0 >= 0) return;
@@ -497,25 +511,24 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
     if (TMA) {
       mbar_wait(barU, *phU);
       *phU ^= 1;
+      if (fix_needed<T, K, BX, BY, BZ, OCC>(C == 0, C == 2, G)) {
+        fix_columns<T, K, BX, BY, BZ, OCC, NT>(C == 0 ? sU : nullptr, C == 1 ? sU : nullptr, C == 2 ? sU : nullptr,
+                                               nullptr, G);
+        __syncthreads();
+      }
     } else {
       cp_async_commit();
       cp_async_wait<0>();
-    }
-    __syncthreads();
-    if (TMA) {
-      fix_columns<T, K, BX, BY, BZ, OCC, NT>(C == 0 ? sU : nullptr, C == 1 ? sU : nullptr, C == 2 ? sU : nullptr,
-                                             nullptr, G);
       __syncthreads();
     }
   }
   // ---- pass 1 (along o2): A1 = M_o2 U (c full, o1 with halo, o2 owned); B1 = L_o2 U (o1 owned) ----
   {
-    constexpr int US = C == 2 ? UX : UX * UY;  // staged-box stride along o2
+    constexpr int US = C == 2 ? UX : (C == 0 ? UX * BR::UYS : UX * UY);  // staged-box stride along o2
     const int bsh = brick_shift<T>(G, H);
     // element (c = ci, o1 = oi, o2 = 0) of the staged box
     auto ub = [&](int ci, int oi) {
-      return C == 0 ? oi * UX + ci + row_shift0<T>(G, H, G.g0[1] - H + oi)
-                    : (C == 1 ? ci * UX + oi : ci * UY * UX + oi) + bsh;
+      return C == 0 ? u0_row<T, BR::SUB0, UX>(G, H, oi) + ci : (C == 1 ? ci * UX + oi : ci * UY * UX + oi) + bsh;
     };
     constexpr int NLA = LC * LO1H;
     for (int it = tid; it < NLA * (NO2 / S1); it += NT) {
@@ -862,13 +875,16 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
       if (TMA) {
         mbar_wait(&bars[2], phP);
         phP ^= 1;
-        __syncthreads();
-        fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, nullptr, nullptr, sP, G);
+        if (fix_needed<T, K, BX, BY, BZ, OCC>(false, false, G)) {
+          __syncthreads();
+          fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, nullptr, nullptr, sP, G);
+          __syncthreads();
+        }
       } else {
         cp_async_commit();
         cp_async_wait<0>();
+        __syncthreads();
       }
-      __syncthreads();
       component<T, K, BX, BY, BZ, OCC, NT, 0, RESID, TMA>(sm, sm, G, h, nullptr, X, Y, B, maps, &bars[2], &bars[0],
                                                           &ph[0], 1, &G);
       component<T, K, BX, BY, BZ, OCC, NT, 1, RESID, TMA>(sm, sm, G, h, nullptr, X, Y, B, maps, &bars[2], &bars[0],
@@ -897,8 +913,8 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
       cp_async_commit();
       cp_async_wait<1>();  // P box and U_0 of this brick
     }
-    __syncthreads();
-    if (TMA) {
+    if (!TMA) __syncthreads();
+    if (TMA && fix_needed<T, K, BX, BY, BZ, OCC>(true, false, G)) {
       fix_columns<T, K, BX, BY, BZ, OCC, NT>(bufA, nullptr, nullptr, sP, G);
       __syncthreads();
     }
@@ -911,8 +927,8 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
       cp_async_commit();
       cp_async_wait<1>();  // U_1
     }
-    __syncthreads();
-    if (TMA) {
+    if (!TMA) __syncthreads();
+    if (TMA && fix_needed<T, K, BX, BY, BZ, OCC>(false, false, G)) {
       fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, bufB, nullptr, nullptr, G);
       __syncthreads();
     }
@@ -925,8 +941,8 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
       cp_async_commit();
       cp_async_wait<1>();  // U_2
     }
-    __syncthreads();
-    if (TMA) {
+    if (!TMA) __syncthreads();
+    if (TMA && fix_needed<T, K, BX, BY, BZ, OCC>(false, true, G)) {
       fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, nullptr, bufA, nullptr, G);
       __syncthreads();
     }
@@ -975,10 +991,11 @@ bool tma_ok(int n, int nz) {
   if ((static_cast<int64_t>(n) * sizeof(T)) % 16 != 0) return false;
   // boxes no larger than the maps: x / y extents against n - 1 (u_y drops two rows), z against the
   // held planes nz
-  const int xy[] = {BR::UX(1), BR::UY(1), BR::UX(2), BR::UY(2), BR::PXT, BR::N(1) + H};
+  const int xy[] = {BR::UX(1), BR::UY(1), BR::UX(2), BR::UY(2), BR::PXT, BR::N(1) + H, BR::UX(0)};
   for (int e : xy)
     if (e > n - 1) return false;
-  const int zz[] = {BR::UZ(1), BR::UZ(2), BR::N(2) + H};
+  if (BR::UYS > n / BR::VEC) return false;
+  const int zz[] = {BR::UZ(0), BR::UZ(1), BR::UZ(2), BR::N(2) + H};
   for (int e : zz)
     if (e > nz) return false;
   return true;
@@ -993,8 +1010,18 @@ Maps make_maps(const LevelLayout& lay, const T* x) {
   const uint64_t es = sizeof(T);
   const uint64_t nn = static_cast<uint64_t>(lay.n);
   const uint64_t nz = static_cast<uint64_t>(lay.zhi - lay.zlo) * H;  // held z node planes
-  // maps over the held part of each block (slab-local z = global z - zlo H; the kernel shifts);
-  // u_x rows have the odd pitch n+1 (not a legal TMA stride): staged by non-tensor bulk copies
+  // maps over the held part of each block (slab-local z = global z - zlo H; the kernel shifts)
+  {  // u_x: the pitch n+1 is not a legal TMA stride, but the rows y = q (mod VEC) are: map q has base
+     // q n (16-B aligned, n % VEC == 0), x' = x + q in [0, n+1+q), rows j = (y - q) / VEC, pitch VEC (n+1)
+    constexpr int VEC = BR::VEC;
+    for (int q = 0; q < VEC; ++q) {
+      const uint64_t d[3] = {nn + 1 + q, nn / VEC, nz};
+      const uint64_t s[2] = {VEC * (nn + 1) * es, nn * (nn + 1) * es};
+      const uint32_t box[3] = {static_cast<uint32_t>(BR::UX(0)), static_cast<uint32_t>(BR::UYS),
+                               static_cast<uint32_t>(BR::UZ(0))};
+      encode<T>(&M.u0[q], x + lay.off[0] + q * nn, 3, d, s, box);
+    }
+  }
   {  // u_y: dims (x n, y n+1, z); base one row in -> y' = y - 1 in [0, n-1): the constrained rows are OOB
     const uint64_t d[3] = {nn, nn - 1, nz};
     const uint64_t s[2] = {nn * es, nn * (nn + 1) * es};
