@@ -656,9 +656,18 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
     constexpr int RPG = H / RG;
     // FULL (CTA-uniform): every row of the brick is held, none is a constrained boundary row, and the
     // brick is not the last along c -- the store predicates drop out of the interior bricks' code
+    // fewer items than threads (k = 3: 128 items for 256 threads): the velocity rows and the pressure
+    // rows of an item become separate items on disjoint threads (the pressure rows need only S)
+    // velocity items on the first PT0 threads (whole warps), pressure items on the rest. Measured
+    // (tools/ab_lib.py, C2-size levels): k = 3 fp64 -3.5 %; k = 2 neutral, k = 4 fp64 +17 % -> k = 3 only
+    constexpr int PT0 = (ITEMS + 31) / 32 * 32;
+    constexpr bool SPLIT = K == 3 && RG == 1 && PT0 < NT;
     auto pass3 = [&](auto fulltag) {
     constexpr bool FULL = decltype(fulltag)::value;
-    for (int it = tid; it < ITEMS * RG; it += NT) {
+    // MODE 0: velocity and pressure rows of the item, 1: velocity rows only, 2: pressure rows only
+    auto item = [&](const int it, auto modetag) {
+      constexpr int MODE = decltype(modetag)::value;
+      constexpr bool DOV = MODE != 2, DOP = MODE != 1;
       const int grp = it / ITEMS, it0 = it - grp * ITEMS;
       const int e0 = (it0 / NL) * S3, r = it0 % NL;
       const int oi = r % No1, oj = r / No1;
@@ -667,10 +676,10 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
 #pragma unroll
       for (int j = 0; j < W + 1; ++j) {
         s[j] = sS[base + j];
-        t[j] = sT[base + j];
+        t[j] = DOV ? sT[base + j] : T(0);
       }
 #pragma unroll
-      for (int j = 0; j < W; ++j) q[j] = sQ[base + j];
+      for (int j = 0; j < W; ++j) q[j] = DOV ? sQ[base + j] : T(0);
       int g[3];
       g[O1] = G.g0[O1] + oi;
       g[O2] = G.g0[O2] + oj;
@@ -696,15 +705,15 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
               bvel[ee * RPG + j] = T(0);
               bpre[ee * RPG + j] = T(0);
               const bool ok = FULL || (inside && gc0 + row < G.nlim[C]);
-              if (DIRECT && ok) bvel[ee * RPG + j] = bc[gbase + row * st[C]];
-              if (C == 2 && ok) bpre[ee * RPG + j] = B.c[3][pbase + row * pplane];
+              if (DOV && DIRECT && ok) bvel[ee * RPG + j] = bc[gbase + row * st[C]];
+              if (DOP && C == 2 && ok) bpre[ee * RPG + j] = B.c[3][pbase + row * pplane];
             }
         }
 #pragma unroll
         for (int ee = 0; ee < S3; ++ee) {
           const int e = e0 + ee;
 #pragma unroll
-          for (int a = A0; a < A1; ++a) {
+          for (int a = A0; a < (DOV ? A1 : A0); ++a) {
             T v = T(0), w = T(0);
 #pragma unroll
             for (int bq = 0; bq < P; ++bq) {
@@ -733,7 +742,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
           }
           // pressure rows of cell e: y_p += h^2 D S
 #pragma unroll
-          for (int i = A0; i < A1; ++i) {
+          for (int i = A0; i < (DOP ? A1 : A0); ++i) {
             T z = T(0);
 #pragma unroll
             for (int bq = 0; bq < P; ++bq) z += cref<T>(R::D + i * P + bq) * s[ee * H + H + bq];
@@ -766,11 +775,18 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         }
       }
       // the constrained plane g_c = n belongs to the brick holding the last cell along c
-      if (!FULL && grp == 0 && (C != 0 || !kStageUx) && e0 + S3 == NCc && inside && G.c0[C] + NCc >= G.mlim[C] &&
-          G.mlim[C] == m) {
+      if (DOV && !FULL && grp == 0 && (C != 0 || !kStageUx) && e0 + S3 == NCc && inside &&
+          G.c0[C] + NCc >= G.mlim[C] && G.mlim[C] == m) {
         g[C] = n;
         yc[g[0] * st[0] + g[1] * st[1] + g[2] * st[2]] = T(0);
       }
+    };
+    if constexpr (SPLIT) {
+      if (tid < ITEMS) item(tid, std::integral_constant<int, 1>());
+      else if (tid >= PT0)
+        for (int it = tid - PT0; it < ITEMS; it += NT - PT0) item(it, std::integral_constant<int, 2>());
+    } else {
+      for (int it = tid; it < ITEMS * RG; it += NT) item(it, std::integral_constant<int, 0>());
     }
     };
     // (not for fp64 k = 7: the second copy of its long, row-grouped pass-3 body measured slower)
@@ -891,8 +907,7 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
                                                           &ph[0], 2, &G);
       component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, sm, G, h, has_next ? &Gn : nullptr, X, Y, B, maps,
                                                           &bars[2], &bars[0], &ph[0], has_next ? 0 : -1, &Gn);
-      __syncthreads();
-      G = Gn;
+      G = Gn;  // (component() ends with a CTA barrier)
     }
     if (!TMA) cp_async_wait<0>();
   } else {
@@ -948,8 +963,7 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
     }
     component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, X, Y, B, maps,
                                                    &bars[2]);
-    __syncthreads();
-    G = Gn;
+    G = Gn;  // (component() ends with a CTA barrier)
     u0 ^= 1;
   }
   if (!TMA) cp_async_wait<0>();
