@@ -15,25 +15,28 @@ def line_table(obj, kernel_sub):
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=tmp, capture_output=True, check=True)
     cubins = [os.path.join(tmp, f) for f in os.listdir(tmp) if f.endswith(".cubin")]
+    found = []
     for cb in cubins:
         dis = subprocess.run(["nvdisasm", "-g", "-c", cb], capture_output=True, text=True).stdout
         # split per function
         funcs = re.split(r"\n\s*\.text\.(\S+):", dis)
         for i in range(1, len(funcs), 2):
-            name, body = funcs[i], funcs[i + 1]
-            if kernel_sub not in name:
-                continue
-            table, cur = {}, None
-            for ln in body.splitlines():
-                m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
-                if m:
-                    cur = (os.path.basename(m.group(1)), int(m.group(2)))
-                    continue
-                m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
-                if m and cur:
-                    table[int(m.group(1), 16)] = cur
-            return name, table
-    raise SystemExit("kernel not found in " + obj)
+            if kernel_sub in funcs[i]:
+                found.append((funcs[i], funcs[i + 1]))
+    if len(found) != 1:
+        # a substring matching several instantiations would attribute with the wrong line table
+        raise SystemExit(f"{len(found)} functions match {kernel_sub!r}: " + ", ".join(n for n, _ in found))
+    name, body = found[0]
+    table, cur = {}, None
+    for ln in body.splitlines():
+        m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
+        if m:
+            cur = (os.path.basename(m.group(1)), int(m.group(2)))
+            continue
+        m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
+        if m and cur:
+            table[int(m.group(1), 16)] = cur
+    return name, table
 
 
 def main():
