@@ -1134,7 +1134,9 @@ void launch_t(Context& ctx, int level, const VmultArgs& a) {
 template <typename T, int K> struct BrickShape;
 // NT: threads per CTA; OCC: resident CTAs per SM (persistent grid of OCC x #SMs, __launch_bounds__(NT, OCC))
 template <typename T> struct BrickShape<T, 1> { static constexpr int X = 8, Y = 4, Z = 4, NT = 256, OCC = 2; };
-template <typename T> struct BrickShape<T, 2> { static constexpr int X = 4, Y = 4, Z = 2, NT = 256, OCC = 2; };
+// k=2: 4x4x4 cells, 384 threads, one CTA per SM (round 2: after the u_x tensor-map staging this shape
+// beat the round-1 4x4x2 / 256 / 2-CTA default, 0.274 vs 0.295 ms at C2 fp64, tools/tune_k2.sh)
+template <typename T> struct BrickShape<T, 2> { static constexpr int X = 4, Y = 4, Z = 4, NT = 384, OCC = 1; };
 template <typename T> struct BrickShape<T, 3> { static constexpr int X = 4, Y = 2, Z = 2, NT = 256, OCC = 1; };
 template <typename T> struct BrickShape<T, 4> { static constexpr int X = 2, Y = 2, Z = 2, NT = 384, OCC = 1; };
 template <> struct BrickShape<double, 5> { static constexpr int X = 2, Y = 1, Z = 1, NT = 256, OCC = 1; };
@@ -1187,6 +1189,11 @@ struct Variants<2> {
       case 7: launch_shape<T, 2, Shape<8, 4, 2, 384, 1>>(ctx, level, a); return true;
       case 8: launch_shape<T, 2, Shape<4, 4, 4, 384, 1>>(ctx, level, a); return true;
       case 9: launch_shape<T, 2, Shape<4, 4, 2, 320, 2>>(ctx, level, a); return true;
+      case 10: launch_shape<T, 2, Shape<4, 4, 4, 320, 1>>(ctx, level, a); return true;
+      case 11: launch_shape<T, 2, Shape<4, 4, 4, 448, 1>>(ctx, level, a); return true;
+      case 12: launch_shape<T, 2, Shape<4, 4, 4, 256, 1>>(ctx, level, a); return true;
+      case 13: launch_shape<T, 2, Shape<4, 4, 4, 576, 1>>(ctx, level, a); return true;
+      case 14: launch_shape<T, 2, Shape<4, 4, 2, 256, 2>>(ctx, level, a); return true;  // round-1 default
       default: return false;
     }
   }

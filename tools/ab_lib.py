@@ -1,7 +1,7 @@
 """A/B timing of two builds of libsmg_b200.so on the same box: the candidate (in-tree) and a baseline copy
 (ab/base.so, git-ignored scratch). Each measurement runs in a fresh process with the chosen library copied
 in place; the in-tree candidate is restored at the end.
-Usage: python tools/ab_lib.py [vmult|smooth] [k:level ...]   (default: vmult 2:5 1:5 3:5 4:4)"""
+Usage: python tools/ab_lib.py [vmult|smooth|e2e] [k:level ...]   (default: vmult 2:5 1:5 3:5 4:4)"""
 import json
 import os
 import shutil
@@ -14,11 +14,27 @@ BASE = os.path.join(ROOT, "ab", "base.so")
 CAND = os.path.join(ROOT, "ab", "cand.so")
 
 CHILD = r"""
-import json, sys, torch
+import json, sys, time, torch
 sys.path.insert(0, %r)
 import paper_2410_09497_b200 as smg
 what, k, level = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 out = {}
+if what == "e2e":  # host BlockVector apply (pinned), wall time per call
+    import numpy as np
+    ctx = smg.Context(k, level)
+    s = ctx.sizes(level)
+    xb = [torch.empty(s[i], dtype=torch.float64, pin_memory=True).numpy() for i in range(4)]
+    yb = [torch.empty(s[i], dtype=torch.float64, pin_memory=True).numpy() for i in range(4)]
+    for a in xb:
+        a[:] = np.random.default_rng(0).standard_normal(a.size)
+    for _ in range(3):
+        ctx.vmult_host(level, xb, smg.F64, out=yb)
+    t0 = time.perf_counter()
+    for _ in range(30):
+        ctx.vmult_host(level, xb, smg.F64, out=yb)
+    t = (time.perf_counter() - t0) / 30
+    print(json.dumps({"f64": {"ms": round(t * 1e3, 3), "gdofs": round(s[4] / t / 1e9, 3)}}))
+    sys.exit(0)
 for name, dt in (("f64", torch.float64), ("f32", torch.float32)):
     if what == "smooth" and name == "f64":
         continue
@@ -57,7 +73,7 @@ def run(lib, what, k, level):
 
 
 def main():
-    what = sys.argv[1] if len(sys.argv) > 1 and sys.argv[1] in ("vmult", "smooth") else "vmult"
+    what = sys.argv[1] if len(sys.argv) > 1 and sys.argv[1] in ("vmult", "smooth", "e2e") else "vmult"
     cases = [a for a in sys.argv[1:] if ":" in a] or ["2:5", "1:5", "3:5", "4:4"]
     shutil.copyfile(LIB, CAND)
     try:
