@@ -1171,6 +1171,10 @@ struct Variants<1> {
       case 2: launch_shape<T, 1, Shape<4, 4, 4, 256, 2>>(ctx, level, a); return true;
       case 3: launch_shape<T, 1, Shape<8, 4, 4, 256, 2>>(ctx, level, a); return true;
       case 4: launch_shape<T, 1, Shape<8, 8, 2, 256, 2>>(ctx, level, a); return true;
+      case 5: launch_shape<T, 1, Shape<8, 8, 4, 384, 1>>(ctx, level, a); return true;
+      case 6: launch_shape<T, 1, Shape<8, 4, 4, 384, 1>>(ctx, level, a); return true;
+      case 7: launch_shape<T, 1, Shape<8, 8, 4, 512, 1>>(ctx, level, a); return true;
+      case 8: launch_shape<T, 1, Shape<8, 4, 8, 384, 1>>(ctx, level, a); return true;
       default: return false;
     }
   }
@@ -1207,6 +1211,10 @@ struct Variants<3> {
       case 2: launch_shape<T, 3, Shape<4, 2, 2, 256, 1>>(ctx, level, a); return true;
       case 3: launch_shape<T, 3, Shape<4, 2, 2, 384, 1>>(ctx, level, a); return true;
       case 4: launch_shape<T, 3, Shape<4, 2, 1, 256, 2>>(ctx, level, a); return true;
+      case 5: launch_shape<T, 3, Shape<4, 4, 1, 384, 1>>(ctx, level, a); return true;
+      case 6: launch_shape<T, 3, Shape<4, 4, 1, 256, 1>>(ctx, level, a); return true;
+      case 7: launch_shape<T, 3, Shape<2, 2, 4, 384, 1>>(ctx, level, a); return true;
+      case 8: launch_shape<T, 3, Shape<2, 4, 2, 384, 1>>(ctx, level, a); return true;
       default: return false;
     }
   }
@@ -1220,6 +1228,8 @@ struct Variants<4> {
       case 2: launch_shape<T, 4, Shape<2, 2, 1, 256, 2>>(ctx, level, a); return true;
       case 3: launch_shape<T, 4, Shape<4, 2, 1, 256, 1>>(ctx, level, a); return true;
       case 4: launch_shape<T, 4, Shape<2, 2, 2, 512, 1>>(ctx, level, a); return true;
+      case 5: launch_shape<T, 4, Shape<4, 2, 1, 384, 1>>(ctx, level, a); return true;
+      case 6: launch_shape<T, 4, Shape<2, 2, 2, 320, 1>>(ctx, level, a); return true;
       default: return false;
     }
   }
