@@ -106,7 +106,7 @@ struct Brick {
   // TMA (measured on B200, tools/tma_test.cu) needs the x start of a box 16-B aligned and >= 0 and the
   // shared-memory destination 128-B aligned. Every row is loaded from the 16-B aligned position at or
   // below the needed start (clamped to 0); UX carries VEC-1 elements of slack and the consumers add
-  // the per-brick shift PADF + x0 - xs (per-row shift for the u_x rows, which are bulk copies).
+  // the per-brick shift PADF + x0 - xs (per sub-box shift for the u_x rows, u0_row).
   static constexpr int XEXT(int c) { return c == 0 ? LC(0) : LO1H(c); }
   static constexpr int UX(int c) { return rup(XEXT(c) + VEC - 1); }
   static constexpr int UY(int c) { return c == 0 ? LO1H(0) : (c == 1 ? LC(1) : LO2H(2)); }
@@ -218,14 +218,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const CUtensorMap* map, i
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(smem_u32(bar))
       : "memory");
-}
-
-// non-tensor bulk copy global -> shared (16-B aligned addresses, size multiple of 16 B)
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
 }
 
 // floor to a multiple of the power of two q (two's complement: also right for negative v)
