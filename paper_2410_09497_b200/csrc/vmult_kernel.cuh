@@ -550,13 +550,13 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
 #pragma unroll
         for (int j = 0; j < (S1 + 2) * H; ++j) in[j] = src[j * US];
         // the pressure column of Q2 below is loaded up front (its latency overlaps the SIPG rows; the
-        // compiler cannot move loads above the sB1 stores). For the one column that skips Q2 (C = 1, 2:
-        // ci = Nc + H) the address lies past the P box, still inside the CTA's shared memory, and the
-        // values are not used.
+        // compiler cannot move loads above the sB1 stores); predicated off for the one column that
+        // skips Q2 (C = 1, 2: ci = Nc + H, past the P box)
+        const bool useq = (C == 0 && K <= 5) || ci < Nc + H;
         const T* ps = sP + psh + ci * PSC + (o + H) * PSO1 + (e2 + 1) * H * PSO2;
         T pc[S1 * H];
 #pragma unroll
-        for (int j = 0; j < S1 * H; ++j) pc[j] = ps[j * PSO2];
+        for (int j = 0; j < S1 * H; ++j) pc[j] = useq ? ps[j * PSO2] : T(0);
         const int eg = cell_o2 + e2;  // global cell of the segment's first cell
         seg_sipg<T, K, S1, BND>(in, out, eg == 0 ? 0 : -1, (m - 1 - eg < S1) ? m - 1 - eg : -1);
 #pragma unroll
@@ -564,7 +564,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         // Q2 = M_o2 p at the same (c, o1, o2-segment); the P box has the same origin. C = 0 walks c
         // fastest, so the last c column (never read as Q) is computed from the P box's pad column rather
         // than branched around in every warp
-        if ((C == 0 && K <= 5) || ci < Nc + H) {  // (k >= 6: the extra column costs more than the branch)
+        if (useq) {  // (k >= 6: the extra column costs more than the branch)
           T q2[S1 * H];
           seg_mass<T, K, S1>(pc, q2);
 #pragma unroll
@@ -605,11 +605,12 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
         for (int j = 0; j < (S2 + 2) * H; ++j) in[j] = a1[j * PC];
 #pragma unroll
         for (int j = 0; j < S2 * H; ++j) bb[j] = b1[j * PC];
-        // Q2 of this item loaded up front (see pass 1); for the skipped column the values are not used
+        // Q2 of this item loaded up front (see pass 1; predicated off for the column that skips Q)
+        const bool useq = K <= 5 || ci < Nc + H;
         T* q = sQ + (oj * No1 + e1 * H) * PC + ci;
         T q2[S2 * H];
 #pragma unroll
-        for (int j = 0; j < S2 * H; ++j) q2[j] = q[j * PC];
+        for (int j = 0; j < S2 * H; ++j) q2[j] = useq ? q[j * PC] : T(0);
         T cu[S2 * H];
 #pragma unroll
         for (int j = 0; j < S2 * H; ++j) cu[j] = in[H + j];
@@ -623,7 +624,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
           sS[(oj * No1 + e1 * H + a) * PC + ci] = sv[a];
           sT[(oj * No1 + e1 * H + a) * PC + ci] = tv[a] + mb[a];
         }
-        if (K <= 5 || ci < Nc + H) {  // Q = M_o1 Q2 in place (last c column never read as Q, see pass 1)
+        if (useq) {  // Q = M_o1 Q2 in place (last c column never read as Q, see pass 1)
           T qq[S2 * H];
           seg_mass<T, K, S2>(q2, qq);
 #pragma unroll
