@@ -252,7 +252,15 @@ void vcycle_graph(Context& c, int level, int prec, void* vx, const void* vb) {
     c.vgraph_launches[prec][level] = c.launches - l0;
     if (c.tmap_pinned.size() != static_cast<size_t>(kTmapSlots)) c.tmap_pinned.assign(kTmapSlots, false);
     for (int slot : c.tmap_recorded) c.tmap_pinned[slot] = true;  // the graph holds their addresses
-    c.launches -= c.vgraph_launches[prec][level];  // counted on every replay below
+    c.launches -= c.vgraph_launches[prec][level];  // counted on every replay
+    // the warm-up cycle already produced this call's result (the capture executes nothing); order
+    // the caller's stream after it and replay from the next call on
+    cudaEvent_t done;
+    SMG_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    SMG_CUDA(cudaEventRecord(done, c.s_capture));
+    SMG_CUDA(cudaStreamWaitEvent(c.stream, done, 0));
+    cudaEventDestroy(done);
+    return;
   }
   SMG_CUDA(cudaGraphLaunch(ge, c.stream));
   c.launches += c.vgraph_launches[prec][level];

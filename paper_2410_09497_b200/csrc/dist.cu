@@ -426,10 +426,7 @@ void vcycle_maybe_graph(Context& c, int prec, void* vx, const void* vb) {
     }
     if (g) cudaGraphDestroy(g);
     c.launches = l0;
-    if (D.graph_failed) {
-      vcycle(c, D.L, prec, vx, vb);
-      return;
-    }
+    return;  // the warm-up cycle already produced this call's result (the capture executes nothing)
   }
   SMG_CUDA(cudaGraphLaunch(D.vgraph[prec], c.stream));
   c.launches += D.vgraph_launches[prec];
