@@ -85,6 +85,11 @@ __device__ __forceinline__ void cp_async_wait() {
 // ---------------------------------------------------------------------------------------------
 // brick geometry
 // ---------------------------------------------------------------------------------------------
+// QDB (default on where it fits): second Q buffer and no CTA barrier after pass 3 (the last warp to
+// finish its pass-3 reads issues the next staging into the component's U buffer)
+#ifndef SMG_VMULT_QDB
+#define SMG_VMULT_QDB 1
+#endif
 template <typename T, int K, int BX, int BY, int BZ, int OCC>
 struct Brick {
   static constexpr int H = K + 1;
@@ -141,8 +146,16 @@ struct Brick {
   // single-buffered "early release" layout: [U][P][A1][B1=T][Q][YP][S]; U is dead after pass 1, so the
   // next component's staging is issued there and overlaps passes 2-3 and the next Q passes
   static constexpr size_t bytes_sb() { return rup16(static_cast<size_t>(U + PBUF + A1 + 3 * ST + YP) * sizeof(T)); }
-  static constexpr size_t bytes_for(int nbuf) { return nbuf == 2 ? bytes_db() : bytes_sb(); }
+  // double-buffered layout + a second Q buffer (QDB): pass 3 of component c reads Q while pass 1 of
+  // component c+1 writes its Q2 into the other buffer, so no CTA barrier is needed after pass 3
+  static constexpr size_t bytes_dbq() {
+    return rup16(static_cast<size_t>(2 * U + PBUF + A1 + 3 * ST + YP + (ALIAS ? 0 : 2 * ST)) * sizeof(T));
+  }
   static constexpr bool DB = bytes_db() <= kSmemCap;
+  // measured (tools/ab_lib.py, profiles/r02/ab_vmult_qdb.jsonl): k = 2 fp64 -2.1 %, k = 3 -1.1 %; k = 1 fp32
+  // +3 %, k = 4 fp64 +4 % -> k = 2, 3 only
+  static constexpr bool QDB = SMG_VMULT_QDB && (K == 2 || K == 3) && DB && bytes_dbq() <= kSmemCap;
+  static constexpr size_t bytes_for(int nbuf) { return nbuf == 2 ? (QDB ? bytes_dbq() : bytes_db()) : bytes_sb(); }
   static constexpr int OFF_U1 = DB ? U : 0;
   static constexpr int OFF_P = (DB ? 2 : 1) * U;
   static constexpr int OFF_A1 = OFF_P + PBUF;
@@ -150,7 +163,8 @@ struct Brick {
   static constexpr int OFF_Q = OFF_B1 + ST;
   static constexpr int OFF_YP = OFF_Q + ST;
   static constexpr int OFF_ST = OFF_YP + YP;  // DB && !ALIAS: S, T; SB: S
-  static constexpr int END = DB ? OFF_YP + YP + (ALIAS ? 0 : 2 * ST) : OFF_YP + YP + ST;
+  static constexpr int OFF_Q2 = OFF_ST + (ALIAS ? 0 : 2 * ST);  // QDB: second Q buffer
+  static constexpr int END = DB ? OFF_Q2 + (QDB ? ST : 0) : OFF_YP + YP + ST;
   static constexpr size_t BYTES = (static_cast<size_t>(END) * sizeof(T) + 15) / 16 * 16 + 3 * 8;
   static_assert(BYTES == bytes_for(DB ? 2 : 1), "smem layout");
   static constexpr int stride(int axis, int a0, int a1) { return axis == 0 ? 1 : (axis == 1 ? a0 : a0 * a1); }
@@ -250,7 +264,9 @@ __device__ __forceinline__ int u0_row(const Geo& G, int H, int oi) {
 // staging: TMA (default) or cp.async element copies (fallback when a pitch is not 16-B aligned,
 // i.e. fp32 on level 0 with even k). Both write the same TMA box layout.
 // ---------------------------------------------------------------------------------------------
-template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, int C, bool TMA>
+// SINGLE: called by one thread (QDB: the U barriers then count one arrival, the issuer's expect_tx);
+// otherwise called by every thread and thread 0 issues while the other warps arrive once each
+template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, int C, bool TMA, bool SINGLE = false>
 __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const T>& X, const Maps& M, const Geo& G) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   constexpr int H = K + 1;
@@ -261,7 +277,7 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
     if constexpr (C == 0) {
       // VEC sub-boxes from the row-residue maps u0[q] (Brick::SUB0); rows / planes outside the domain
       // are OOB-filled with zeros, the columns x <= 0 and x >= n are zeroed by fix_columns
-      if (tid == 0) {
+      if (SINGLE || tid == 0) {
         constexpr int VEC = BR::VEC;
         mbar_expect(bar, static_cast<unsigned>(VEC * UX * BR::UYS * UZ * sizeof(T)));
         const int y0 = G.g0[1] - H, x0 = G.g0[0] - H, zc = G.g0[2] - H - G.zoff;
@@ -276,7 +292,7 @@ __device__ __forceinline__ void issue_u(T* sU, uint64_t* bar, const Blocks<const
         mbar_arrive(bar);  // the U barriers count one arrival per warp
       }
     } else {
-      if (tid == 0) {
+      if (SINGLE || tid == 0) {
         mbar_expect(bar, static_cast<unsigned>(BR::sizeU(C) * sizeof(T)));
         // the u_y map starts one row in, so its constrained rows 0 and n fall outside
         const int xs = max(floor_to(G.g0[0] - H, BR::VEC), 0);
@@ -467,7 +483,7 @@ template <typename T, int K, int BX, int BY, int BZ, int OCC, int NT, int C, boo
 __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const Geo* Gn, const Blocks<const T>& X,
                                           const Blocks<T>& Y, const Blocks<const T>& B, const Maps& M, uint64_t* barP,
                                           uint64_t* barU = nullptr, unsigned* phU = nullptr, int nextC = -1,
-                                          const Geo* Gnext = nullptr) {
+                                          const Geo* Gnext = nullptr, int qsel = 0) {
   using BR = Brick<T, K, BX, BY, BZ, OCC>;
   using R = Ref<K>;
   constexpr int H = K + 1, P = K + 2;
@@ -484,7 +500,7 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
 
   T* sA1 = sm + BR::OFF_A1;
   T* sB1 = sm + BR::OFF_B1;
-  T* sQ = sm + BR::OFF_Q;
+  T* sQ = sm + (BR::QDB && qsel ? BR::OFF_Q2 : BR::OFF_Q);
   T* sP = sm + BR::OFF_P;
   T* sYP = sm + BR::OFF_YP;
   T* sS = (BR::DB && BR::ALIAS) ? sU : sm + BR::OFF_ST;
@@ -818,8 +834,26 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       }
     }
   }
-  fence_proxy_async();  // generic reads of this U buffer happen-before the next TMA into it
-  __syncthreads();
+  if constexpr (!(BR::QDB && TMA)) {  // (QDB: last_warp_done in the caller)
+    fence_proxy_async();  // generic reads of this U buffer happen-before the next TMA into it
+    __syncthreads();
+  }
+}
+
+// QDB release of a component's U buffer: every warp arrives once its pass-3 reads are done; true in
+// lane 0 of the last warp to arrive, which then issues the next staging into the buffer. The other
+// warps go straight on to the next component (its U box was issued one component earlier).
+template <int NT>
+__device__ __forceinline__ bool last_warp_done(unsigned* cnt) {
+  __syncwarp();
+  bool last = false;
+  if ((threadIdx.x & 31) == 0) {
+    fence_proxy_async();  // this warp's generic reads of the buffer before the async-proxy writes
+    __threadfence_block();
+    last = atomicInc(cnt, NT / 32 - 1) == NT / 32 - 1;  // wraps to 0 for the next release
+    if (last) __threadfence_block();
+  }
+  return last;
 }
 
 __device__ __forceinline__ void brick_geo(Geo& G, int brick, int lnbx, int lnby, int bx, int by, int bz, int H,
@@ -868,9 +902,12 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
   const Maps& maps = *mapsp;  // tensor maps live in global memory (64-B aligned slots)
   int brick = blockIdx.x;
   if (brick >= nbricks) return;
+  constexpr bool QB = BR::QDB && TMA;  // barrier-free pass-3 release (TMA staging only)
+  __shared__ unsigned rel_cnt;          // QB: warps done with the current component's pass 3
   if (TMA && threadIdx.x == 0) {
-    mbar_init(&bars[0], NT / 32);  // U buffers: one arrival per warp (issue_u)
-    mbar_init(&bars[1], NT / 32);
+    rel_cnt = 0;
+    mbar_init(&bars[0], QB ? 1 : NT / 32);  // U buffers: the issuer (QB) or one arrival per warp (issue_u)
+    mbar_init(&bars[1], QB ? 1 : NT / 32);
     mbar_init(&bars[2], 1);        // P box: thread 0
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -878,7 +915,11 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
   __syncthreads();
   brick_geo(G, brick, lnbx, lnby, BX, BY, BZ, H, zc0);
   issue_p<T, K, BX, BY, BZ, OCC, NT, TMA>(sP, &bars[2], X, maps, G);
-  issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sm, &bars[0], X, maps, G);
+  if constexpr (QB) {
+    if (threadIdx.x == 0) issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA, true>(sm, &bars[0], X, maps, G);
+  } else {
+    issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA>(sm, &bars[0], X, maps, G);
+  }
   if (!TMA) cp_async_commit();
   int u0 = 0;
   unsigned ph[2] = {0, 0}, phP = 0;  // mbarrier phase of buffer 0 / 1 / P
@@ -910,6 +951,55 @@ __global__ void __launch_bounds__(NT, OCC) stokes_vmult_kernel(const Blocks<cons
       G = Gn;  // (component() ends with a CTA barrier)
     }
     if (!TMA) cp_async_wait<0>();
+  } else if constexpr (QB) {
+    // two U buffers, two Q buffers, no CTA barrier after pass 3: the last warp done with a component's
+    // pass 3 issues the staging that reuses its U buffer (component c + 2 in brick order)
+    if (threadIdx.x == 0) issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA, true>(sm + BR::OFF_U1, &bars[1], X, maps, G);
+    int q = 0;
+    for (; brick < nbricks; brick += gridDim.x) {
+      const int ia = u0, ib = u0 ^ 1;
+      T* bufA = sm + (ia ? BR::OFF_U1 : 0);  // components 0 and 2 of this brick, then 1 of the next
+      T* bufB = sm + (ib ? BR::OFF_U1 : 0);  // component 1, then component 0 of the next brick
+      const int next = brick + gridDim.x;
+      const bool has_next = next < nbricks;
+      if (has_next) brick_geo(Gn, next, lnbx, lnby, BX, BY, BZ, H, zc0);
+      mbar_wait(&bars[2], phP);
+      phP ^= 1;
+      mbar_wait(&bars[ia], ph[ia]);
+      ph[ia] ^= 1;
+      if (fix_needed<T, K, BX, BY, BZ, OCC>(true, false, G)) {
+        fix_columns<T, K, BX, BY, BZ, OCC, NT>(bufA, nullptr, nullptr, sP, G);
+        __syncthreads();
+      }
+      component<T, K, BX, BY, BZ, OCC, NT, 0, RESID, TMA>(sm, bufA, G, h, nullptr, X, Y, B, maps, &bars[2], nullptr,
+                                                          nullptr, -1, nullptr, q);
+      q ^= 1;
+      if (last_warp_done<NT>(&rel_cnt)) issue_u<T, K, BX, BY, BZ, OCC, NT, 2, TMA, true>(bufA, &bars[ia], X, maps, G);
+      mbar_wait(&bars[ib], ph[ib]);
+      ph[ib] ^= 1;
+      if (fix_needed<T, K, BX, BY, BZ, OCC>(false, false, G)) {
+        fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, bufB, nullptr, nullptr, G);
+        __syncthreads();
+      }
+      component<T, K, BX, BY, BZ, OCC, NT, 1, RESID, TMA>(sm, bufB, G, h, nullptr, X, Y, B, maps, &bars[2], nullptr,
+                                                          nullptr, -1, nullptr, q);
+      q ^= 1;
+      if (last_warp_done<NT>(&rel_cnt) && has_next)
+        issue_u<T, K, BX, BY, BZ, OCC, NT, 0, TMA, true>(bufB, &bars[ib], X, maps, Gn);
+      mbar_wait(&bars[ia], ph[ia]);
+      ph[ia] ^= 1;
+      if (fix_needed<T, K, BX, BY, BZ, OCC>(false, true, G)) {
+        fix_columns<T, K, BX, BY, BZ, OCC, NT>(nullptr, nullptr, bufA, nullptr, G);
+        __syncthreads();
+      }
+      component<T, K, BX, BY, BZ, OCC, NT, 2, RESID, TMA>(sm, bufA, G, h, has_next ? &Gn : nullptr, X, Y, B, maps,
+                                                          &bars[2], nullptr, nullptr, -1, nullptr, q);
+      q ^= 1;
+      if (last_warp_done<NT>(&rel_cnt) && has_next)
+        issue_u<T, K, BX, BY, BZ, OCC, NT, 1, TMA, true>(bufA, &bars[ia], X, maps, Gn);
+      G = Gn;
+      u0 ^= 1;
+    }
   } else {
   for (; brick < nbricks; brick += gridDim.x) {
     const int ia = u0, ib = u0 ^ 1;
