@@ -346,3 +346,19 @@ print(worst)
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root, timeout=600)
     assert out.returncode == 0, out.stderr
     assert float(out.stdout.strip().splitlines()[-1]) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunks", ["4", "3", "2", "8", "16"])
+def test_vmult_host_pipeline_chunkings(chunks, monkeypatch):
+    # the host pipeline overlaps z-chunk copies with the operator rows of the resident chunks: every
+    # chunking (SMG_HOST_CHUNKS, read per call) must give the device operator's result
+    k, level = 2, 4
+    monkeypatch.setenv("SMG_HOST_CHUNKS", chunks)
+    ctx = smg.Context(k, level)
+    x = rand_vec(k, level, 21)
+    y_dev = ctx.apply_stokes(level, torch.from_numpy(x).cuda()).cpu().numpy()
+    ys = ctx.vmult_host(level, smg.to_blockvector(x, k, level))
+    assert rel(smg.from_blockvector(ys, k, level), y_dev) <= 1e-14
+    if chunks == "4":
+        assert rel(smg.from_blockvector(ys, k, level), oracle.apply_stokes(k, level, x)) <= 1e-12
