@@ -153,7 +153,7 @@ struct Brick {
   }
   static constexpr bool DB = bytes_db() <= kSmemCap;
   // measured (tools/ab_lib.py, profiles/r02/ab_vmult_qdb.jsonl): k = 2 fp64 -2.1 %, k = 3 -1.1 %; k = 1 fp32
-  // +3 %, k = 4 fp64 +4 % -> k = 2, 3 only
+  // +3 %, k = 4 fp64 +4 %, k = 5 / 6 fp64 +20 % (ab_vmult_qdb_high_degree.jsonl) -> k = 2, 3 only
   static constexpr bool QDB = SMG_VMULT_QDB && (K == 2 || K == 3) && DB && bytes_dbq() <= kSmemCap;
   static constexpr size_t bytes_for(int nbuf) { return nbuf == 2 ? (QDB ? bytes_dbq() : bytes_db()) : bytes_sb(); }
   static constexpr int OFF_U1 = DB ? U : 0;

@@ -362,3 +362,18 @@ def test_vmult_host_pipeline_chunkings(chunks, monkeypatch):
     assert rel(smg.from_blockvector(ys, k, level), y_dev) <= 1e-14
     if chunks == "4":
         assert rel(smg.from_blockvector(ys, k, level), oracle.apply_stokes(k, level, x)) <= 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,dtype,tol", [(5, "f64", 1e-12), (6, "f64", 1e-12), (7, "f64", 1e-12), (5, "f32", 1e-5),
+                                         (7, "f32", 1e-5)])
+def test_vmult_high_degree_tma_path_matches_oracle(k, dtype, tol):
+    # level 3 (8^3 cells) is the smallest level whose boxes take the TMA staging path at k >= 5 (level <= 2
+    # runs the cp.async fallback): the persistent multi-brick pipeline at high degree against the oracle
+    level = 3
+    ctx = smg.Context(k, level)
+    x = rand_vec(k, level, 5)
+    y_ref = oracle.apply_stokes(k, level, x)
+    t = torch.float64 if dtype == "f64" else torch.float32
+    y = ctx.apply_stokes(level, dev(x, t)).double().cpu().numpy()
+    assert rel(y, y_ref) <= tol
