@@ -458,6 +458,10 @@ using bool_c = std::integral_constant<bool, V>;
 #define SMG_STAGE_UX 0
 #endif
 constexpr bool kStageUx = SMG_STAGE_UX;
+#ifndef SMG_VMULT_WIDE_A
+#define SMG_VMULT_WIDE_A 1
+#endif
+constexpr bool kWideA = SMG_VMULT_WIDE_A;  // component(): AWIDE
 // cells per work item along a brick axis of nc cells: segments of 2 cells for low degrees (shared
 // neighbour loads, fewer index computations), single cells otherwise
 constexpr int seg_cells(int nc, int k) { return (nc % 2 == 0 && k <= 3) ? 2 : 1; }
@@ -539,18 +543,24 @@ __device__ __forceinline__ void component(T* sm, T* sU, const Geo& G, T h, const
       return C == 0 ? u0_row<T, BR::SUB0, UX>(G, H, oi) + ci : (C == 1 ? ci * UX + oi : ci * UY * UX + oi) + bsh;
     };
     constexpr int NLA = LC * LO1H;
-    for (int it = tid; it < NLA * (NO2 / S1); it += NT) {
-      const int e2 = (it / NLA) * S1, r = it % NLA;
+    // SA: cells per A item. QDB k = 2 fp64: whole 4-cell o2 lines (288 items, one per thread, more
+    // independent loads per item) handed out from the top thread down, so that threads 96..383 take them
+    // and the threads 288..383 without a pass-3 item of the previous component start on them at once.
+    // Measured (ab_vmult_qdb_wide_a.jsonl): C2 fp64 -1.3 % on top of QDB; fp32 at 32^3 +5 % -> fp64 only
+    constexpr bool AWIDE = kWideA && BR::QDB && TMA && K == 2 && sizeof(T) == 8 && NO2 == 4 && NLA * (NO2 / 4) <= NT;
+    constexpr int SA = AWIDE ? 4 : S1;
+    for (int it = AWIDE ? NT - 1 - tid : tid; it < NLA * (NO2 / SA); it += NT) {
+      const int e2 = (it / NLA) * SA, r = it % NLA;
       // consecutive items walk the staged box's x axis: c for C=0, o1 for C=1,2
       const int ci = C == 0 ? r % LC : r / LO1H;
       const int oi = C == 0 ? r / LC : r % LO1H;
       const T* src = sU + ub(ci, oi) + (e2 + 1) * H * US;
-      T cu[S1 * H], out[S1 * H];
+      T cu[SA * H], out[SA * H];
 #pragma unroll
-      for (int j = 0; j < S1 * H; ++j) cu[j] = src[j * US];
-      seg_mass<T, K, S1>(cu, out);
+      for (int j = 0; j < SA * H; ++j) cu[j] = src[j * US];
+      seg_mass<T, K, SA>(cu, out);
 #pragma unroll
-      for (int a = 0; a < S1 * H; ++a) sA1[((e2 * H + a) * LO1H + oi) * PC + ci] = out[a];
+      for (int a = 0; a < SA * H; ++a) sA1[((e2 * H + a) * LO1H + oi) * PC + ci] = out[a];
     }
     const int cell_o2 = G.c0[O2];
     const int psh = brick_shift<T>(G, H);
