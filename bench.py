@@ -32,7 +32,7 @@ METRIC = "Stokes operator-apply DoF/s (fp64), RT_2 64^3 cells; + fp32 smoother D
 
 
 # brick shapes of the operator kernel per degree (fp64), csrc/vmult_kernel.cuh BrickShape
-SHAPES = {1: "8x4x4-cell bricks, 2 CTAs/SM, 256 threads", 2: "4x4x4-cell bricks, 1 CTA/SM, 384 threads, two U buffers",
+SHAPES = {1: "8x4x4-cell bricks, 2 CTAs/SM, 256 threads", 2: "4x4x4-cell bricks, 1 CTA/SM, 384 threads, two U and two Q buffers, no barrier after pass 3",
           3: "4x2x2-cell bricks, 1 CTA/SM, 256 threads", 4: "2x2x2-cell bricks, 384 threads"}
 
 
